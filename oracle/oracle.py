@@ -1,0 +1,318 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes binding of the CPU oracle (oracle/_build/liboracle.so).
+
+The oracle restates the reference's hot path on the CPU (see tlsph_oracle.hpp).
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl
+reference) may import this module, and only as the checker or the CPU
+baseline. The product package never imports it.
+
+Arrays are numpy float64 in reference particle order: vectors (n, D),
+matrices (n, D, D) row-major.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+_lib = None
+
+FIELDS = {"r0": 0, "r": 1, "v": 2, "a": 3, "F": 4, "dFdt": 5, "B0": 6, "V0": 7, "m": 8,
+          "rho0": 9, "rho": 10, "body": 11, "constrained": 12}
+_VEC = {"r0", "r", "v", "a", "body"}
+_MAT = {"F", "dFdt", "B0"}
+
+SCHEMES = {"explicit": 0, "particle_split": 1, "pairwise_split": 2}
+
+ERROR_KINDS = {1: "invalid-argument", 2: "parse-error", 3: "degenerate-geometry",
+               4: "inverted-element", 5: "numerical-failure", 6: "io-error", 7: "internal-error"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{ERROR_KINDS.get(status, status)}: {message}")
+        self.status = status
+        self.kind = ERROR_KINDS.get(status, str(status))
+        self.message = message
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = C.CDLL(_LIB_PATH)
+        P = C.c_void_p
+        D = C.POINTER(C.c_double)
+        I = C.c_int
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_create.argtypes = [I, C.c_size_t, D, D, D, C.POINTER(C.c_ubyte), C.c_double, I, C.POINTER(P)]
+        L.orc_destroy.argtypes = [P]
+        L.orc_size.argtypes = [P]
+        L.orc_size.restype = C.c_size_t
+        L.orc_set_field.argtypes = [P, I, D]
+        L.orc_get_field.argtypes = [P, I, D]
+        L.orc_set_material.argtypes = [P, C.c_double, C.c_double, C.c_double, I]
+        L.orc_material.argtypes = [C.c_double, C.c_double, C.c_double, I, D]
+        L.orc_grid_info.argtypes = [P, C.POINTER(I), D, D, C.POINTER(C.c_longlong)]
+        L.orc_grid_cells.argtypes = [P, C.POINTER(I), C.POINTER(C.c_longlong), C.POINTER(I)]
+        L.orc_blocks.argtypes = [P, C.POINTER(C.c_longlong), C.POINTER(I)]
+        L.orc_slot_count.argtypes = [P]
+        L.orc_slot_count.restype = C.c_longlong
+        L.orc_get_neighborhood.argtypes = [P, C.POINTER(C.c_longlong), C.POINTER(I), D, D, D, D]
+        L.orc_set_neighborhood.argtypes = [P, C.POINTER(C.c_longlong), C.POINTER(I), D, D, D, D]
+        for name in ("orc_correction_matrices", "orc_deformation_rate", "orc_update_density",
+                     "orc_momentum_rhs", "orc_prepare"):
+            getattr(L, name).argtypes = [P, I]
+        L.orc_verlet_step.argtypes = [P, C.c_double, I]
+        L.orc_apply_constraints.argtypes = [P]
+        L.orc_stable_dt.argtypes = [P, C.c_double, D]
+        L.orc_kinetic_energy.argtypes = [P, D]
+        L.orc_check_finite.argtypes = [P, C.c_ulonglong]
+        L.orc_damping_sweep.argtypes = [P, I, C.c_double, C.c_double, I]
+        L.orc_particle_split_update.argtypes = [P, C.c_size_t, C.c_double, C.c_double]
+        L.orc_pairwise_split_update.argtypes = [P, C.c_size_t, C.c_longlong, C.c_double, C.c_double]
+        L.orc_explicit_damping_accel.argtypes = [P, C.c_double, D, I]
+        L.orc_grad_mag.argtypes = [C.c_double, I, C.c_double, D]
+        L.orc_kernel_value.argtypes = [C.c_double, I, C.c_double, D]
+        L.orc_random_uniforms.argtypes = [C.c_ulonglong, C.c_size_t, D]
+        L.orc_random_choice.argtypes = [C.c_double, C.c_double, C.c_ulonglong, C.c_size_t, D]
+        L.orc_viscous_bounds.argtypes = [C.c_double, C.c_double, I, D]
+        L.orc_artificial_viscosity.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, D]
+        L.orc_second_pk.argtypes = [I, D, C.c_double, C.c_double, C.c_double, I, D]
+        L.orc_box_lattice.argtypes = [I, D, D, C.c_double, D]
+        L.orc_box_lattice.restype = C.c_longlong
+        L.orc_run.argtypes = [P, D, D]
+        L.orc_openmp_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None
+
+
+def _check(status):
+    if status != 0:
+        raise OracleError(status, lib().orc_last_error().decode())
+
+
+def openmp_threads() -> int:
+    return int(lib().orc_openmp_threads())
+
+
+class OracleSystem:
+    """A ParticleSystem<D> + CellGrid + blocks + ReferenceNeighborhood held by the oracle."""
+
+    def __init__(self, r0, V0, rho0, h, constrained=None, build=True):
+        r0 = np.ascontiguousarray(r0, dtype=np.float64)
+        self.n, self.dim = r0.shape
+        V0 = np.ascontiguousarray(np.broadcast_to(np.asarray(V0, dtype=np.float64), (self.n,)))
+        rho0 = np.ascontiguousarray(np.broadcast_to(np.asarray(rho0, dtype=np.float64), (self.n,)))
+        cons = None
+        if constrained is not None:
+            cons = np.ascontiguousarray(constrained, dtype=np.uint8)
+        self.h = float(h)
+        self._h = C.c_void_p()
+        _check(lib().orc_create(self.dim, self.n, _dp(r0), _dp(V0), _dp(rho0),
+                                cons.ctypes.data_as(C.POINTER(C.c_ubyte)) if cons is not None else None,
+                                self.h, 1 if build else 0, C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().orc_destroy(self._h)
+            self._h = None
+
+    # ---- fields
+    def _shape(self, name):
+        if name in _VEC:
+            return (self.n, self.dim)
+        if name in _MAT:
+            return (self.n, self.dim, self.dim)
+        return (self.n,)
+
+    def get(self, name):
+        out = np.empty(self._shape(name), dtype=np.float64)
+        _check(lib().orc_get_field(self._h, FIELDS[name], _dp(out)))
+        return out
+
+    def set(self, name, value):
+        arr = np.ascontiguousarray(np.broadcast_to(np.asarray(value, dtype=np.float64), self._shape(name)))
+        _check(lib().orc_set_field(self._h, FIELDS[name], _dp(arr)))
+
+    def set_material(self, E, nu, rho0, model="neo_hookean"):
+        _check(lib().orc_set_material(self._h, E, nu, rho0, 1 if model == "neo_hookean" else 0))
+
+    # ---- grid / blocks / neighbourhood
+    def grid(self):
+        dims = (C.c_int * 3)()
+        origin = (C.c_double * 3)()
+        cs = C.c_double()
+        nc = C.c_longlong()
+        _check(lib().orc_grid_info(self._h, dims, origin, C.byref(cs), C.byref(nc)))
+        ncell = nc.value
+        cell_of = np.empty(self.n, dtype=np.int32)
+        cell_start = np.empty(ncell + 1, dtype=np.int64)
+        cell_particles = np.empty(self.n, dtype=np.int32)
+        _check(lib().orc_grid_cells(self._h, cell_of.ctypes.data_as(C.POINTER(C.c_int)),
+                                    cell_start.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                    cell_particles.ctypes.data_as(C.POINTER(C.c_int))))
+        return {"dims": list(dims)[: self.dim], "origin": list(origin)[: self.dim], "cell_size": cs.value,
+                "cell_of": cell_of, "cell_start": cell_start, "cell_particles": cell_particles}
+
+    def blocks(self):
+        g = self.grid()
+        ncell = len(g["cell_start"]) - 1
+        nb = 9 if self.dim == 2 else 27
+        bs = np.empty(nb + 1, dtype=np.int64)
+        bc = np.empty(ncell, dtype=np.int32)
+        _check(lib().orc_blocks(self._h, bs.ctypes.data_as(C.POINTER(C.c_longlong)), bc.ctypes.data_as(C.POINTER(C.c_int))))
+        return [bc[bs[b]:bs[b + 1]].tolist() for b in range(nb)]
+
+    def neighborhood(self):
+        S = int(lib().orc_slot_count(self._h))
+        off = np.empty(self.n + 1, dtype=np.int64)
+        nb = np.empty(S, dtype=np.int32)
+        ln = np.empty(S)
+        e0 = np.empty((S, self.dim))
+        dw = np.empty(S)
+        pf = np.empty(S)
+        _check(lib().orc_get_neighborhood(self._h, off.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                          nb.ctypes.data_as(C.POINTER(C.c_int)), _dp(ln), _dp(e0), _dp(dw), _dp(pf)))
+        return {"offsets": off, "neighbor": nb, "r0_len": ln, "e0": e0, "dwdr0": dw, "pair_factor": pf}
+
+    def set_neighborhood(self, offsets, neighbor, r0_len, e0, dwdr0, pf):
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        nb = np.ascontiguousarray(neighbor, dtype=np.int32)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (r0_len, e0, dwdr0, pf)]
+        _check(lib().orc_set_neighborhood(self._h, off.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                          nb.ctypes.data_as(C.POINTER(C.c_int)), *[_dp(a) for a in arrs]))
+
+    # ---- operators
+    def correction_matrices(self, threads=1):
+        _check(lib().orc_correction_matrices(self._h, threads))
+
+    def deformation_rate(self, threads=1):
+        _check(lib().orc_deformation_rate(self._h, threads))
+
+    def update_density(self, threads=1):
+        _check(lib().orc_update_density(self._h, threads))
+
+    def momentum_rhs(self, threads=1):
+        _check(lib().orc_momentum_rhs(self._h, threads))
+
+    def verlet_step(self, dt, threads=1):
+        _check(lib().orc_verlet_step(self._h, dt, threads))
+
+    def apply_constraints(self):
+        _check(lib().orc_apply_constraints(self._h))
+
+    def prepare(self, threads=1):
+        _check(lib().orc_prepare(self._h, threads))
+
+    def stable_dt(self, h=None):
+        out = C.c_double()
+        _check(lib().orc_stable_dt(self._h, self.h if h is None else h, C.byref(out)))
+        return out.value
+
+    def kinetic_energy(self):
+        out = C.c_double()
+        _check(lib().orc_kinetic_energy(self._h, C.byref(out)))
+        return out.value
+
+    def check_finite(self, step):
+        _check(lib().orc_check_finite(self._h, step))
+
+    def damping_sweep(self, scheme, eta_tilde, dt, threads=1):
+        _check(lib().orc_damping_sweep(self._h, SCHEMES[scheme], eta_tilde, dt, threads))
+
+    def particle_split_update(self, i, eta, dt_half):
+        _check(lib().orc_particle_split_update(self._h, i, eta, dt_half))
+
+    def pairwise_split_update(self, i, slot, eta, dt_half):
+        _check(lib().orc_pairwise_split_update(self._h, i, slot, eta, dt_half))
+
+    def explicit_damping_accel(self, eta, threads=1):
+        out = np.empty((self.n, self.dim))
+        _check(lib().orc_explicit_damping_accel(self._h, eta, _dp(out), threads))
+        return out
+
+    def run(self, *, eta, alpha, scheme="particle_split", steps, fixed_dt=0.0, end_time=0.0,
+            elastic=True, seed=0, threads=1):
+        params = np.array([self.h, eta, alpha, SCHEMES[scheme], steps, fixed_dt, end_time,
+                           1.0 if elastic else 0.0, seed, threads], dtype=np.float64)
+        out = np.zeros(8)
+        _check(lib().orc_run(self._h, _dp(params), _dp(out)))
+        return {"steps": int(out[0]), "damped": int(out[1]), "t": out[2], "elastic_s": out[3],
+                "damping_s": out[4], "total_s": out[5], "last_dt": out[6]}
+
+
+# ---- stateless helpers
+def grad_mag(h, dim, r):
+    out = C.c_double()
+    _check(lib().orc_grad_mag(h, dim, r, C.byref(out)))
+    return out.value
+
+
+def kernel_value(h, dim, r):
+    out = C.c_double()
+    _check(lib().orc_kernel_value(h, dim, r, C.byref(out)))
+    return out.value
+
+
+def random_uniforms(seed, n):
+    out = np.empty(n)
+    _check(lib().orc_random_uniforms(seed, n, _dp(out)))
+    return out
+
+
+def random_choice(eta, alpha, seed, n):
+    out = np.empty(n)
+    _check(lib().orc_random_choice(eta, alpha, seed, n, _dp(out)))
+    return out
+
+
+def viscous_bounds(h, nu_kin, dim):
+    out = np.empty(2)
+    _check(lib().orc_viscous_bounds(h, nu_kin, dim, _dp(out)))
+    return out[0], out[1]
+
+
+def artificial_viscosity(beta, rho0, E, L):
+    out = C.c_double()
+    _check(lib().orc_artificial_viscosity(beta, rho0, E, L, C.byref(out)))
+    return out.value
+
+
+def material(E, nu, rho0, model="neo_hookean"):
+    out = np.empty(8)
+    _check(lib().orc_material(E, nu, rho0, 1 if model == "neo_hookean" else 0, _dp(out)))
+    return dict(zip(["lambda", "mu", "K", "G", "E", "nu", "rho0", "c"], out.tolist()))
+
+
+def second_pk(F, E, nu, rho0, model="neo_hookean"):
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    d = F.shape[0]
+    out = np.empty((d, d))
+    _check(lib().orc_second_pk(d, _dp(F), E, nu, rho0, 1 if model == "neo_hookean" else 0, _dp(out)))
+    return out
+
+
+def box_lattice(lo, hi, dp):
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    hi = np.ascontiguousarray(hi, dtype=np.float64)
+    d = len(lo)
+    n = int(lib().orc_box_lattice(d, _dp(lo), _dp(hi), dp, None))
+    if n < 0:
+        raise OracleError(1, lib().orc_last_error().decode())
+    out = np.empty((n, d))
+    lib().orc_box_lattice(d, _dp(lo), _dp(hi), dp, _dp(out))
+    return out

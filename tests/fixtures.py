@@ -1,0 +1,93 @@
+"""Shared test fixtures, mirroring proj/tests/test_support.hpp of the reference.
+
+lattice_r0 follows test_support.hpp:27-44 (cell-centred lattice, x fastest);
+the O(N^2) brute-force discretisations follow test_support.hpp:74-119.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+SMOOTHING_RATIO = 1.3
+
+
+def lattice_r0(counts, dp, lo=None):
+    """(idx + 0.5) * dp (+ lo) over an x-fastest index walk (test_support.hpp:27-44, cases.cpp:21-46)."""
+    dim = len(counts)
+    lo = np.zeros(dim) if lo is None else np.asarray(lo, dtype=np.float64)
+    pts = []
+    for idx in itertools.product(*[range(c) for c in reversed(counts)]):
+        idx = idx[::-1]
+        pts.append([lo[d] + (idx[d] + 0.5) * dp for d in range(dim)])
+    return np.array(pts, dtype=np.float64)
+
+
+def random_velocities(n, dim, scale, seed):
+    rng = np.random.RandomState(seed)
+    return rng.uniform(-scale, scale, size=(n, dim))
+
+
+def wendland_grad(h, dim, r):
+    sigma = 7.0 / (4.0 * np.pi * h * h) if dim == 2 else 21.0 / (16.0 * np.pi * h * h * h)
+    q = r / h
+    t = 1.0 - 0.5 * q
+    return np.where(q < 2.0, -5.0 * q * (sigma / h) * t * t * t, 0.0)
+
+
+def brute_pairs(r0, cutoff):
+    diff = r0[:, None, :] - r0[None, :, :]
+    dist = np.sqrt((diff ** 2).sum(-1))
+    np.fill_diagonal(dist, np.inf)
+    return diff, dist, dist < cutoff
+
+
+def oracle_deformation_rate(r0, v, V0, B0, h):
+    """test_support.hpp:74-87"""
+    dim = r0.shape[1]
+    diff, dist, mask = brute_pairs(r0, 2 * h)
+    out = np.zeros((len(r0), dim, dim))
+    for i in range(len(r0)):
+        js = np.nonzero(mask[i])[0]
+        s = np.zeros((dim, dim))
+        for j in js:
+            grad = wendland_grad(h, dim, dist[i, j]) * (diff[i, j] / dist[i, j])
+            s -= V0[j] * np.outer(v[i] - v[j], grad)
+        out[i] = s @ B0[i]
+    return out
+
+
+def oracle_momentum_accel(r0, V0, m, B0, P, h):
+    """test_support.hpp:89-105"""
+    dim = r0.shape[1]
+    diff, dist, mask = brute_pairs(r0, 2 * h)
+    out = np.zeros((len(r0), dim))
+    for i in range(len(r0)):
+        s = np.zeros(dim)
+        for j in np.nonzero(mask[i])[0]:
+            grad = wendland_grad(h, dim, dist[i, j]) * (diff[i, j] / dist[i, j])
+            avg = 0.5 * (P[i] @ B0[i] + P[j] @ B0[j])
+            s += 2.0 * V0[i] * V0[j] * (avg @ grad)
+        out[i] = s / m[i]
+    return out
+
+
+def oracle_viscous_accel(r0, v, V0, m, h, eta):
+    """test_support.hpp:107-119"""
+    dim = r0.shape[1]
+    diff, dist, mask = brute_pairs(r0, 2 * h)
+    out = np.zeros((len(r0), dim))
+    for i in range(len(r0)):
+        s = np.zeros(dim)
+        for j in np.nonzero(mask[i])[0]:
+            s += V0[i] * V0[j] * wendland_grad(h, dim, dist[i, j]) / dist[i, j] * (v[i] - v[j])
+        out[i] = (2.0 * eta / m[i]) * s
+    return out
+
+
+def total_momentum(m, v):
+    return (m[:, None] * v).sum(0)
+
+
+def momentum_scale(m, v):
+    return float((m * np.sqrt((v ** 2).sum(1))).sum())
