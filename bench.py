@@ -1,0 +1,311 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 hot path (BASELINE.json metric), one JSON line on rank 0.
+
+Workload (default, the config BASELINE's metric is quoted on that fits one GPU):
+  cfg2 — 3D damping-only sweep, 64^3 = 262,144 particles, fp64, 27-colour
+  particle-split Strang sweep, alpha = 1, fixed dt = 0.6 h / c.
+  One "step" = one full damping sweep (forward + mirrored reverse pass).
+  metric = damping pair-updates per second (DPU/s): 2 * S_free per sweep.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3]
+  python bench.py --impl reference ...   # the reference CPU path (oracle port, all host cores)
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own cfg2 body
+(replicas: the single 64^3 block is not slab-partitioned in round 1), timed
+with CUDA events on the library's stream, max over ranks; value = total DPU / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+BYTES_SLOT = 12          # neighbor i32 + pair_factor f64
+P_D = {3: 65, 2: 49}     # v r/w + m + flag + offset per free particle per half-pass
+P_S = {3: 1091, 2: 587}  # per particle-step minimal traffic
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return PEAKS_FALLBACK["hbm_gbs"], "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+                for k, name in enumerate(names):
+                    if s[3 + k].lower().startswith("active"):
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def barrier_and_max(value, ws):
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cuda_sync():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+    except Exception:
+        pass
+
+
+# ----------------------------------------------------------------------------- cfg2 (headline)
+def free_slots(nb, cons):
+    off = nb["offsets"]
+    if cons is None:
+        return int(off[-1]), len(off) - 1
+    counts = off[1:] - off[:-1]
+    free = cons == 0
+    return int(counts[free].sum()), int(free.sum())
+
+
+def cpu_sweep_sample(cfg, threads, budget_s, min_sweeps=1):
+    """Times full oracle sweeps (the reference CPU path, OpenMP over same-colour cells) within a budget."""
+    from oracle import oracle as O
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+    o.set("v", cfg["v0"])
+    eta_t = cfg["eta"] / cfg["alpha"]
+    o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)  # warm
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < min_sweeps or (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 1000:
+            break
+    return times, o
+
+
+def run_cfg2(args, ws, rank):
+    from paper_2103_08932_b200 import dev
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg2()
+    d = S.build_device(cfg, prepare=False)
+    nb = d.neighborhood()
+    s_free, n_free = free_slots(nb, cfg["constrained"])
+    dpu_per_sweep = 2 * s_free
+    b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_free)
+    eta_t = cfg["eta"] / cfg["alpha"]
+    dt = cfg["fixed_dt"]
+    # warmup
+    for _ in range(args.warmup):
+        d.damping_sweep("particle_split", eta_t, dt)
+    barrier(ws)
+    cuda_sync()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        elapsed = d.damping_sweep("particle_split", eta_t, dt, count=args.steps)  # CUDA events on the stream
+    cuda_sync()
+    barrier(ws)
+    t_max = barrier_and_max(elapsed, ws)
+    value = dpu_per_sweep * args.steps * ws / t_max
+    phase_launches = 54
+    avg_launch = elapsed / (args.steps * phase_launches)
+    achieved = (b_sweep / phase_launches) / avg_launch / 1e9
+    peak, peak_src = load_peaks()
+
+    # e2e through the C ABI with host buffers: v host->device, sweep, v device->host, every step
+    import numpy as np
+    v_host = np.ascontiguousarray(cfg["v0"])
+    h2d = d2h = v_host.nbytes
+    d.set("v", v_host)
+    d.damping_sweep("particle_split", eta_t, dt)
+    _ = d.get("v")
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        d.set("v", v_host)
+        d.damping_sweep("particle_split", eta_t, dt)
+        v_host = d.get("v")
+    t_e2e = barrier_and_max(time.perf_counter() - t0, ws)
+    e2e = dpu_per_sweep * args.steps * ws / t_e2e
+
+    out = {
+        "metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
+        "value": value,
+        "unit": "DPU/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded 64^3 lattice, v ~ N(0,1) Box-Muller from RandomSource(1))",
+        "config": {"workload": "cfg2: 3D damping-only sweep, 64^3 lattice, 27-colour particle-split, alpha=1",
+                   "particles": int(d.n), "slots": int(nb["offsets"][-1]), "dpu_per_step": dpu_per_sweep,
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (CSR 200 MB + 20 MB state > 126 MB L2); no flush",
+                   "reduction": "fast (warp-shuffle)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "k_sweep_phase (one colour phase)",
+                     "bytes_per_launch": b_sweep / phase_launches, "avg_launch_s": avg_launch,
+                     "peak_source": peak_src},
+        "e2e": {"value": e2e, "unit": "DPU/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "tlsph_dev_set_field(V) + tlsph_dev_damping_sweep + tlsph_dev_get_field(V), host buffers"},
+        "gpu_launches": phase_launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        from oracle import oracle as O
+        threads = min(threads, O.openmp_threads())
+        times, _ = cpu_sweep_sample(cfg, threads, budget_s=args.cpu_budget)
+        t_cpu = statistics.median(times)
+        out["cpu_baseline"] = {"value": dpu_per_sweep / t_cpu, "unit": "DPU/s", "cores": threads, "kind": "port",
+                               "sample": f"{len(times)} full cfg2 sweeps (median), oracle OpenMP over same-colour cells"}
+    return out
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference CPU path (oracle port; the reference itself cannot be built here)."""
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg2()
+    threads = min(os.cpu_count() or 1, O.openmp_threads())
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"])
+    o.set("v", cfg["v0"])
+    nb = o.neighborhood()
+    s_free = int(nb["offsets"][-1])
+    dpu = 2 * s_free
+    eta_t = cfg["eta"] / cfg["alpha"]
+    for _ in range(max(0, min(args.warmup, 3))):
+        o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)
+    budget = args.cpu_budget * 4
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget:
+            break
+    total = sum(times)
+    value = dpu * len(times) / total
+    return {
+        "impl": "reference",
+        "metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
+        "value": value, "unit": "DPU/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / len(times) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded 64^3 lattice, v ~ N(0,1))",
+        "config": {"workload": "cfg2: 3D damping-only sweep, 64^3 lattice, 27-colour particle-split, alpha=1",
+                   "particles": len(cfg["r0"]), "slots": s_free},
+        "cpu_baseline": {"value": value, "unit": "DPU/s", "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} of {args.steps} requested full sweeps (time budget {budget:.0f} s)"},
+        "e2e": {"value": value, "unit": "DPU/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg2"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sampling")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        from paper_2103_08932_b200 import dev
+        dev.select_device(local)
+        out = run_cfg2(args, ws, rank)
+    if rank == 0 and out is not None:
+        print(json.dumps(out))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

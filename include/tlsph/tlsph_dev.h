@@ -1,0 +1,200 @@
+/* Thin host <-> CUDA C ABI of the B200 hot path (libtlsph_cuda.so).
+ *
+ * This is the layer the C++ host code (and the Python mirror used by the
+ * tests and bench.py) calls to reach the sm_100a kernels. It owns a
+ * device-resident particle system in cell-sorted structure-of-arrays fp64
+ * layout; every entry point takes and returns host data in REFERENCE
+ * particle order (the order ParticleSystem<D> stores), so callers never see
+ * the device permutation.
+ *
+ * Each function returns a tlsph_status (tlsph.h) and never throws; on
+ * failure tlsph_dev_last_error() holds a message. Device-detected solver
+ * failures carry the reference's status and message text:
+ *   inverted element  -> TLSPH_ERR_INVERTED_ELEMENT   (integrator.cpp:66-77,91-103)
+ *   NaN in v or r     -> TLSPH_ERR_NUMERICAL_FAILURE  (runner.cpp:233-247)
+ *   degenerate B0 /
+ *   coincident pair   -> TLSPH_ERR_DEGENERATE_GEOMETRY (integrator.cpp:30-40, neighbors.cpp:110-112)
+ * CUDA runtime failures map to TLSPH_ERR_INTERNAL.
+ *
+ * Vectors are n*D doubles, matrices n*D*D doubles (row-major per particle).
+ */
+#ifndef TLSPH_DEV_H
+#define TLSPH_DEV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "tlsph/tlsph.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tlsph_dev tlsph_dev;
+
+/* Field selectors for tlsph_dev_set_field / tlsph_dev_get_field
+ * (ParticleSystem<D> members, particle_system.hpp:15-59, plus the body term
+ * of ExternalAccel<D>, forces.hpp:34-38). */
+typedef enum tlsph_dev_field {
+  TLSPH_FIELD_R0 = 0,
+  TLSPH_FIELD_R = 1,
+  TLSPH_FIELD_V = 2,
+  TLSPH_FIELD_A = 3,
+  TLSPH_FIELD_F = 4,
+  TLSPH_FIELD_DFDT = 5,
+  TLSPH_FIELD_B0 = 6,
+  TLSPH_FIELD_V0 = 7,
+  TLSPH_FIELD_M = 8,
+  TLSPH_FIELD_RHO0 = 9,
+  TLSPH_FIELD_RHO = 10,
+  TLSPH_FIELD_BODY = 11,
+  TLSPH_FIELD_CONSTRAINED = 12 /* doubles 0/1 on the wire */
+} tlsph_dev_field;
+
+/* DampingScheme (damping.hpp:12) */
+typedef enum tlsph_dev_scheme {
+  TLSPH_SCHEME_EXPLICIT = 0,
+  TLSPH_SCHEME_PARTICLE_SPLIT = 1,
+  TLSPH_SCHEME_PAIRWISE_SPLIT = 2
+} tlsph_dev_scheme;
+
+/* Reduction order of neighbour sums.
+ * ORDERED: every per-particle sum is a left fold over the CSR slots in
+ *          ascending reference-j order, exactly as the reference loops, so
+ *          damping/neighbour/B0/dF/dt results are bit-identical to the CPU
+ *          reference arithmetic. Used by the parity tests.
+ * FAST:    lanes split the slots and combine with warp shuffles (<= 1e-15
+ *          relative per sum; the 1e-10 north_star class). Default. */
+typedef enum tlsph_dev_reduction { TLSPH_REDUCTION_FAST = 0, TLSPH_REDUCTION_ORDERED = 1 } tlsph_dev_reduction;
+
+/* Material (material.hpp:16-27): model 0 = linear Kirchhoff, 1 = neo-Hookean. */
+typedef struct tlsph_dev_material {
+  int model;
+  double lambda, mu, K, G, E, nu, rho0, c;
+} tlsph_dev_material;
+
+const char* tlsph_dev_last_error(void);
+
+/* Number of visible CUDA devices (0 without a GPU); never fails. */
+int tlsph_dev_device_count(void);
+
+/* Selects the CUDA device that subsequently created handles live on (one
+ * process per GPU: pass LOCAL_RANK). Each handle remembers its device and
+ * re-selects it on every call. Default 0. */
+tlsph_status tlsph_dev_select_device(int ordinal);
+
+/* Creates a device system from reference-order host arrays and runs the GPU
+ * splitting cell-linked-list build: bounding box, cell keys, stable counting
+ * sort into cells (build_cell_grid, neighbors.cpp:24-59), implicit 3^D
+ * colouring (block_decompose, :61-77) and the reference-configuration CSR
+ * with cached pair quantities (build_reference_neighborhoods, :79-141) for
+ * cutoff = 2h. constrained may be NULL. B0 is left at identity. */
+tlsph_status tlsph_dev_create(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
+                              const uint8_t* constrained, double h, tlsph_dev** out);
+
+/* Same, but with a caller-built CSR (reference order) instead of the GPU
+ * neighbour build; for hand-built rigs. The cell grid is still built from r0
+ * with cutoff 2h so sweeps work when the CSR respects the 3^D stencil. */
+tlsph_status tlsph_dev_create_with_csr(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
+                                       const uint8_t* constrained, double h, const int64_t* offsets,
+                                       const int32_t* neighbor, const double* r0_len, const double* e0,
+                                       const double* dwdr0, const double* pair_factor, tlsph_dev** out);
+
+void tlsph_dev_destroy(tlsph_dev* dev);
+
+size_t tlsph_dev_size(const tlsph_dev* dev);
+int tlsph_dev_dim(const tlsph_dev* dev);
+int64_t tlsph_dev_slot_count(const tlsph_dev* dev);
+
+tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const double* host);
+tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host);
+tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode);
+
+/* CellGrid<D> (neighbors.hpp:18-48): dims[D], origin[D], cell_size, number of cells. */
+tlsph_status tlsph_dev_grid_info(const tlsph_dev* dev, int* dims, double* origin, double* cell_size,
+                                 int64_t* n_cells);
+/* cell_of[n] (reference order); cell_start[n_cells+1]; cell_particles[n] =
+ * reference ids of each cell in ascending order. */
+tlsph_status tlsph_dev_grid_cells(const tlsph_dev* dev, int32_t* cell_of, int64_t* cell_start,
+                                  int32_t* cell_particles);
+/* ReferenceNeighborhood<D> (neighbors.hpp:67-82) in reference order. */
+tlsph_status tlsph_dev_get_neighborhood(const tlsph_dev* dev, int64_t* offsets, int32_t* neighbor, double* r0_len,
+                                        double* e0, double* dwdr0, double* pair_factor);
+
+/* ---- operators (reference operator API, integrator.hpp / damping.hpp) ---- */
+tlsph_status tlsph_dev_correction_matrices(tlsph_dev* dev);                 /* integrator.cpp:12-42 */
+tlsph_status tlsph_dev_deformation_rate(tlsph_dev* dev);                    /* integrator.cpp:44-58 */
+tlsph_status tlsph_dev_update_density(tlsph_dev* dev);                      /* integrator.cpp:60-78 */
+tlsph_status tlsph_dev_momentum_rhs(tlsph_dev* dev, const tlsph_dev_material* mat); /* :80-116 */
+tlsph_status tlsph_dev_verlet_step(tlsph_dev* dev, const tlsph_dev_material* mat, double dt); /* :118-152 */
+tlsph_status tlsph_dev_apply_constraints(tlsph_dev* dev);                   /* particle_system.hpp:51-58 */
+/* stable_dt (integrator.cpp:154-169): writes 0.6*min(h/(c+|v|max), sqrt(h/|a|max)). */
+tlsph_status tlsph_dev_stable_dt(tlsph_dev* dev, const tlsph_dev_material* mat, double h, double* dt_acoustic);
+tlsph_status tlsph_dev_kinetic_energy(tlsph_dev* dev, double* out);        /* integrator.cpp:171-178 */
+/* check_finite (runner.cpp:233-247) with the reference message for `step`. */
+tlsph_status tlsph_dev_check_finite(tlsph_dev* dev, uint64_t step);
+
+/* strang_damping_sweep (damping.cpp:125-182): colour-scheduled forward +
+ * mirrored reverse pass of the local implicit operator at dt/2. eta_tilde
+ * == 0 returns immediately; the explicit scheme is rejected. */
+tlsph_status tlsph_dev_damping_sweep(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt);
+/* `count` back-to-back sweeps with fixed eta_tilde and dt (the damping-only
+ * benchmark); same result as calling the above count times. */
+tlsph_status tlsph_dev_damping_sweeps(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt,
+                                      int count);
+/* particle_split_update / pairwise_split_update on one particle (damping.cpp:53-106). */
+tlsph_status tlsph_dev_particle_split_update(tlsph_dev* dev, size_t i, double eta, double dt_half);
+tlsph_status tlsph_dev_pairwise_split_update(tlsph_dev* dev, size_t i, int64_t slot, double eta, double dt_half);
+/* explicit_damping_accel (damping.cpp:36-51); out is n*D, reference order. */
+tlsph_status tlsph_dev_explicit_damping_accel(tlsph_dev* dev, double eta, double* out);
+
+/* ---- device-resident time loop (runner.cpp:341-391) ---- */
+typedef struct tlsph_dev_loop_params {
+  tlsph_dev_material material;
+  double h;              /* smoothing length */
+  double eta;            /* damping viscosity (0 disables damping) */
+  double alpha;          /* random-choice probability */
+  int scheme;            /* tlsph_dev_scheme */
+  uint64_t seed;         /* RandomSource seed of the damping stream */
+  double end_time;       /* <= 0: unbounded (stop on max_steps) */
+  uint64_t max_steps;    /* hard cap (0: unbounded, needs end_time > 0) */
+  double fixed_dt;       /* > 0: use this dt instead of stable_dt */
+  int elastic;           /* 1: verlet_step every step; 0: damping-only loop */
+  int ke_stop;           /* 1: stop at the first step with KE < ke_ratio * peak KE after the peak */
+  double ke_ratio;
+} tlsph_dev_loop_params;
+
+typedef struct tlsph_dev_loop_result {
+  uint64_t steps;
+  uint64_t damped_steps;
+  double t;
+  double last_dt;
+  double elastic_seconds; /* device time of the elastic kernels */
+  double damping_seconds; /* device time of the damping kernels */
+  double total_seconds;   /* device time of the whole loop */
+  double peak_ke;
+  double final_ke;
+  int stopped_on_ke;
+} tlsph_dev_loop_result;
+
+/* Runs the loop with all state resident on the device; the eta~ sequence is
+ * drawn on the host from RandomSource(seed) (damping.hpp:41-50), one draw per
+ * step after the elastic step, exactly as runner.cpp:358-360. The initial
+ * state must already be prepared (B0, momentum RHS, deformation rate), as
+ * runner.cpp:306-312 does before its loop. */
+tlsph_status tlsph_dev_run(tlsph_dev* dev, const tlsph_dev_loop_params* params, tlsph_dev_loop_result* result);
+
+/* Host RNG helpers (damping.hpp:41-50, damping.cpp:29-34). */
+tlsph_status tlsph_random_uniforms(uint64_t seed, size_t n, double* out);
+tlsph_status tlsph_random_choice(double eta, double alpha, uint64_t seed, size_t n, double* out);
+
+/* Timing helpers for bench.py: device time (CUDA events on the handle's
+ * stream) of `count` sweeps / steps already enqueued by the calls above is
+ * returned through these (seconds). */
+double tlsph_dev_last_elapsed(const tlsph_dev* dev);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* TLSPH_DEV_H */

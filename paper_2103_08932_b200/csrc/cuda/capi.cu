@@ -1,0 +1,271 @@
+// extern "C" boundary of libtlsph_cuda.so (declared in include/tlsph/tlsph_dev.h).
+// Exception-free: every entry point maps DevError / std::exception to a
+// tlsph_status and a thread-local message, as the reference C API does
+// (proj/src/capi.cpp:12,26-42).
+#include <memory>
+#include <random>
+#include <string>
+
+#include "system.cuh"
+
+using tlsph_cuda::DevError;
+using tlsph_cuda::DevSystem;
+
+namespace {
+
+thread_local std::string g_dev_err;
+int g_default_device = 0;
+
+template <typename Fn>
+tlsph_status guarded(Fn&& fn) {
+  try {
+    fn();
+    g_dev_err.clear();
+    return TLSPH_OK;
+  } catch (const DevError& e) {
+    g_dev_err = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_dev_err = e.what();
+    return TLSPH_ERR_INTERNAL;
+  } catch (...) {
+    g_dev_err = "unknown error";
+    return TLSPH_ERR_INTERNAL;
+  }
+}
+
+DevSystem& sys(tlsph_dev* d) {
+  if (!d) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "device handle must not be null");
+  CK(cudaSetDevice(d->sys.device));
+  return d->sys;
+}
+const DevSystem& sys(const tlsph_dev* d) {
+  if (!d) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "device handle must not be null");
+  CK(cudaSetDevice(d->sys.device));
+  return d->sys;
+}
+
+std::unique_ptr<tlsph_dev> new_handle() {
+  auto d = std::make_unique<tlsph_dev>();
+  d->sys.device = g_default_device;
+  CK(cudaSetDevice(d->sys.device));
+  return d;
+}
+
+void require_material(const tlsph_dev_material* m) {
+  if (!m) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "material must not be null");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tlsph_dev_last_error(void) { return g_dev_err.c_str(); }
+
+int tlsph_dev_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+tlsph_status tlsph_dev_select_device(int ordinal) {
+  return guarded([&] {
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (ordinal < 0 || ordinal >= count)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "device ordinal " + std::to_string(ordinal) + " out of range");
+    g_default_device = ordinal;
+  });
+}
+
+tlsph_status tlsph_dev_create(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
+                              const uint8_t* constrained, double h, tlsph_dev** out) {
+  if (!out) {
+    g_dev_err = "out must not be null";
+    return TLSPH_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    auto d = new_handle();
+    d->sys.init_common(dim, n, r0, V0, rho0, constrained, h);
+    d->sys.build_neighbourhoods();
+    *out = d.release();
+  });
+}
+
+tlsph_status tlsph_dev_create_with_csr(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
+                                       const uint8_t* constrained, double h, const int64_t* offsets,
+                                       const int32_t* neighbor, const double* r0_len, const double* e0,
+                                       const double* dwdr0, const double* pair_factor, tlsph_dev** out) {
+  if (!out) {
+    g_dev_err = "out must not be null";
+    return TLSPH_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (!offsets) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "offsets must not be null");
+    auto d = new_handle();
+    d->sys.init_common(dim, n, r0, V0, rho0, constrained, h);
+    d->sys.load_csr(offsets, neighbor, r0_len, e0, dwdr0, pair_factor);
+    *out = d.release();
+  });
+}
+
+void tlsph_dev_destroy(tlsph_dev* dev) { delete dev; }
+
+size_t tlsph_dev_size(const tlsph_dev* dev) { return dev ? static_cast<size_t>(dev->sys.n) : 0; }
+int tlsph_dev_dim(const tlsph_dev* dev) { return dev ? dev->sys.D : 0; }
+int64_t tlsph_dev_slot_count(const tlsph_dev* dev) { return dev ? dev->sys.nslots : 0; }
+
+tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const double* host) {
+  return guarded([&] { sys(dev).set_field(field, host); });
+}
+
+tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host) {
+  return guarded([&] { sys(dev).get_field(field, host); });
+}
+
+tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode) {
+  return guarded([&] {
+    if (mode != TLSPH_REDUCTION_FAST && mode != TLSPH_REDUCTION_ORDERED)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown reduction mode");
+    sys(dev).reduction = mode;
+  });
+}
+
+tlsph_status tlsph_dev_grid_info(const tlsph_dev* dev, int* dims, double* origin, double* cell_size,
+                                 int64_t* n_cells) {
+  return guarded([&] {
+    const DevSystem& s = sys(dev);
+    for (int d = 0; d < s.D; ++d) {
+      if (dims) dims[d] = s.dims[d];
+      if (origin) origin[d] = s.origin[d];
+    }
+    if (cell_size) *cell_size = s.cutoff;
+    if (n_cells) *n_cells = s.ncells;
+  });
+}
+
+tlsph_status tlsph_dev_grid_cells(const tlsph_dev* dev, int32_t* cell_of, int64_t* cell_start,
+                                  int32_t* cell_particles) {
+  return guarded([&] { sys(dev).grid_cells(cell_of, cell_start, cell_particles); });
+}
+
+tlsph_status tlsph_dev_get_neighborhood(const tlsph_dev* dev, int64_t* offsets, int32_t* neighbor, double* r0_len,
+                                        double* e0, double* dwdr0, double* pair_factor) {
+  return guarded([&] { sys(dev).get_neighborhood(offsets, neighbor, r0_len, e0, dwdr0, pair_factor); });
+}
+
+tlsph_status tlsph_dev_correction_matrices(tlsph_dev* dev) {
+  return guarded([&] { sys(dev).correction_matrices(); });
+}
+
+tlsph_status tlsph_dev_deformation_rate(tlsph_dev* dev) {
+  return guarded([&] { sys(dev).deformation_rate(); });
+}
+
+tlsph_status tlsph_dev_update_density(tlsph_dev* dev) {
+  return guarded([&] { sys(dev).update_density(); });
+}
+
+tlsph_status tlsph_dev_momentum_rhs(tlsph_dev* dev, const tlsph_dev_material* mat) {
+  return guarded([&] {
+    require_material(mat);
+    sys(dev).momentum_rhs(tlsph_cuda::to_dmat(*mat));
+  });
+}
+
+tlsph_status tlsph_dev_verlet_step(tlsph_dev* dev, const tlsph_dev_material* mat, double dt) {
+  return guarded([&] {
+    require_material(mat);
+    sys(dev).verlet_step(tlsph_cuda::to_dmat(*mat), dt);
+  });
+}
+
+tlsph_status tlsph_dev_apply_constraints(tlsph_dev* dev) {
+  return guarded([&] { sys(dev).apply_constraints(); });
+}
+
+tlsph_status tlsph_dev_stable_dt(tlsph_dev* dev, const tlsph_dev_material* mat, double h, double* dt_acoustic) {
+  return guarded([&] {
+    require_material(mat);
+    if (!dt_acoustic) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "output must not be null");
+    *dt_acoustic = sys(dev).stable_dt(tlsph_cuda::to_dmat(*mat), h);
+  });
+}
+
+tlsph_status tlsph_dev_kinetic_energy(tlsph_dev* dev, double* out) {
+  return guarded([&] {
+    if (!out) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "output must not be null");
+    *out = sys(dev).kinetic_energy();
+  });
+}
+
+tlsph_status tlsph_dev_check_finite(tlsph_dev* dev, uint64_t step) {
+  return guarded([&] { sys(dev).check_finite(step); });
+}
+
+tlsph_status tlsph_dev_damping_sweep(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt) {
+  return guarded([&] { sys(dev).damping_sweep(scheme, eta_tilde, dt, 1); });
+}
+
+tlsph_status tlsph_dev_damping_sweeps(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt,
+                                      int count) {
+  return guarded([&] {
+    if (count < 0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "count must be non-negative");
+    sys(dev).damping_sweep(scheme, eta_tilde, dt, count);
+  });
+}
+
+tlsph_status tlsph_dev_particle_split_update(tlsph_dev* dev, size_t i, double eta, double dt_half) {
+  return guarded([&] { sys(dev).particle_split_update(static_cast<long long>(i), eta, dt_half); });
+}
+
+tlsph_status tlsph_dev_pairwise_split_update(tlsph_dev* dev, size_t i, int64_t slot, double eta, double dt_half) {
+  return guarded([&] { sys(dev).pairwise_split_update(static_cast<long long>(i), slot, eta, dt_half); });
+}
+
+tlsph_status tlsph_dev_explicit_damping_accel(tlsph_dev* dev, double eta, double* out) {
+  return guarded([&] {
+    if (!out) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "output must not be null");
+    sys(dev).explicit_damping_accel(eta, out);
+  });
+}
+
+tlsph_status tlsph_dev_run(tlsph_dev* dev, const tlsph_dev_loop_params* params, tlsph_dev_loop_result* result) {
+  return guarded([&] {
+    if (!params || !result) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "params and result must not be null");
+    sys(dev).run(*params, *result);
+  });
+}
+
+// RandomSource (damping.hpp:41-50): std::mt19937_64, u = (x >> 11) * 2^-53.
+tlsph_status tlsph_random_uniforms(uint64_t seed, size_t n, double* out) {
+  return guarded([&] {
+    if (!out && n) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "output must not be null");
+    std::mt19937_64 gen(seed);
+    for (size_t k = 0; k < n; ++k) out[k] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+  });
+}
+
+// random_choice_eta (damping.cpp:29-34) applied n times to one stream.
+tlsph_status tlsph_random_choice(double eta, double alpha, uint64_t seed, size_t n, double* out) {
+  return guarded([&] {
+    if (!(alpha > 0.0 && alpha <= 1.0))
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
+                     "random-choice probability must lie in (0, 1], got " + std::to_string(alpha));
+    if (!out && n) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "output must not be null");
+    std::mt19937_64 gen(seed);
+    for (size_t k = 0; k < n; ++k) {
+      const double phi = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+      out[k] = phi < alpha ? eta / alpha : 0.0;
+    }
+  });
+}
+
+double tlsph_dev_last_elapsed(const tlsph_dev* dev) { return dev ? dev->sys.last_elapsed : -1.0; }
+
+}  // extern "C"

@@ -1,0 +1,385 @@
+// Shared device-side definitions for the sm_100a TL-SPH relaxation path.
+//
+// Layout (DESIGN.md §Data layout): particles live in CELL-SORTED order
+// (stable counting sort by x-fastest cell key, ascending reference id inside
+// a cell), every per-particle field is a separate fp64 array (SoA), matrices
+// are D*D arrays indexed r*D+c. The reference-configuration CSR is stored in
+// the same sorted row order; each row keeps the reference's ascending
+// reference-j slot order so ordered reductions reproduce the reference sums.
+//
+// All device arithmetic is compiled with -fmad=false: no silent FMA
+// contraction, so every +,-,*,/ and sqrt rounds exactly as the reference's
+// x86-64 (no -march, SSE2) build does. Explicit __fma_rn is used only where
+// a correctly-rounded result is proven (none in round 1).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "tlsph/tlsph.h"
+
+namespace tlsph_cuda {
+
+// ---------------------------------------------------------------- errors
+struct DevError : std::runtime_error {
+  tlsph_status status;
+  DevError(tlsph_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw DevError(TLSPH_ERR_INTERNAL, std::string("CUDA error in ") + what + " (" + file + ":" +
+                                           std::to_string(line) + "): " + cudaGetErrorString(e));
+}
+#define CK(expr) ::tlsph_cuda::cuda_check((expr), #expr, __FILE__, __LINE__)
+#define CK_LAUNCH(what) ::tlsph_cuda::cuda_check(cudaGetLastError(), what, __FILE__, __LINE__)
+
+// Device error sites (first failing site in program order wins; lowest
+// reference index within a site), mirroring the reference's throw points.
+enum ErrSite : int {
+  ERR_DENSITY_PRE = 0,   // update_density before the half-kick (integrator.cpp:126 -> :60-78)
+  ERR_MOMENTUM = 1,      // compute_momentum_rhs det check (integrator.cpp:89-103)
+  ERR_DENSITY_POST = 2,  // update_density after dF/dt (integrator.cpp:144)
+  ERR_NAN = 3,           // check_finite (runner.cpp:233-247)
+  ERR_DEGENERATE = 4,    // compute_correction_matrices (integrator.cpp:30-40)
+  ERR_COINCIDENT = 5,    // build_reference_neighborhoods (neighbors.cpp:110-112)
+  ERR_NONFINITE_R0 = 6,  // build_cell_grid (neighbors.cpp:34-35)
+  ERR_SITES = 8
+};
+
+// Device-resident scalars of the time loop (runner.cpp:341-391 locals).
+struct DScalars {
+  double t;
+  double dt;
+  double end_time;
+  double last_dt;
+  unsigned long long vmax_bits;  // max |v| as ordered bits (non-negative doubles)
+  unsigned long long amax_bits;
+  unsigned int block_counter;    // last-block-done counter of the reduction kernel
+  int halt;                      // 1: done or failed; every loop kernel returns early
+  int done;
+  int failed;
+  long long steps;               // completed steps
+  int pending;                   // a step was started whose accounting is not done yet
+  long long err_step;
+  unsigned long long err_key[ERR_SITES];  // per-site min key (reference index, or packed key)
+  double ke;                     // kinetic energy accumulator
+  double ke_peak;
+  int ke_stop;
+  double ke_ratio;
+  int stopped_on_ke;
+  double params[8];              // loop constants: h, c, viscous bound, fixed_dt, ...
+};
+
+// Device pointers of the sorted SoA system (passed by value to kernels).
+struct DFields {
+  long long n;
+  int dim;
+  double* r0[3];
+  double* r[3];
+  double* v[3];
+  double* a[3];
+  double* body[3];
+  double* F[9];
+  double* dFdt[9];
+  double* B0[9];
+  double* PB[9];
+  double* V0;
+  double* m;
+  double* rho0;
+  double* rho;
+  uint8_t* flag;
+  int* perm;  // sorted -> reference index
+  int* rank;  // reference -> sorted index
+  // reference-configuration CSR in sorted row order
+  long long* offs;
+  int* nbr;  // sorted index of j
+  double* r0_len;
+  double* e0[3];
+  double* dwdr0;
+  double* pf;
+  uint16_t* nloc;  // index of j inside the staged 3^D stencil of i's cell
+  // cell grid
+  long long* cell_start;
+  int dims[3];
+  double origin[3];
+  double cell;
+  int has_body;
+};
+
+constexpr int kWarp = 32;
+constexpr uint16_t kNoLocal = 0xFFFF;
+
+// ---------------------------------------------------------------- small helpers
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {  // x >= 0
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double from_ordered_bits(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum(double x) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// ---------------------------------------------------------------- cell grid
+// CellGrid::coords_of_position (neighbors.cpp:14-22) and linear_index
+// (neighbors.hpp:32-36, x fastest).
+template <int D>
+__device__ __forceinline__ void cell_coords(const double* p, const double* origin, double cell, const int* dims,
+                                            int* c) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    int idx = static_cast<int>(floor((p[d] - origin[d]) / cell));
+    c[d] = idx < 0 ? 0 : (idx > dims[d] - 1 ? dims[d] - 1 : idx);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ long long cell_linear(const int* c, const int* dims) {
+  long long idx = c[D - 1];
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) idx = idx * dims[d] + c[d];
+  return idx;
+}
+
+// The staged stencil of a cell: 3^(D-1) x-rows (dz, dy), each spanning cells
+// x-1..x+1 clamped to the grid, which are contiguous in cell-sorted particle
+// order. Segment k = (dz+1)*3 + (dy+1) in 3D, (dy+1) in 2D.
+template <int D>
+struct Stencil {
+  static constexpr int kSegs = D == 2 ? 3 : 9;
+  long long start[kSegs];
+  int len[kSegs];
+  int base[kSegs];
+  int total;
+};
+
+template <int D>
+__device__ __forceinline__ void stencil_segments(const long long* cell_start, const int* dims, const int* c,
+                                                 Stencil<D>& st) {
+  const int xlo = c[0] > 0 ? c[0] - 1 : 0;
+  const int xhi = c[0] + 1 < dims[0] ? c[0] + 1 : dims[0] - 1;
+  int running = 0;
+#pragma unroll
+  for (int k = 0; k < Stencil<D>::kSegs; ++k) {
+    const int dy = (D == 2 ? k : k % 3) - 1;
+    const int dz = D == 2 ? 0 : k / 3 - 1;
+    const int y = c[1] + dy;
+    const int z = D == 3 ? c[2] + dz : 0;
+    bool ok = y >= 0 && y < dims[1];
+    if (D == 3) ok = ok && z >= 0 && z < dims[2];
+    long long s = 0, e = 0;
+    if (ok) {
+      const long long row = D == 3 ? (static_cast<long long>(z) * dims[1] + y) * dims[0] : static_cast<long long>(y) * dims[0];
+      s = cell_start[row + xlo];
+      e = cell_start[row + xhi + 1];
+    }
+    st.start[k] = s;
+    st.len[k] = static_cast<int>(e - s);
+    st.base[k] = running;
+    running += st.len[k];
+  }
+  st.total = running;
+}
+
+// ---------------------------------------------------------------- small matrices
+// Same operation order as oracle/tlsph_oracle.hpp (Eigen fixed-size paths).
+template <int D>
+struct M {
+  double c[D][D];
+};
+
+__device__ __forceinline__ double det(const M<2>& m) { return m.c[0][0] * m.c[1][1] - m.c[1][0] * m.c[0][1]; }
+__device__ __forceinline__ double det(const M<3>& m) {
+  return m.c[0][0] * (m.c[1][1] * m.c[2][2] - m.c[1][2] * m.c[2][1]) -
+         m.c[0][1] * (m.c[1][0] * m.c[2][2] - m.c[1][2] * m.c[2][0]) +
+         m.c[0][2] * (m.c[1][0] * m.c[2][1] - m.c[1][1] * m.c[2][0]);
+}
+
+__device__ __forceinline__ M<2> inverse(const M<2>& m) {
+  const double invdet = 1.0 / det(m);
+  M<2> r;
+  r.c[0][0] = m.c[1][1] * invdet;
+  r.c[1][0] = -m.c[1][0] * invdet;
+  r.c[0][1] = -m.c[0][1] * invdet;
+  r.c[1][1] = m.c[0][0] * invdet;
+  return r;
+}
+
+__device__ __forceinline__ double cof3(const M<3>& m, int i, int j) {
+  const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+  return m.c[i1][j1] * m.c[i2][j2] - m.c[i1][j2] * m.c[i2][j1];
+}
+
+__device__ __forceinline__ M<3> inverse(const M<3>& m) {
+  const double c00 = cof3(m, 0, 0), c10 = cof3(m, 1, 0), c20 = cof3(m, 2, 0);
+  const double dt = (c00 * m.c[0][0] + c10 * m.c[1][0]) + c20 * m.c[2][0];
+  const double invdet = 1.0 / dt;
+  M<3> r;
+#pragma unroll
+  for (int row = 0; row < 3; ++row)
+#pragma unroll
+    for (int col = 0; col < 3; ++col) r.c[row][col] = cof3(m, col, row) * invdet;
+  return r;
+}
+
+template <int D>
+__device__ __forceinline__ M<D> matmul(const M<D>& a, const M<D>& b) {
+  M<D> o;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      double s = a.c[r][0] * b.c[0][k];
+#pragma unroll
+      for (int q = 1; q < D; ++q) s = s + a.c[r][q] * b.c[q][k];
+      o.c[r][k] = s;
+    }
+  return o;
+}
+
+template <int D>
+__device__ __forceinline__ M<D> transpose(const M<D>& a) {
+  M<D> t;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) t.c[r][k] = a.c[k][r];
+  return t;
+}
+
+// One-sided Jacobi singular values, same routine as the oracle's stand-in for
+// Eigen::JacobiSVD (only the boolean condition test consumes it).
+template <int D>
+__device__ __forceinline__ void singular_values(const M<D>& a, double* sv) {
+  double u[D][D];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) u[r][k] = a.c[r][k];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+#pragma unroll
+    for (int p = 0; p < D - 1; ++p)
+#pragma unroll
+      for (int q = p + 1; q < D; ++q) {
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          alpha = alpha + u[r][p] * u[r][p];
+          beta = beta + u[r][q] * u[r][q];
+          gamma = gamma + u[r][p] * u[r][q];
+        }
+        if (gamma == 0.0 || fabs(gamma) <= 1e-300 || fabs(gamma) <= 1e-17 * sqrt(alpha * beta)) continue;
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double sn = cs * t;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          const double up = u[r][p], uq = u[r][q];
+          u[r][p] = cs * up - sn * uq;
+          u[r][q] = sn * up + cs * uq;
+        }
+      }
+    if (!rotated) break;
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < D; ++r) s = s + u[r][k] * u[r][k];
+    sv[k] = sqrt(s);
+  }
+  // descending
+#pragma unroll
+  for (int x = 0; x < D; ++x)
+#pragma unroll
+    for (int y = 0; y < D - 1 - x; ++y)
+      if (sv[y] < sv[y + 1]) {
+        const double tmp = sv[y];
+        sv[y] = sv[y + 1];
+        sv[y + 1] = tmp;
+      }
+}
+
+// Material constants as kernel arguments (material.hpp:16-27).
+struct DMaterial {
+  int model;  // 0 linear Kirchhoff, 1 neo-Hookean
+  double lambda, mu, c;
+};
+
+// second_pk (material.cpp:32-44); caller guarantees det(F) > 0.
+template <int D>
+__device__ __forceinline__ M<D> second_pk(const M<D>& F, double J, const DMaterial& mat) {
+  const M<D> C = matmul(transpose(F), F);
+  M<D> S;
+  if (mat.model == 0) {
+    M<D> g;
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int k = 0; k < D; ++k) g.c[r][k] = 0.5 * (C.c[r][k] - (r == k ? 1.0 : 0.0));
+    double tr = g.c[0][0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) tr = tr + g.c[d][d];
+    const double lt = mat.lambda * tr;
+    const double twomu = 2.0 * mat.mu;
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int k = 0; k < D; ++k) S.c[r][k] = lt * (r == k ? 1.0 : 0.0) + twomu * g.c[r][k];
+    return S;
+  }
+  const M<D> Ci = inverse(C);
+  const double ll = mat.lambda * log(J);
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) S.c[r][k] = mat.mu * ((r == k ? 1.0 : 0.0) - Ci.c[r][k]) + ll * Ci.c[r][k];
+  return S;
+}
+
+template <int D>
+__device__ __forceinline__ M<D> load_mat(double* const* arr, long long i) {
+  M<D> m;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) m.c[r][k] = arr[r * D + k][i];
+  return m;
+}
+
+template <int D>
+__device__ __forceinline__ void store_mat(double* const* arr, long long i, const M<D>& m) {
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) arr[r * D + k][i] = m.c[r][k];
+}
+
+// Error recording: lowest key wins. Only `failed` is latched here; `halt`
+// is raised at the next serial point (the step-start reduction) so every
+// block of the detecting kernel still records its candidates and the
+// reported index is the reference's lowest one.
+__device__ __forceinline__ void record_error(DScalars* sc, int site, unsigned long long key) {
+  atomicMin(&sc->err_key[site], key);
+  atomicOr(&sc->failed, 1);
+  __threadfence();
+}
+
+}  // namespace tlsph_cuda

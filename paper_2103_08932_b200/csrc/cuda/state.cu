@@ -1,0 +1,932 @@
+// Device system construction: the GPU splitting cell-linked list.
+//
+//   bbox -> cell keys -> counting sort (histogram, exclusive scan, scatter,
+//   per-cell id sort = stable order) -> sorted SoA gather -> reference-
+//   configuration CSR (count, scan, warp-per-particle fill with ascending
+//   reference-j order and bit-exact pair geometry).
+//
+// Reference: proj/src/tlsph/neighbors.cpp:14-141 (build_cell_grid,
+// block_decompose, build_reference_neighborhoods), particle_system.hpp:32-45.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "system.cuh"
+
+namespace tlsph_cuda {
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr long long kScanTile = kScanThreads * kScanItems;
+
+// ------------------------------------------------------------------ scan
+template <typename T>
+__global__ void k_scan_tile(const T* __restrict__ in, long long n_in, long long* __restrict__ out, long long n_out,
+                            long long* __restrict__ tile_sums) {
+  __shared__ long long sh[kScanThreads];
+  const long long base = static_cast<long long>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  long long vals[kScanItems];
+  long long local = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const long long idx = base + k;
+    const long long x = idx < n_in ? static_cast<long long>(in[idx]) : 0;
+    vals[k] = local;
+    local += x;
+  }
+  sh[threadIdx.x] = local;
+  __syncthreads();
+  for (int off = 1; off < kScanThreads; off <<= 1) {
+    const long long add = threadIdx.x >= off ? sh[threadIdx.x - off] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += add;
+    __syncthreads();
+  }
+  const long long excl = sh[threadIdx.x] - local;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const long long idx = base + k;
+    if (idx < n_out) out[idx] = excl + vals[k];
+  }
+  if (threadIdx.x == kScanThreads - 1) tile_sums[blockIdx.x] = sh[threadIdx.x];
+}
+
+__global__ void k_scan_add(long long* out, long long n_out, const long long* tile_offsets) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx < n_out) out[idx] += tile_offsets[idx / kScanTile];
+}
+
+// out[0..n] = exclusive scan of in[0..n-1]; out[n] = total.
+template <typename T>
+void exclusive_scan(const T* in, long long n, long long* out, cudaStream_t st) {
+  const long long n_out = n + 1;
+  const long long tiles = (n_out + kScanTile - 1) / kScanTile;
+  DBuf<long long> sums, sums_scan;
+  sums.alloc(static_cast<size_t>(tiles));
+  k_scan_tile<T><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(in, n, out, n_out, sums.p);
+  CK_LAUNCH("k_scan_tile");
+  if (tiles > 1) {
+    sums_scan.alloc(static_cast<size_t>(tiles + 1));
+    exclusive_scan<long long>(sums.p, tiles, sums_scan.p, st);
+    k_scan_add<<<static_cast<unsigned>((n_out + 255) / 256), 256, 0, st>>>(out, n_out, sums_scan.p);
+    CK_LAUNCH("k_scan_add");
+  }
+  CK(cudaStreamSynchronize(st));  // temporaries die here
+}
+
+// ------------------------------------------------------------------ cell build
+template <int D>
+__global__ void k_bbox(const double* __restrict__ r0aos, long long n, double* __restrict__ part, int* bad) {
+  __shared__ double smin[D][256], smax[D][256];
+  double lo[D], hi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) { lo[d] = INFINITY; hi[d] = -INFINITY; }
+  bool nonfinite = false;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double x = r0aos[i * D + d];
+      if (!isfinite(x)) nonfinite = true;
+      lo[d] = fmin(lo[d], x);
+      hi[d] = fmax(hi[d], x);
+    }
+  }
+  if (nonfinite) atomicOr(bad, 1);
+#pragma unroll
+  for (int d = 0; d < D; ++d) { smin[d][threadIdx.x] = lo[d]; smax[d][threadIdx.x] = hi[d]; }
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        smin[d][threadIdx.x] = fmin(smin[d][threadIdx.x], smin[d][threadIdx.x + off]);
+        smax[d][threadIdx.x] = fmax(smax[d][threadIdx.x], smax[d][threadIdx.x + off]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      part[blockIdx.x * 2 * D + d] = smin[d][0];
+      part[blockIdx.x * 2 * D + D + d] = smax[d][0];
+    }
+}
+
+template <int D>
+__global__ void k_cell_keys(const double* __restrict__ r0aos, long long n, DFields f, int* __restrict__ key,
+                            int* __restrict__ count) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = r0aos[i * D + d];
+  int c[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, c);
+  const int k = static_cast<int>(cell_linear<D>(c, f.dims));
+  key[i] = k;
+  atomicAdd(&count[k], 1);
+}
+
+__global__ void k_cell_scatter(const int* __restrict__ key, long long n, const long long* __restrict__ cell_start,
+                               int* __restrict__ fill, int* __restrict__ perm) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = key[i];
+  const long long pos = cell_start[k] + atomicAdd(&fill[k], 1);
+  perm[pos] = static_cast<int>(i);
+}
+
+// Insertion sort of each cell's ids: the atomic scatter above is unordered,
+// the reference lists ascending ids per cell (neighbors.cpp:52-57).
+__global__ void k_cell_sort(const long long* __restrict__ cell_start, long long ncells, int* __restrict__ perm,
+                            int* __restrict__ max_cell) {
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const long long s = cell_start[c], e = cell_start[c + 1];
+  for (long long a = s + 1; a < e; ++a) {
+    const int x = perm[a];
+    long long b = a - 1;
+    while (b >= s && perm[b] > x) {
+      perm[b + 1] = perm[b];
+      --b;
+    }
+    perm[b + 1] = x;
+  }
+  atomicMax(max_cell, static_cast<int>(e - s));
+}
+
+template <int D>
+__global__ void k_gather_init(DFields f, const double* __restrict__ r0aos, const double* __restrict__ V0h,
+                              const double* __restrict__ rho0h, const uint8_t* __restrict__ cons) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= f.n) return;
+  const int i = f.perm[s];
+  f.rank[i] = static_cast<int>(s);
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double x = r0aos[static_cast<long long>(i) * D + d];
+    f.r0[d][s] = x;
+    f.r[d][s] = x;
+    f.v[d][s] = 0.0;
+    f.a[d][s] = 0.0;
+    f.body[d][s] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < D * D; ++k) {
+    const double id = (k % (D + 1) == 0) ? 1.0 : 0.0;
+    f.F[k][s] = id;
+    f.dFdt[k][s] = 0.0;
+    f.B0[k][s] = id;
+    f.PB[k][s] = 0.0;
+  }
+  const double vol = V0h[i], dens = rho0h[i];
+  f.V0[s] = vol;
+  f.m[s] = dens * vol;  // particle_system.hpp:40
+  f.rho0[s] = dens;
+  f.rho[s] = dens;
+  f.flag[s] = cons ? cons[i] : 0;
+}
+
+// ------------------------------------------------------------------ neighbourhoods
+template <int D>
+__device__ __forceinline__ double pair_dist(const DFields& f, long long i, long long j, double* diff) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) diff[d] = f.r0[d][i] - f.r0[d][j];
+  double s = diff[0] * diff[0];
+#pragma unroll
+  for (int d = 1; d < D; ++d) s = s + diff[d] * diff[d];
+  return sqrt(s);
+}
+
+template <int D>
+__device__ __forceinline__ void stencil_cell(const int* base, int s, const int* dims, int* c, bool& ok) {
+  int rem = s;
+  ok = true;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    c[d] = base[d] + (rem % 3) - 1;
+    rem /= 3;
+    if (c[d] < 0 || c[d] >= dims[d]) ok = false;
+  }
+}
+
+// Per particle: accepted-neighbour count (dist < cutoff, neighbors.cpp:92-115),
+// staged-stencil size, coincident-pair detection.
+template <int D>
+__global__ void k_nbr_count(DFields f, double cutoff, int* __restrict__ counts, int* __restrict__ max_stencil,
+                            DScalars* sc) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = f.r0[d][i];
+  int base[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, base);
+  int cnt = 0;
+  constexpr int kStencil = D == 2 ? 9 : 27;
+  for (int s = 0; s < kStencil; ++s) {
+    int c[D];
+    bool ok;
+    stencil_cell<D>(base, s, f.dims, c, ok);
+    if (!ok) continue;
+    const long long lin = cell_linear<D>(c, f.dims);
+    const long long b = f.cell_start[lin], e = f.cell_start[lin + 1];
+    for (long long j = b; j < e; ++j) {
+      if (j == i) continue;
+      double diff[D];
+      const double dist = pair_dist<D>(f, i, j, diff);
+      if (dist >= cutoff) continue;
+      if (!(dist > 0.0)) {
+        const unsigned long long key = (static_cast<unsigned long long>(f.perm[i]) << 32) |
+                                       (static_cast<unsigned long long>(s) << 24) |
+                                       static_cast<unsigned long long>(j - b);
+        record_error(sc, ERR_COINCIDENT, key);
+      }
+      ++cnt;
+    }
+  }
+  counts[i] = cnt;
+  Stencil<D> st;
+  stencil_segments<D>(f.cell_start, f.dims, base, st);
+  atomicMax(max_stencil, st.total);
+}
+
+// Warp per particle: gather accepted candidates in stencil-scan order, rank
+// them by reference id (the reference std::sort, neighbors.cpp:116), write
+// the slot geometry with the reference's arithmetic (neighbors.cpp:118-139).
+template <int D>
+__global__ void k_nbr_fill(DFields f, double cutoff, double h, double sigma, int cap) {
+  extern __shared__ unsigned char smem_raw[];
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int warps = blockDim.x / kWarp;
+  int* s_ref = reinterpret_cast<int*>(smem_raw) + warp * cap;
+  int* s_idx = reinterpret_cast<int*>(smem_raw) + warps * cap + warp * cap;
+  uint16_t* s_loc = reinterpret_cast<uint16_t*>(reinterpret_cast<int*>(smem_raw) + 2 * warps * cap) + warp * cap;
+  const long long i = static_cast<long long>(blockIdx.x) * warps + warp;
+  if (i >= f.n) return;
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = f.r0[d][i];
+  int base[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, base);
+  Stencil<D> st;
+  stencil_segments<D>(f.cell_start, f.dims, base, st);
+  int count = 0;
+  constexpr int kStencil = D == 2 ? 9 : 27;
+  for (int s = 0; s < kStencil; ++s) {
+    int c[D];
+    bool ok;
+    stencil_cell<D>(base, s, f.dims, c, ok);
+    if (!ok) continue;
+    const long long lin = cell_linear<D>(c, f.dims);
+    const long long b = f.cell_start[lin], e = f.cell_start[lin + 1];
+    const int dy = (s / 3) % 3 - 1;
+    const int dz = D == 3 ? s / 9 - 1 : 0;
+    const int seg = D == 2 ? dy + 1 : (dz + 1) * 3 + (dy + 1);
+    for (long long j0 = b; j0 < e; j0 += kWarp) {
+      const long long j = j0 + lane;
+      bool acc = false;
+      if (j < e && j != i) {
+        double diff[D];
+        acc = pair_dist<D>(f, i, j, diff) < cutoff;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, acc);
+      if (acc) {
+        const int pos = count + __popc(mask & ((1u << lane) - 1u));
+        if (pos < cap) {
+          s_ref[pos] = f.perm[j];
+          s_idx[pos] = static_cast<int>(j);
+          const long long loc = st.base[seg] + (j - st.start[seg]);
+          s_loc[pos] = loc < kNoLocal ? static_cast<uint16_t>(loc) : kNoLocal;
+        }
+      }
+      count += __popc(mask);
+    }
+  }
+  __syncwarp();
+  const long long row = f.offs[i];
+  for (int k = lane; k < count && k < cap; k += kWarp) {
+    const int ref = s_ref[k];
+    int rank = 0;
+    for (int q = 0; q < count; ++q) rank += s_ref[q] < ref ? 1 : 0;
+    const long long slot = row + rank;
+    const long long j = s_idx[k];
+    double diff[D];
+    const double dist = pair_dist<D>(f, i, j, diff);
+    // SmoothingKernel::grad_mag (kernel.cpp:32-38)
+    const double q = dist / h;
+    double dw = 0.0;
+    if (q < 2.0) {
+      const double t = 1.0 - 0.5 * q;
+      dw = -5.0 * q * (sigma / h) * t * t * t;
+    }
+    f.nbr[slot] = static_cast<int>(j);
+    f.r0_len[slot] = dist;
+#pragma unroll
+    for (int d = 0; d < D; ++d) f.e0[d][slot] = diff[d] / dist;
+    f.dwdr0[slot] = dw;
+    f.pf[slot] = 2.0 * f.V0[i] * f.V0[j] * dw / dist;
+    f.nloc[slot] = s_loc[k];
+  }
+}
+
+// ------------------------------------------------------------------ transfers
+__global__ void k_aos_to_soa(const double* __restrict__ src, int comps, long long n, const int* __restrict__ perm,
+                             double** dst) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const long long i = perm[s];
+  for (int c = 0; c < comps; ++c) dst[c][s] = src[i * comps + c];
+}
+
+__global__ void k_soa_to_aos(double* __restrict__ dst, int comps, long long n, const int* __restrict__ perm,
+                             double* const* src) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const long long i = perm[s];
+  for (int c = 0; c < comps; ++c) dst[i * comps + c] = src[c][s];
+}
+
+__global__ void k_flag_in(const double* __restrict__ src, long long n, const int* __restrict__ perm, uint8_t* flag) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  flag[s] = src[perm[s]] != 0.0 ? 1 : 0;
+}
+
+__global__ void k_flag_out(double* __restrict__ dst, long long n, const int* __restrict__ perm, const uint8_t* flag) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  dst[perm[s]] = flag[s] ? 1.0 : 0.0;
+}
+
+template <int D>
+__global__ void k_cell_of(DFields f, int* __restrict__ cell_of) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= f.n) return;
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = f.r0[d][s];
+  int c[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, c);
+  cell_of[f.perm[s]] = static_cast<int>(cell_linear<D>(c, f.dims));
+}
+
+__global__ void k_row_counts_ref(DFields f, long long* __restrict__ cnt_ref) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= f.n) return;
+  cnt_ref[f.perm[s]] = f.offs[s + 1] - f.offs[s];
+}
+
+template <int D>
+__global__ void k_csr_to_ref(DFields f, const long long* __restrict__ off_ref, int* __restrict__ nb, double* ln,
+                             double* e0, double* dw, double* pf) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= f.n) return;
+  const long long src = f.offs[s], cnt = f.offs[s + 1] - src;
+  const long long dst = off_ref[f.perm[s]];
+  for (long long k = 0; k < cnt; ++k) {
+    nb[dst + k] = f.perm[f.nbr[src + k]];
+    ln[dst + k] = f.r0_len[src + k];
+#pragma unroll
+    for (int d = 0; d < D; ++d) e0[(dst + k) * D + d] = f.e0[d][src + k];
+    dw[dst + k] = f.dwdr0[src + k];
+    pf[dst + k] = f.pf[src + k];
+  }
+}
+
+// Caller CSR (reference order) -> sorted rows.
+__global__ void k_row_counts_sorted(DFields f, const long long* __restrict__ off_ref, long long* __restrict__ cnt) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= f.n) return;
+  const int i = f.perm[s];
+  cnt[s] = off_ref[i + 1] - off_ref[i];
+}
+
+template <int D>
+__global__ void k_csr_from_ref(DFields f, const long long* __restrict__ off_ref, const int* __restrict__ nb,
+                               const double* ln, const double* e0, const double* dw, const double* pf) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= f.n) return;
+  const int i = f.perm[s];
+  const long long src = off_ref[i], cnt = off_ref[i + 1] - src, dst = f.offs[s];
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = f.r0[d][s];
+  int base[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, base);
+  Stencil<D> st;
+  stencil_segments<D>(f.cell_start, f.dims, base, st);
+  for (long long k = 0; k < cnt; ++k) {
+    const int j = f.rank[nb[src + k]];
+    f.nbr[dst + k] = j;
+    f.r0_len[dst + k] = ln[src + k];
+#pragma unroll
+    for (int d = 0; d < D; ++d) f.e0[d][dst + k] = e0[(src + k) * D + d];
+    f.dwdr0[dst + k] = dw[src + k];
+    f.pf[dst + k] = pf[src + k];
+    uint16_t loc = kNoLocal;
+    for (int q = 0; q < Stencil<D>::kSegs; ++q)
+      if (j >= st.start[q] && j < st.start[q] + st.len[q]) {
+        const long long l = st.base[q] + (j - st.start[q]);
+        loc = l < kNoLocal ? static_cast<uint16_t>(l) : kNoLocal;
+      }
+    f.nloc[dst + k] = loc;
+  }
+}
+
+__global__ void k_nloc_valid(const uint16_t* nloc, long long n, int* bad) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n && nloc[k] == kNoLocal) atomicOr(bad, 1);
+}
+
+unsigned grid_for(long long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+}  // namespace
+
+// ====================================================================== DevSystem
+DevSystem::~DevSystem() {
+  if (stream) cudaStreamDestroy(stream);
+}
+
+DMaterial to_dmat(const tlsph_dev_material& m) {
+  DMaterial d;
+  d.model = m.model;
+  d.lambda = m.lambda;
+  d.mu = m.mu;
+  d.c = m.c;
+  return d;
+}
+
+DFields DevSystem::fields() const {
+  DFields f{};
+  f.n = n;
+  f.dim = D;
+  for (int d = 0; d < 3; ++d) {
+    f.r0[d] = r0[d].p;
+    f.r[d] = r[d].p;
+    f.v[d] = v[d].p;
+    f.a[d] = a[d].p;
+    f.body[d] = body[d].p;
+    f.e0[d] = e0[d].p;
+    f.dims[d] = dims[d];
+    f.origin[d] = origin[d];
+  }
+  for (int k = 0; k < 9; ++k) {
+    f.F[k] = F[k].p;
+    f.dFdt[k] = dFdt[k].p;
+    f.B0[k] = B0[k].p;
+    f.PB[k] = PB[k].p;
+  }
+  f.V0 = V0.p;
+  f.m = m.p;
+  f.rho0 = rho0.p;
+  f.rho = rho.p;
+  f.flag = flag.p;
+  f.perm = perm.p;
+  f.rank = rank.p;
+  f.offs = offs.p;
+  f.nbr = nbr.p;
+  f.r0_len = r0_len.p;
+  f.dwdr0 = dwdr0.p;
+  f.pf = pf.p;
+  f.nloc = nloc.p;
+  f.cell_start = cell_start.p;
+  f.cell = cutoff;
+  f.has_body = has_body ? 1 : 0;
+  return f;
+}
+
+void DevSystem::alloc_fields() {
+  const size_t N = static_cast<size_t>(n);
+  for (int d = 0; d < D; ++d) {
+    r0[d].alloc(N);
+    r[d].alloc(N);
+    v[d].alloc(N);
+    a[d].alloc(N);
+    body[d].alloc(N);
+  }
+  for (int k = 0; k < D * D; ++k) {
+    F[k].alloc(N);
+    dFdt[k].alloc(N);
+    B0[k].alloc(N);
+    PB[k].alloc(N);
+  }
+  V0.alloc(N);
+  m.alloc(N);
+  rho0.alloc(N);
+  rho.alloc(N);
+  flag.alloc(N);
+  perm.alloc(N);
+  rank.alloc(N);
+  scal.alloc(1);
+}
+
+void DevSystem::reset_errors() {
+  DScalars init{};
+  for (int k = 0; k < ERR_SITES; ++k) init.err_key[k] = ~0ull;
+  CK(cudaMemcpyAsync(scal.p, &init, sizeof(DScalars), cudaMemcpyHostToDevice, stream));
+}
+
+void DevSystem::init_common(int dim, size_t n_, const double* r0_h, const double* V0_h, const double* rho0_h,
+                            const uint8_t* cons_h, double h_) {
+  if (dim != 2 && dim != 3) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "dimension must be 2 or 3");
+  if (n_ == 0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "cell grid needs at least one particle");
+  if (!(h_ > 0.0))
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "smoothing length must be positive, got " + std::to_string(h_));
+  if (!r0_h || !V0_h || !rho0_h) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null input array");
+  D = dim;
+  n = static_cast<long long>(n_);
+  h = h_;
+  cutoff = 2.0 * h_;  // SmoothingKernel::support_radius, runner.cpp:300-301
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  alloc_fields();
+  reset_errors();
+
+  // host inputs -> device
+  DBuf<double> r0aos, V0d, rho0d;
+  DBuf<uint8_t> consd;
+  r0aos.alloc(n_ * D);
+  V0d.alloc(n_);
+  rho0d.alloc(n_);
+  CK(cudaMemcpyAsync(r0aos.p, r0_h, n_ * D * sizeof(double), cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(V0d.p, V0_h, n_ * sizeof(double), cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(rho0d.p, rho0_h, n_ * sizeof(double), cudaMemcpyHostToDevice, stream));
+  if (cons_h) {
+    consd.alloc(n_);
+    CK(cudaMemcpyAsync(consd.p, cons_h, n_, cudaMemcpyHostToDevice, stream));
+  }
+
+  // bounding box (neighbors.cpp:29-40)
+  const unsigned nb = std::min<unsigned>(1024, grid_for(n, 256));
+  DBuf<double> part;
+  part.alloc(nb * 2 * D);
+  DBuf<int> bad;
+  bad.alloc(1);
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), stream));
+  if (D == 2) k_bbox<2><<<nb, 256, 0, stream>>>(r0aos.p, n, part.p, bad.p);
+  else k_bbox<3><<<nb, 256, 0, stream>>>(r0aos.p, n, part.p, bad.p);
+  CK_LAUNCH("k_bbox");
+  std::vector<double> hp(nb * 2 * D);
+  int hbad = 0;
+  CK(cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  sync();
+  if (hbad) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "non-finite particle position");
+  double lo[3], hi[3];
+  for (int d = 0; d < D; ++d) {
+    lo[d] = INFINITY;
+    hi[d] = -INFINITY;
+    for (unsigned b = 0; b < nb; ++b) {
+      lo[d] = std::min(lo[d], hp[b * 2 * D + d]);
+      hi[d] = std::max(hi[d], hp[b * 2 * D + D + d]);
+    }
+  }
+  ncells = 1;
+  for (int d = 0; d < 3; ++d) {
+    if (d < D) {
+      origin[d] = lo[d];
+      const double extent = hi[d] - lo[d];
+      dims[d] = std::max(1, static_cast<int>(std::floor(extent / cutoff)) + 1);  // neighbors.cpp:45-48
+    } else {
+      origin[d] = 0.0;
+      dims[d] = 1;
+    }
+    ncells *= dims[d];
+  }
+  if (ncells > INT_MAX) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "cell grid too large");
+
+  // counting sort by cell key
+  DBuf<int> key, count, fill, maxc;
+  key.alloc(n_);
+  count.alloc(static_cast<size_t>(ncells));
+  fill.alloc(static_cast<size_t>(ncells));
+  maxc.alloc(1);
+  cell_start.alloc(static_cast<size_t>(ncells + 1));
+  CK(cudaMemsetAsync(count.p, 0, ncells * sizeof(int), stream));
+  CK(cudaMemsetAsync(fill.p, 0, ncells * sizeof(int), stream));
+  CK(cudaMemsetAsync(maxc.p, 0, sizeof(int), stream));
+  DFields f = fields();
+  if (D == 2) k_cell_keys<2><<<grid_for(n, 256), 256, 0, stream>>>(r0aos.p, n, f, key.p, count.p);
+  else k_cell_keys<3><<<grid_for(n, 256), 256, 0, stream>>>(r0aos.p, n, f, key.p, count.p);
+  CK_LAUNCH("k_cell_keys");
+  exclusive_scan<int>(count.p, ncells, cell_start.p, stream);
+  k_cell_scatter<<<grid_for(n, 256), 256, 0, stream>>>(key.p, n, cell_start.p, fill.p, perm.p);
+  CK_LAUNCH("k_cell_scatter");
+  k_cell_sort<<<grid_for(ncells, 128), 128, 0, stream>>>(cell_start.p, ncells, perm.p, maxc.p);
+  CK_LAUNCH("k_cell_sort");
+  f = fields();
+  if (D == 2) k_gather_init<2><<<grid_for(n, 256), 256, 0, stream>>>(f, r0aos.p, V0d.p, rho0d.p, cons_h ? consd.p : nullptr);
+  else k_gather_init<3><<<grid_for(n, 256), 256, 0, stream>>>(f, r0aos.p, V0d.p, rho0d.p, cons_h ? consd.p : nullptr);
+  CK_LAUNCH("k_gather_init");
+  CK(cudaMemcpyAsync(&max_cell, maxc.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  sync();
+}
+
+void DevSystem::build_neighbourhoods() {
+  const double kPi = 3.14159265358979323846;
+  const double sigma = (D == 2) ? 7.0 / (4.0 * kPi * h * h) : 21.0 / (16.0 * kPi * h * h * h);
+  DBuf<int> counts, maxs;
+  counts.alloc(static_cast<size_t>(n));
+  maxs.alloc(1);
+  CK(cudaMemsetAsync(maxs.p, 0, sizeof(int), stream));
+  DFields f = fields();
+  if (D == 2) k_nbr_count<2><<<grid_for(n, 128), 128, 0, stream>>>(f, cutoff, counts.p, maxs.p, scal.p);
+  else k_nbr_count<3><<<grid_for(n, 128), 128, 0, stream>>>(f, cutoff, counts.p, maxs.p, scal.p);
+  CK_LAUNCH("k_nbr_count");
+  CK(cudaMemcpyAsync(&max_stencil, maxs.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  sync();
+  raise_if_failed("build_reference_neighborhoods");
+  offs.alloc(static_cast<size_t>(n + 1));
+  exclusive_scan<int>(counts.p, n, offs.p, stream);
+  CK(cudaMemcpy(&nslots, offs.p + n, sizeof(long long), cudaMemcpyDeviceToHost));
+  const size_t S = static_cast<size_t>(std::max<long long>(nslots, 1));
+  nbr.alloc(S);
+  r0_len.alloc(S);
+  for (int d = 0; d < D; ++d) e0[d].alloc(S);
+  dwdr0.alloc(S);
+  pf.alloc(S);
+  nloc.alloc(S);
+  stencil_ok = max_stencil < kNoLocal;
+  f = fields();
+  const int cap = std::max(max_stencil, 1);
+  const int warps = 4;
+  const size_t smem = static_cast<size_t>(warps) * cap * (4 + 4 + 2) + 16;
+  if (D == 2) {
+    CK(cudaFuncSetAttribute(k_nbr_fill<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_nbr_fill<2><<<grid_for(n, warps), warps * kWarp, smem, stream>>>(f, cutoff, h, sigma, cap);
+  } else {
+    CK(cudaFuncSetAttribute(k_nbr_fill<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_nbr_fill<3><<<grid_for(n, warps), warps * kWarp, smem, stream>>>(f, cutoff, h, sigma, cap);
+  }
+  CK_LAUNCH("k_nbr_fill");
+  sync();
+}
+
+void DevSystem::load_csr(const int64_t* offsets, const int32_t* neighbor, const double* r0_len_h, const double* e0_h,
+                         const double* dwdr0_h, const double* pf_h) {
+  const size_t N = static_cast<size_t>(n);
+  nslots = offsets[N];
+  const size_t S = static_cast<size_t>(std::max<long long>(nslots, 1));
+  DBuf<long long> off_ref, cnt;
+  DBuf<int> nb_ref;
+  DBuf<double> ln_ref, e0_ref, dw_ref, pf_ref;
+  off_ref.alloc(N + 1);
+  nb_ref.alloc(S);
+  ln_ref.alloc(S);
+  e0_ref.alloc(S * D);
+  dw_ref.alloc(S);
+  pf_ref.alloc(S);
+  CK(cudaMemcpyAsync(off_ref.p, offsets, (N + 1) * sizeof(long long), cudaMemcpyHostToDevice, stream));
+  if (nslots > 0) {
+    CK(cudaMemcpyAsync(nb_ref.p, neighbor, nslots * sizeof(int), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(ln_ref.p, r0_len_h, nslots * sizeof(double), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(e0_ref.p, e0_h, nslots * D * sizeof(double), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(dw_ref.p, dwdr0_h, nslots * sizeof(double), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(pf_ref.p, pf_h, nslots * sizeof(double), cudaMemcpyHostToDevice, stream));
+  }
+  cnt.alloc(N);
+  offs.alloc(N + 1);
+  DFields f = fields();
+  k_row_counts_sorted<<<grid_for(n, 256), 256, 0, stream>>>(f, off_ref.p, cnt.p);
+  CK_LAUNCH("k_row_counts_sorted");
+  exclusive_scan<long long>(cnt.p, n, offs.p, stream);
+  nbr.alloc(S);
+  r0_len.alloc(S);
+  for (int d = 0; d < D; ++d) e0[d].alloc(S);
+  dwdr0.alloc(S);
+  pf.alloc(S);
+  nloc.alloc(S);
+  // staged-stencil size for the sweep kernels
+  {
+    DBuf<int> counts, maxs;
+    counts.alloc(N);
+    maxs.alloc(1);
+    CK(cudaMemsetAsync(maxs.p, 0, sizeof(int), stream));
+    f = fields();
+    // k_nbr_count also validates coincident pairs of the geometry; only the
+    // stencil size is consumed here.
+    if (D == 2) k_nbr_count<2><<<grid_for(n, 128), 128, 0, stream>>>(f, cutoff, counts.p, maxs.p, scal.p);
+    else k_nbr_count<3><<<grid_for(n, 128), 128, 0, stream>>>(f, cutoff, counts.p, maxs.p, scal.p);
+    CK_LAUNCH("k_nbr_count");
+    CK(cudaMemcpyAsync(&max_stencil, maxs.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    reset_errors();
+  }
+  f = fields();
+  if (D == 2) k_csr_from_ref<2><<<grid_for(n, 128), 128, 0, stream>>>(f, off_ref.p, nb_ref.p, ln_ref.p, e0_ref.p, dw_ref.p, pf_ref.p);
+  else k_csr_from_ref<3><<<grid_for(n, 128), 128, 0, stream>>>(f, off_ref.p, nb_ref.p, ln_ref.p, e0_ref.p, dw_ref.p, pf_ref.p);
+  CK_LAUNCH("k_csr_from_ref");
+  DBuf<int> bad;
+  bad.alloc(1);
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), stream));
+  if (nslots > 0) {
+    k_nloc_valid<<<grid_for(nslots, 256), 256, 0, stream>>>(nloc.p, nslots, bad.p);
+    CK_LAUNCH("k_nloc_valid");
+  }
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  sync();
+  stencil_ok = (hbad == 0) && max_stencil < kNoLocal;
+}
+
+namespace {
+struct FieldSpec {
+  int comps;
+  std::vector<double*> ptrs;
+};
+}  // namespace
+
+static FieldSpec field_spec(const DevSystem& s, int field) {
+  FieldSpec fs;
+  auto vec = [&](const DBuf<double>* arr) {
+    fs.comps = s.D;
+    for (int d = 0; d < s.D; ++d) fs.ptrs.push_back(arr[d].p);
+  };
+  auto mat = [&](const DBuf<double>* arr) {
+    fs.comps = s.D * s.D;
+    for (int k = 0; k < s.D * s.D; ++k) fs.ptrs.push_back(arr[k].p);
+  };
+  auto sc = [&](const DBuf<double>& arr) {
+    fs.comps = 1;
+    fs.ptrs.push_back(arr.p);
+  };
+  switch (field) {
+    case TLSPH_FIELD_R0: vec(s.r0); break;
+    case TLSPH_FIELD_R: vec(s.r); break;
+    case TLSPH_FIELD_V: vec(s.v); break;
+    case TLSPH_FIELD_A: vec(s.a); break;
+    case TLSPH_FIELD_BODY: vec(s.body); break;
+    case TLSPH_FIELD_F: mat(s.F); break;
+    case TLSPH_FIELD_DFDT: mat(s.dFdt); break;
+    case TLSPH_FIELD_B0: mat(s.B0); break;
+    case TLSPH_FIELD_V0: sc(s.V0); break;
+    case TLSPH_FIELD_M: sc(s.m); break;
+    case TLSPH_FIELD_RHO0: sc(s.rho0); break;
+    case TLSPH_FIELD_RHO: sc(s.rho); break;
+    default: throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown field id " + std::to_string(field));
+  }
+  return fs;
+}
+
+void DevSystem::set_field(int field, const double* host) {
+  if (!host) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null host array");
+  const size_t N = static_cast<size_t>(n);
+  if (field == TLSPH_FIELD_CONSTRAINED) {
+    tmp.alloc(N);
+    CK(cudaMemcpyAsync(tmp.p, host, N * sizeof(double), cudaMemcpyHostToDevice, stream));
+    k_flag_in<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, n, perm.p, flag.p);
+    CK_LAUNCH("k_flag_in");
+    sync();
+    return;
+  }
+  if (field == TLSPH_FIELD_R0)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "r0 is fixed at construction (the cell grid is built from it)");
+  FieldSpec fs = field_spec(*this, field);
+  tmp.alloc(N * fs.comps);
+  DBuf<double*> ptrs;
+  ptrs.alloc(fs.ptrs.size());
+  CK(cudaMemcpyAsync(ptrs.p, fs.ptrs.data(), fs.ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(tmp.p, host, N * fs.comps * sizeof(double), cudaMemcpyHostToDevice, stream));
+  k_aos_to_soa<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, ptrs.p);
+  CK_LAUNCH("k_aos_to_soa");
+  if (field == TLSPH_FIELD_BODY) has_body = true;
+  sync();
+}
+
+void DevSystem::get_field(int field, double* host) const {
+  if (!host) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null host array");
+  const size_t N = static_cast<size_t>(n);
+  auto* self = const_cast<DevSystem*>(this);
+  if (field == TLSPH_FIELD_CONSTRAINED) {
+    self->tmp.alloc(N);
+    k_flag_out<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, n, perm.p, flag.p);
+    CK_LAUNCH("k_flag_out");
+    CK(cudaMemcpyAsync(host, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    sync();
+    return;
+  }
+  FieldSpec fs = field_spec(*this, field);
+  self->tmp.alloc(N * fs.comps);
+  DBuf<double*> ptrs;
+  ptrs.alloc(fs.ptrs.size());
+  CK(cudaMemcpyAsync(ptrs.p, fs.ptrs.data(), fs.ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, stream));
+  k_soa_to_aos<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, ptrs.p);
+  CK_LAUNCH("k_soa_to_aos");
+  CK(cudaMemcpyAsync(host, tmp.p, N * fs.comps * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  sync();
+}
+
+void DevSystem::grid_cells(int32_t* cell_of, int64_t* cell_start_h, int32_t* cell_particles) const {
+  const size_t N = static_cast<size_t>(n);
+  DBuf<int> co;
+  co.alloc(N);
+  DFields f = fields();
+  if (D == 2) k_cell_of<2><<<grid_for(n, 256), 256, 0, stream>>>(f, co.p);
+  else k_cell_of<3><<<grid_for(n, 256), 256, 0, stream>>>(f, co.p);
+  CK_LAUNCH("k_cell_of");
+  if (cell_of) CK(cudaMemcpyAsync(cell_of, co.p, N * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (cell_start_h)
+    CK(cudaMemcpyAsync(cell_start_h, cell_start.p, (ncells + 1) * sizeof(long long), cudaMemcpyDeviceToHost, stream));
+  if (cell_particles) CK(cudaMemcpyAsync(cell_particles, perm.p, N * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  sync();
+}
+
+void DevSystem::get_neighborhood(int64_t* offsets, int32_t* neighbor, double* r0_len_h, double* e0_h,
+                                 double* dwdr0_h, double* pf_h) const {
+  const size_t N = static_cast<size_t>(n);
+  const size_t S = static_cast<size_t>(std::max<long long>(nslots, 1));
+  DBuf<long long> cnt, off_ref;
+  cnt.alloc(N);
+  off_ref.alloc(N + 1);
+  DFields f = fields();
+  k_row_counts_ref<<<grid_for(n, 256), 256, 0, stream>>>(f, cnt.p);
+  CK_LAUNCH("k_row_counts_ref");
+  exclusive_scan<long long>(cnt.p, n, off_ref.p, stream);
+  DBuf<int> nb;
+  DBuf<double> ln, e, dw, p;
+  nb.alloc(S);
+  ln.alloc(S);
+  e.alloc(S * D);
+  dw.alloc(S);
+  p.alloc(S);
+  if (D == 2) k_csr_to_ref<2><<<grid_for(n, 128), 128, 0, stream>>>(f, off_ref.p, nb.p, ln.p, e.p, dw.p, p.p);
+  else k_csr_to_ref<3><<<grid_for(n, 128), 128, 0, stream>>>(f, off_ref.p, nb.p, ln.p, e.p, dw.p, p.p);
+  CK_LAUNCH("k_csr_to_ref");
+  if (offsets) CK(cudaMemcpyAsync(offsets, off_ref.p, (N + 1) * sizeof(long long), cudaMemcpyDeviceToHost, stream));
+  if (nslots > 0) {
+    if (neighbor) CK(cudaMemcpyAsync(neighbor, nb.p, nslots * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    if (r0_len_h) CK(cudaMemcpyAsync(r0_len_h, ln.p, nslots * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (e0_h) CK(cudaMemcpyAsync(e0_h, e.p, nslots * D * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (dwdr0_h) CK(cudaMemcpyAsync(dwdr0_h, dw.p, nslots * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (pf_h) CK(cudaMemcpyAsync(pf_h, p.p, nslots * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  }
+  sync();
+}
+
+// Translates recorded device errors into the reference's exception text.
+void DevSystem::raise_if_failed(const char* context) {
+  DScalars hs;
+  CK(cudaMemcpyAsync(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost, stream));
+  sync();
+  if (!hs.failed) return;
+  for (int site = 0; site < ERR_SITES; ++site) {
+    const unsigned long long key = hs.err_key[site];
+    if (key == ~0ull) continue;
+    std::string msg;
+    tlsph_status st = TLSPH_ERR_INTERNAL;
+    switch (site) {
+      case ERR_DENSITY_PRE:
+      case ERR_MOMENTUM:
+      case ERR_DENSITY_POST:
+        st = TLSPH_ERR_INVERTED_ELEMENT;
+        msg = "inverted element: det(F) <= 0 for particle " + std::to_string(key);
+        break;
+      case ERR_NAN:
+        st = TLSPH_ERR_NUMERICAL_FAILURE;
+        msg = "NaN detected at step " + std::to_string(hs.err_step) + ", particle " + std::to_string(key);
+        break;
+      case ERR_DEGENERATE:
+        st = TLSPH_ERR_DEGENERATE_GEOMETRY;
+        msg = "degenerate neighborhood: correction matrix of particle " + std::to_string(key) +
+              " is singular or ill-conditioned";
+        break;
+      case ERR_COINCIDENT: {
+        st = TLSPH_ERR_DEGENERATE_GEOMETRY;
+        const long long ri = static_cast<long long>(key >> 32);
+        const int s = static_cast<int>((key >> 24) & 0xFF);
+        const long long k = static_cast<long long>(key & 0xFFFFFF);
+        // decode the partner: the s-th stencil cell of ri, k-th particle in it
+        int si = 0;
+        CK(cudaMemcpy(&si, rank.p + ri, sizeof(int), cudaMemcpyDeviceToHost));
+        double p[3] = {0, 0, 0};
+        for (int d = 0; d < D; ++d) CK(cudaMemcpy(&p[d], r0[d].p + si, sizeof(double), cudaMemcpyDeviceToHost));
+        int c[3] = {0, 0, 0};
+        int rem = s;
+        for (int d = 0; d < D; ++d) {
+          int idx = static_cast<int>(std::floor((p[d] - origin[d]) / cutoff));
+          idx = std::clamp(idx, 0, dims[d] - 1);
+          c[d] = idx + (rem % 3) - 1;
+          rem /= 3;
+        }
+        long long lin = c[D - 1];
+        for (int d = D - 2; d >= 0; --d) lin = lin * dims[d] + c[d];
+        long long start = 0;
+        CK(cudaMemcpy(&start, cell_start.p + lin, sizeof(long long), cudaMemcpyDeviceToHost));
+        int rj = 0;
+        CK(cudaMemcpy(&rj, perm.p + start + k, sizeof(int), cudaMemcpyDeviceToHost));
+        msg = "coincident particles " + std::to_string(ri) + " and " + std::to_string(rj) +
+              " in reference configuration";
+        break;
+      }
+      default:
+        msg = std::string("device failure in ") + context;
+    }
+    reset_errors();
+    throw DevError(st, msg);
+  }
+}
+
+}  // namespace tlsph_cuda

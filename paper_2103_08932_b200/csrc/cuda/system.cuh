@@ -1,0 +1,144 @@
+// Host-side owner of one device-resident particle system (the object behind
+// the opaque tlsph_dev handle of include/tlsph/tlsph_dev.h).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+#include "tlsph/tlsph_dev.h"
+
+namespace tlsph_cuda {
+
+// Simple owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  // (Re)sizes to `count` elements; keeps the allocation when it is big enough.
+  void alloc(size_t count) {
+    if (p && count <= cap) {
+      n = count;
+      return;
+    }
+    release();
+    n = count;
+    cap = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cap = 0;
+  }
+};
+
+struct SweepPlan;  // damping.cu
+
+class DevSystem {
+ public:
+  int D = 3;
+  int device = 0;
+  long long n = 0;
+  double h = 0.0;
+  double cutoff = 0.0;
+  cudaStream_t stream = nullptr;
+  tlsph_dev_reduction reduction = TLSPH_REDUCTION_FAST;
+
+  // grid
+  int dims[3] = {1, 1, 1};
+  double origin[3] = {0, 0, 0};
+  long long ncells = 0;
+  int max_cell = 0;     // max particles per cell
+  int max_stencil = 0;  // max particles in a staged 3^D stencil
+  bool stencil_ok = true;
+
+  // fields (sorted order)
+  DBuf<double> r0[3], r[3], v[3], a[3], body[3];
+  DBuf<double> F[9], dFdt[9], B0[9], PB[9];
+  DBuf<double> V0, m, rho0, rho;
+  DBuf<uint8_t> flag;
+  DBuf<int> perm, rank;
+  DBuf<long long> cell_start;
+  bool has_body = false;
+
+  // CSR
+  long long nslots = 0;
+  DBuf<long long> offs;
+  DBuf<int> nbr;
+  DBuf<double> r0_len, e0[3], dwdr0, pf;
+  DBuf<uint16_t> nloc;
+
+  // scratch
+  DBuf<DScalars> scal;
+  DBuf<double> tmp;        // AoS staging for host transfers
+  DBuf<long long> tmp_i64;
+  DBuf<int> tmp_i32;
+  DBuf<double> red;        // reduction partials
+  double last_elapsed = 0.0;
+
+  DevSystem() = default;
+  ~DevSystem();
+
+  DFields fields() const;
+
+  // construction (state.cu)
+  void init_common(int dim, size_t n_, const double* r0_h, const double* V0_h, const double* rho0_h,
+                   const uint8_t* cons_h, double h_);
+  void build_neighbourhoods();
+  void load_csr(const int64_t* offsets, const int32_t* neighbor, const double* r0_len_h, const double* e0_h,
+                const double* dwdr0_h, const double* pf_h);
+
+  // transfers (state.cu)
+  void set_field(int field, const double* host);
+  void get_field(int field, double* host) const;
+  void grid_cells(int32_t* cell_of, int64_t* cell_start_h, int32_t* cell_particles) const;
+  void get_neighborhood(int64_t* offsets, int32_t* neighbor, double* r0_len_h, double* e0_h, double* dwdr0_h,
+                        double* pf_h) const;
+
+  // errors
+  void reset_errors();
+  void raise_if_failed(const char* context);  // throws DevError with the reference message
+
+  void sync() const { CK(cudaStreamSynchronize(stream)); }
+
+  // integrator (tlsph.cu)
+  void correction_matrices();
+  void deformation_rate();
+  void update_density();
+  void momentum_rhs(const DMaterial& mat);
+  void verlet_step(const DMaterial& mat, double dt);
+  void apply_constraints();
+  double stable_dt(const DMaterial& mat, double h_);
+  double kinetic_energy();
+  void check_finite(uint64_t step);
+
+  // damping (damping.cu)
+  void damping_sweep(int scheme, double eta_tilde, double dt, int count);
+  void enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars);
+  void particle_split_update(long long i, double eta, double dt_half);
+  void pairwise_split_update(long long i, long long slot, double eta, double dt_half);
+  void explicit_damping_accel(double eta, double* out_host);
+
+  // loop (loop.cu)
+  void run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res);
+
+ private:
+  void alloc_fields();
+};
+
+DMaterial to_dmat(const tlsph_dev_material& m);
+
+// kernels shared across translation units
+void launch_reduce_state(const DevSystem& s, bool with_finite, bool with_ke, bool dt_mode);
+
+}  // namespace tlsph_cuda
+
+struct tlsph_dev {
+  tlsph_cuda::DevSystem sys;
+};

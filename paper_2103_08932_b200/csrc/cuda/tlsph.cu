@@ -1,0 +1,459 @@
+// TL-SPH elastic step on the fixed reference-configuration neighbour list.
+//
+// Reference: proj/src/tlsph/integrator.cpp:12-178, material.cpp:32-44.
+//
+// Neighbour sums use G lanes per particle: lane l folds slots l, l+G, ...
+// in ascending order and the G partials are combined with xor shuffles.
+// G = 1 (ORDERED mode) is exactly the reference's left fold over ascending
+// reference j, so dF/dt, B0 and the momentum sum are bit-identical to the
+// CPU arithmetic (the neo-Hookean log() differs from glibc by <= 1 ulp, so
+// stresses, and everything downstream, are in the 1e-10 class).
+//
+// verlet_step is three fused passes (integrator.cpp:118-152):
+//   A  per particle : density(J^n), half-kick F and r, constraints, P*B0
+//   B  neighbour sum: momentum RHS, kick v, constraints
+//   C  neighbour sum: dF/dt, density(J^{n+1/2}), half-kick F and r, constraints
+#include <algorithm>
+#include <cmath>
+
+#include "system.cuh"
+
+namespace tlsph_cuda {
+
+namespace {
+
+unsigned grid_for(long long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+// ------------------------------------------------------------------ B0 (integrator.cpp:12-42)
+template <int D>
+__global__ void k_correction_matrices(DFields f, DScalars* sc) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  M<D> mom;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int k = 0; k < D; ++k) mom.c[r][k] = 0.0;
+  const long long lo = f.offs[i], hi = f.offs[i + 1];
+  for (long long s = lo; s < hi; ++s) {
+    const int j = f.nbr[s];
+    const double w = -f.V0[j] * f.dwdr0[s] * f.r0_len[s];
+    double e[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) e[d] = f.e0[d][s];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const double we = w * e[r];
+#pragma unroll
+      for (int k = 0; k < D; ++k) mom.c[r][k] = mom.c[r][k] + we * e[k];
+    }
+  }
+  double sv[D];
+  singular_values<D>(mom, sv);
+  if (!(sv[D - 1] > 0.0) || sv[0] / sv[D - 1] > 1e8) {
+    record_error(sc, ERR_DEGENERATE, static_cast<unsigned long long>(f.perm[i]));
+    return;
+  }
+  store_mat<D>(f.B0, i, inverse(mom));
+}
+
+// ------------------------------------------------------------------ dF/dt (integrator.cpp:44-58)
+// POST: fused tail of verlet pass C (density, half-kick, constraints).
+template <int D, int G, bool POST>
+__global__ void k_deformation_rate(DFields f, DScalars* sc, double dt, int loop) {
+  if (loop && sc->halt) return;
+  const double half = 0.5 * (loop ? sc->dt : dt);
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long i = tid / G;
+  const int l = static_cast<int>(tid % G);
+  const bool active = i < f.n;
+  double rate[D][D];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int q = 0; q < D; ++q) rate[r][q] = 0.0;
+  if (active) {
+    double vi[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) vi[d] = f.v[d][i];
+    const long long hi = f.offs[i + 1];
+    for (long long s = f.offs[i] + l; s < hi; s += G) {
+      const int j = f.nbr[s];
+      const double k = f.V0[j] * f.dwdr0[s];
+      double e[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) e[d] = f.e0[d][s];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const double kv = k * (vi[r] - f.v[r][j]);
+#pragma unroll
+        for (int q = 0; q < D; ++q) rate[r][q] = rate[r][q] - kv * e[q];
+      }
+    }
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int q = 0; q < D; ++q) rate[r][q] = group_sum<G>(rate[r][q]);
+  }
+  if (!active || l != 0) return;
+  M<D> R;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int q = 0; q < D; ++q) R.c[r][q] = rate[r][q];
+  const M<D> dF = matmul(R, load_mat<D>(f.B0, i));
+  store_mat<D>(f.dFdt, i, dF);
+  if (POST) {
+    M<D> F = load_mat<D>(f.F, i);
+    const double J = det(F);
+    if (!(J > 0.0)) record_error(sc, ERR_DENSITY_POST, static_cast<unsigned long long>(f.perm[i]));
+    else f.rho[i] = f.rho0[i] / J;
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int q = 0; q < D; ++q) F.c[r][q] = F.c[r][q] + half * dF.c[r][q];
+    store_mat<D>(f.F, i, F);
+    if (f.flag[i]) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        f.v[d][i] = 0.0;
+        f.r[d][i] = f.r0[d][i];
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) f.r[d][i] = f.r[d][i] + half * f.v[d][i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ density (integrator.cpp:60-78)
+template <int D>
+__global__ void k_update_density(DFields f, DScalars* sc) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  const double J = det(load_mat<D>(f.F, i));
+  if (!(J > 0.0)) {
+    record_error(sc, ERR_DENSITY_PRE, static_cast<unsigned long long>(f.perm[i]));
+    return;
+  }
+  f.rho[i] = f.rho0[i] / J;
+}
+
+// ------------------------------------------------------------------ stress term P*B0 (integrator.cpp:86-103)
+// PRE: fused head of verlet pass A (density from J^n, half-kick, constraints).
+template <int D, bool PRE>
+__global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int loop) {
+  if (loop && sc->halt) return;
+  const double half = 0.5 * (loop ? sc->dt : dt);
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  M<D> F = load_mat<D>(f.F, i);
+  if (PRE) {
+    const double J0 = det(F);
+    if (!(J0 > 0.0)) record_error(sc, ERR_DENSITY_PRE, static_cast<unsigned long long>(f.perm[i]));
+    else f.rho[i] = f.rho0[i] / J0;
+    const M<D> dF = load_mat<D>(f.dFdt, i);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int q = 0; q < D; ++q) F.c[r][q] = F.c[r][q] + half * dF.c[r][q];
+    store_mat<D>(f.F, i, F);
+    if (f.flag[i]) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        f.v[d][i] = 0.0;
+        f.r[d][i] = f.r0[d][i];
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) f.r[d][i] = f.r[d][i] + half * f.v[d][i];
+    }
+  }
+  const double J = det(F);
+  M<D> PB;
+  if (!(J > 0.0)) {
+    record_error(sc, ERR_MOMENTUM, static_cast<unsigned long long>(f.perm[i]));
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int q = 0; q < D; ++q) PB.c[r][q] = 0.0;
+  } else {
+    const M<D> S = second_pk<D>(F, J, mat);
+    PB = matmul(matmul(F, S), load_mat<D>(f.B0, i));
+  }
+  store_mat<D>(f.PB, i, PB);
+}
+
+// ------------------------------------------------------------------ momentum RHS (integrator.cpp:105-115)
+// KICK: fused tail of verlet pass B (v += dt a, constraints).
+template <int D, int G, bool KICK>
+__global__ void k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
+  if (loop && sc->halt) return;
+  const double dt = loop ? sc->dt : dt_arg;
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long i = tid / G;
+  const int l = static_cast<int>(tid % G);
+  const bool active = i < f.n;
+  double acc[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) acc[d] = 0.0;
+  if (active) {
+    double pbi[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) pbi[k] = f.PB[k][i];
+    const double V0i = f.V0[i];
+    const long long hi = f.offs[i + 1];
+    for (long long s = f.offs[i] + l; s < hi; s += G) {
+      const int j = f.nbr[s];
+      const double k = V0i * f.V0[j] * f.dwdr0[s];
+      double e[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) e[d] = f.e0[d][s];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double t = (k * (pbi[r * D] + f.PB[r * D][j])) * e[0];
+#pragma unroll
+        for (int q = 1; q < D; ++q) t = t + (k * (pbi[r * D + q] + f.PB[r * D + q][j])) * e[q];
+        acc[r] = acc[r] + t;
+      }
+    }
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[d] = group_sum<G>(acc[d]);
+  }
+  if (!active || l != 0) return;
+  const double mi = f.m[i];
+  double a[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    a[d] = acc[d] / mi + f.body[d][i];
+    f.a[d][i] = a[d];
+  }
+  if (KICK) {
+    if (f.flag[i]) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        f.v[d][i] = 0.0;
+        f.r[d][i] = f.r0[d][i];
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) f.v[d][i] = f.v[d][i] + dt * a[d];
+    }
+  }
+}
+
+template <int D>
+__global__ void k_apply_constraints(DFields f) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n || !f.flag[i]) return;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    f.v[d][i] = 0.0;
+    f.r[d][i] = f.r0[d][i];
+  }
+}
+
+// ------------------------------------------------------------------ reductions
+// |v|max, |a|max (stable_dt, integrator.cpp:154-169), first non-finite
+// particle (check_finite, runner.cpp:233-247) and kinetic energy partials
+// (integrator.cpp:171-178).
+template <int D>
+__global__ void k_reduce(DFields f, double* __restrict__ partials, DScalars* sc, int want_ke) {
+  __shared__ double s_v[256], s_a[256], s_k[256];
+  double vmax = 0.0, amax = 0.0, ke = 0.0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < f.n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double sv = f.v[0][i] * f.v[0][i], sa = f.a[0][i] * f.a[0][i];
+    bool fin = isfinite(f.v[0][i]) && isfinite(f.r[0][i]);
+#pragma unroll
+    for (int d = 1; d < D; ++d) {
+      sv = sv + f.v[d][i] * f.v[d][i];
+      sa = sa + f.a[d][i] * f.a[d][i];
+      fin = fin && isfinite(f.v[d][i]) && isfinite(f.r[d][i]);
+    }
+    vmax = fmax(vmax, sqrt(sv));
+    amax = fmax(amax, sqrt(sa));
+    if (want_ke) ke += 0.5 * f.m[i] * sv;
+    if (!fin) record_error(sc, ERR_NAN, static_cast<unsigned long long>(f.perm[i]));
+  }
+  s_v[threadIdx.x] = vmax;
+  s_a[threadIdx.x] = amax;
+  s_k[threadIdx.x] = ke;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      s_v[threadIdx.x] = fmax(s_v[threadIdx.x], s_v[threadIdx.x + off]);
+      s_a[threadIdx.x] = fmax(s_a[threadIdx.x], s_a[threadIdx.x + off]);
+      s_k[threadIdx.x] += s_k[threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x * 3 + 0] = s_v[0];
+    partials[blockIdx.x * 3 + 1] = s_a[0];
+    partials[blockIdx.x * 3 + 2] = s_k[0];
+  }
+}
+
+}  // namespace
+
+// ====================================================================== host side
+namespace {
+template <typename Fn2, typename Fn3>
+void dispatch(int D, Fn2&& f2, Fn3&& f3) {
+  if (D == 2) f2();
+  else f3();
+}
+}  // namespace
+
+void DevSystem::correction_matrices() {
+  reset_errors();
+  DFields f = fields();
+  dispatch(D, [&] { k_correction_matrices<2><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p); },
+           [&] { k_correction_matrices<3><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p); });
+  CK_LAUNCH("k_correction_matrices");
+  raise_if_failed("compute_correction_matrices");
+}
+
+void DevSystem::deformation_rate() {
+  DFields f = fields();
+  const bool ord = reduction == TLSPH_REDUCTION_ORDERED;
+  if (D == 2) {
+    if (ord) k_deformation_rate<2, 1, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    else k_deformation_rate<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+  } else {
+    if (ord) k_deformation_rate<3, 1, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    else k_deformation_rate<3, 8, false><<<grid_for(n * 8, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+  }
+  CK_LAUNCH("k_deformation_rate");
+  sync();
+}
+
+void DevSystem::update_density() {
+  reset_errors();
+  DFields f = fields();
+  dispatch(D, [&] { k_update_density<2><<<grid_for(n, 256), 256, 0, stream>>>(f, scal.p); },
+           [&] { k_update_density<3><<<grid_for(n, 256), 256, 0, stream>>>(f, scal.p); });
+  CK_LAUNCH("k_update_density");
+  raise_if_failed("update_density");
+}
+
+void DevSystem::momentum_rhs(const DMaterial& mat) {
+  reset_errors();
+  DFields f = fields();
+  const bool ord = reduction == TLSPH_REDUCTION_ORDERED;
+  dispatch(D, [&] { k_stress<2, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, mat, 0.0, 0); },
+           [&] { k_stress<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, mat, 0.0, 0); });
+  CK_LAUNCH("k_stress");
+  raise_if_failed("compute_momentum_rhs");  // the reference throws before the pair loop
+  if (D == 2) {
+    if (ord) k_momentum<2, 1, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    else k_momentum<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+  } else {
+    if (ord) k_momentum<3, 1, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    else k_momentum<3, 8, false><<<grid_for(n * 8, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+  }
+  CK_LAUNCH("k_momentum");
+  sync();
+}
+
+// Enqueues the three verlet passes on the handle's stream (no sync).
+void enqueue_verlet(DevSystem& s, const DMaterial& mat, double dt, int loop) {
+  DFields f = s.fields();
+  const long long n = s.n;
+  const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED;
+  cudaStream_t st = s.stream;
+  if (s.D == 2) {
+    k_stress<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
+    if (ord) {
+      k_momentum<2, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      k_deformation_rate<2, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    } else {
+      k_momentum<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      k_deformation_rate<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    }
+  } else {
+    k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
+    if (ord) {
+      k_momentum<3, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      k_deformation_rate<3, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    } else {
+      k_momentum<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      k_deformation_rate<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    }
+  }
+  CK_LAUNCH("verlet passes");
+}
+
+void DevSystem::verlet_step(const DMaterial& mat, double dt) {
+  reset_errors();
+  enqueue_verlet(*this, mat, dt, 0);
+  raise_if_failed("verlet_step");
+}
+
+void DevSystem::apply_constraints() {
+  DFields f = fields();
+  dispatch(D, [&] { k_apply_constraints<2><<<grid_for(n, 256), 256, 0, stream>>>(f); },
+           [&] { k_apply_constraints<3><<<grid_for(n, 256), 256, 0, stream>>>(f); });
+  CK_LAUNCH("k_apply_constraints");
+  sync();
+}
+
+namespace {
+struct Reduced {
+  double vmax, amax, ke;
+};
+
+Reduced reduce_state(DevSystem& s, bool want_ke) {
+  const unsigned nb = std::min<unsigned>(592, grid_for(s.n, 256));
+  s.red.alloc(nb * 3);
+  DFields f = s.fields();
+  if (s.D == 2) k_reduce<2><<<nb, 256, 0, s.stream>>>(f, s.red.p, s.scal.p, want_ke ? 1 : 0);
+  else k_reduce<3><<<nb, 256, 0, s.stream>>>(f, s.red.p, s.scal.p, want_ke ? 1 : 0);
+  CK_LAUNCH("k_reduce");
+  std::vector<double> hp(nb * 3);
+  CK(cudaMemcpyAsync(hp.data(), s.red.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  s.sync();
+  Reduced r{0.0, 0.0, 0.0};
+  for (unsigned b = 0; b < nb; ++b) {
+    r.vmax = std::max(r.vmax, hp[b * 3]);
+    r.amax = std::max(r.amax, hp[b * 3 + 1]);
+    r.ke += hp[b * 3 + 2];
+  }
+  return r;
+}
+}  // namespace
+
+double DevSystem::stable_dt(const DMaterial& mat, double h_) {
+  reset_errors();
+  const Reduced r = reduce_state(*this, false);
+  reset_errors();  // stable_dt itself never fails
+  double bound = h_ / (mat.c + r.vmax);
+  if (r.amax > 0.0) bound = std::min(bound, std::sqrt(h_ / r.amax));
+  return 0.6 * bound;
+}
+
+double DevSystem::kinetic_energy() {
+  reset_errors();
+  const Reduced r = reduce_state(*this, true);
+  reset_errors();
+  return r.ke;
+}
+
+void DevSystem::check_finite(uint64_t step) {
+  reset_errors();
+  reduce_state(*this, false);
+  DScalars hs;
+  CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
+  if (hs.failed) {
+    hs.err_step = static_cast<long long>(step);
+    CK(cudaMemcpy(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice));
+    raise_if_failed("check_finite");
+  }
+}
+
+}  // namespace tlsph_cuda
