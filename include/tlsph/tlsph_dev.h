@@ -193,6 +193,11 @@ tlsph_status tlsph_random_choice(double eta, double alpha, uint64_t seed, size_t
  * returned through these (seconds). */
 double tlsph_dev_last_elapsed(const tlsph_dev* dev);
 
+/* Device self-test of the corrected quotient RN(x/d) = q0 + r*y used where the
+ * divisor is known ahead of the Gauss-Seidel chain: counts mismatches against
+ * IEEE division over n random operand pairs (expected 0). */
+tlsph_status tlsph_dev_selftest_division(int64_t n, uint64_t seed, uint64_t* mismatches);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -268,4 +268,12 @@ tlsph_status tlsph_random_choice(double eta, double alpha, uint64_t seed, size_t
 
 double tlsph_dev_last_elapsed(const tlsph_dev* dev) { return dev ? dev->sys.last_elapsed : -1.0; }
 
+tlsph_status tlsph_dev_selftest_division(int64_t n, uint64_t seed, uint64_t* mismatches) {
+  return guarded([&] {
+    if (!mismatches) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "output must not be null");
+    CK(cudaSetDevice(g_default_device));
+    *mismatches = tlsph_cuda::selftest_division(n, seed);
+  });
+}
+
 }  // extern "C"

@@ -89,6 +89,12 @@ struct DFields {
   double* PB[9];
   double* V0;
   double* m;
+  double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
+  long long* cell_slot;  // offs[cell_start[c]]: first CSR slot of cell c (ncells+1)
+  // per-sweep particle-split constants (sweep.cu, k_sweep_folds)
+  double* fdiag;  // sum_j b_ij - m_i
+  double* fden;   // diag^2 + sum_j b_ij^2
+  double* fy;     // RN(1 / den)
   double* rho0;
   double* rho;
   uint8_t* flag;
@@ -158,6 +164,11 @@ __device__ __forceinline__ long long cell_linear(const int* c, const int* dims) 
 // The staged stencil of a cell: 3^(D-1) x-rows (dz, dy), each spanning cells
 // x-1..x+1 clamped to the grid, which are contiguous in cell-sorted particle
 // order. Segment k = (dz+1)*3 + (dy+1) in 3D, (dy+1) in 2D.
+// Shared-memory layout: each segment is staged as the 16-byte aligned
+// superset of its fp64 range (so it can be moved by one TMA bulk copy);
+// particle g of segment k sits at base[k] + (g - start[k]), where base[k]
+// already includes the 0/1 element alignment offset. `total` is the padded
+// tile length.
 template <int D>
 struct Stencil {
   static constexpr int kSegs = D == 2 ? 3 : 9;
@@ -189,8 +200,9 @@ __device__ __forceinline__ void stencil_segments(const long long* cell_start, co
     }
     st.start[k] = s;
     st.len[k] = static_cast<int>(e - s);
-    st.base[k] = running;
-    running += st.len[k];
+    const int par = static_cast<int>(s & 1);
+    st.base[k] = running + par;
+    running += st.len[k] > 0 ? ((st.len[k] + par + 1) & ~1) : 0;
   }
   st.total = running;
 }

@@ -1,23 +1,7 @@
-// Colour-scheduled, operator-split implicit viscous damping sweep.
+// Single-particle damping operators, the explicit scheme and the host side
+// of strang_damping_sweep. The colour-phase sweep kernel is in sweep.cu.
 //
-// Reference: proj/src/tlsph/damping.cpp:53-182 (particle_split_update,
-// pairwise_split_update, strang_damping_sweep), neighbors.cpp:143-174
-// (block_sweep), neighbors.cpp:61-77 (3^D residue colouring).
-//
-// One launch per colour phase: colour b holds the cells whose coordinates
-// are congruent to b's residues mod 3 on every axis; their 3^D stencils are
-// disjoint (neighbors.hpp:50-52), so each cell is one independent task. One
-// warp owns one cell:
-//   1. stage the cell's stencil (3^(D-1) contiguous x-rows of the cell-sorted
-//      arrays) of v, m and the clamp flag into shared memory;
-//   2. run the cell's particles in order (ascending id forward, descending on
-//      the reverse leg, damping.cpp:112-121); for particle i the lanes split
-//      its CSR slots, reduce residual / sum b / sum b^2 with warp shuffles
-//      (FAST) or lane 0 folds them in slot order (ORDERED, bit-exact), then
-//      apply the momentum-conserving neighbour correction lane-parallel;
-//   3. write the stencil back (same-colour stencils are disjoint: no races).
-// The pairwise scheme runs the same staging with lane 0 applying the 2x2
-// pair solves in the palindromic slot order (damping.cpp:161-176).
+// Reference: proj/src/tlsph/damping.cpp:36-182.
 #include <algorithm>
 #include <cmath>
 
@@ -28,193 +12,6 @@ namespace tlsph_cuda {
 namespace {
 
 unsigned grid_for(long long n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
-
-constexpr int kSweepWarps = 4;
-
-struct Phase {
-  int res[3];     // colour residues per axis
-  int cnt[3];     // cells of this colour per axis
-  long long ncol; // cells in the colour
-  int forward;
-  int stride;     // staged stencil capacity per warp (elements)
-  double eta;
-  double dt;      // used when dt_from_scalars == 0
-  int dt_from_scalars;
-};
-
-template <int D>
-__host__ __device__ constexpr int colour_count() { return D == 2 ? 9 : 27; }
-
-// bytes of staged state per warp
-template <int D>
-__host__ __device__ size_t warp_smem_bytes(int stride) {
-  return static_cast<size_t>(stride) * (sizeof(double) * (D + 1) + 1);
-}
-
-template <int D, int SCHEME, bool ORDERED>
-__global__ void __launch_bounds__(kSweepWarps * kWarp)
-k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
-  if (ph.dt_from_scalars && sc->halt) return;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  const long long k = static_cast<long long>(blockIdx.x) * kSweepWarps + warp;
-  if (k >= ph.ncol) return;
-  // cell coordinates of task k in colour (res)
-  int c[3];
-  c[0] = ph.res[0] + 3 * static_cast<int>(k % ph.cnt[0]);
-  c[1] = ph.res[1] + 3 * static_cast<int>((k / ph.cnt[0]) % ph.cnt[1]);
-  c[2] = D == 3 ? ph.res[2] + 3 * static_cast<int>(k / (static_cast<long long>(ph.cnt[0]) * ph.cnt[1])) : 0;
-  const long long lin = cell_linear<D>(c, f.dims);
-  const long long p0 = f.cell_start[lin], p1 = f.cell_start[lin + 1];
-  if (p0 == p1) return;
-
-  const int S = ph.stride;
-  unsigned char* wbase = smem + static_cast<size_t>(warp) * warp_smem_bytes<D>(S);
-  double* sv[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) sv[d] = reinterpret_cast<double*>(wbase) + d * S;
-  double* sm = reinterpret_cast<double*>(wbase) + D * S;
-  uint8_t* sf = wbase + sizeof(double) * (D + 1) * S;
-
-  Stencil<D> st;
-  stencil_segments<D>(f.cell_start, f.dims, c, st);
-#pragma unroll
-  for (int q = 0; q < Stencil<D>::kSegs; ++q) {
-    const long long g0 = st.start[q];
-    const int b = st.base[q];
-    for (int e = lane; e < st.len[q]; e += kWarp) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) sv[d][b + e] = f.v[d][g0 + e];
-      sm[b + e] = f.m[g0 + e];
-      sf[b + e] = f.flag[g0 + e];
-    }
-  }
-  __syncwarp();
-
-  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
-  const double dt_half = 0.5 * dt;
-  const double eta = ph.eta;
-  const int center = D == 2 ? 1 : 4;
-  const long long cbase = st.start[center];
-  const int lbase = st.base[center];
-  const long long np = p1 - p0;
-
-  for (long long kk = 0; kk < np; ++kk) {
-    const long long i = ph.forward ? p0 + kk : p1 - 1 - kk;
-    const int li = lbase + static_cast<int>(i - cbase);
-    if (sf[li]) continue;  // constrained i is skipped (damping.cpp:151,163)
-    const long long lo = f.offs[i], hi = f.offs[i + 1];
-    if (SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT) {
-      if (lo == hi) continue;
-      double vi[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) vi[d] = sv[d][li];
-      double R[D], sb = 0.0, sb2 = 0.0;
-#pragma unroll
-      for (int d = 0; d < D; ++d) R[d] = 0.0;
-      if (ORDERED) {
-        if (lane == 0) {
-          for (long long s = lo; s < hi; ++s) {
-            const double b = eta * f.pf[s] * dt_half;
-            const int j = f.nloc[s];
-#pragma unroll
-            for (int d = 0; d < D; ++d) R[d] = R[d] - b * (vi[d] - sv[d][j]);
-            sb = sb + b;
-            sb2 = sb2 + b * b;
-          }
-        }
-#pragma unroll
-        for (int d = 0; d < D; ++d) R[d] = __shfl_sync(0xffffffffu, R[d], 0);
-        sb = __shfl_sync(0xffffffffu, sb, 0);
-        sb2 = __shfl_sync(0xffffffffu, sb2, 0);
-      } else {
-        for (long long s = lo + lane; s < hi; s += kWarp) {
-          const double b = eta * f.pf[s] * dt_half;
-          const int j = f.nloc[s];
-#pragma unroll
-          for (int d = 0; d < D; ++d) R[d] = R[d] - b * (vi[d] - sv[d][j]);
-          sb = sb + b;
-          sb2 = sb2 + b * b;
-        }
-#pragma unroll
-        for (int d = 0; d < D; ++d) R[d] = warp_sum(R[d]);
-        sb = warp_sum(sb);
-        sb2 = warp_sum(sb2);
-      }
-      const double diag = sb - sm[li];
-      const double denom = diag * diag + sb2;
-      double rate[D], vnew[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        rate[d] = R[d] / denom;
-        vnew[d] = vi[d] + diag * rate[d];
-      }
-      // neighbour correction: every j is distinct within the row, so the
-      // lane-parallel order is bit-identical to the reference loop.
-      for (long long s = lo + lane; s < hi; s += kWarp) {
-        const double b = eta * f.pf[s] * dt_half;
-        const int j = f.nloc[s];
-        if (!sf[j]) {
-          const double bm = b / sm[j];
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const double vj = sv[d][j];
-            const double pred = vj - b * rate[d];
-            sv[d][j] = vj - bm * (vnew[d] - pred);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int d = 0; d < D; ++d) sv[d][li] = vnew[d];
-      }
-      __syncwarp();
-    } else {
-      // pairwise split: palindromic chain of 2x2 solves at dt/4 (damping.cpp:161-176)
-      if (lane == 0) {
-        const double dt_pair = 0.5 * dt_half;
-        const double mi = sm[li];
-        double vi[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) vi[d] = sv[d][li];
-        for (int pass = 0; pass < 2; ++pass) {
-          const long long cnt = hi - lo;
-          for (long long t = 0; t < cnt; ++t) {
-            const long long s = pass == 0 ? lo + t : hi - 1 - t;
-            const double b = eta * f.pf[s] * dt_pair;
-            const int j = f.nloc[s];
-            const double mj = sm[j];
-            const double denom = mi * mj - (mi + mj) * b;
-            const double kf = b / denom;
-            const bool upd = !sf[j];
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-              const double vj = sv[d][j];
-              const double scaled = kf * (vi[d] - vj);
-              vi[d] = vi[d] + mj * scaled;
-              if (upd) sv[d][j] = vj - mi * scaled;
-            }
-          }
-        }
-#pragma unroll
-        for (int d = 0; d < D; ++d) sv[d][li] = vi[d];
-      }
-      __syncwarp();
-    }
-  }
-
-  // write the stencil back
-#pragma unroll
-  for (int q = 0; q < Stencil<D>::kSegs; ++q) {
-    const long long g0 = st.start[q];
-    const int b = st.base[q];
-    for (int e = lane; e < st.len[q]; e += kWarp) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) f.v[d][g0 + e] = sv[d][b + e];
-    }
-  }
-}
 
 // ------------------------------------------------------------------ single-particle operators
 template <int D>
@@ -334,68 +131,7 @@ __global__ void k_explicit_accel_loop(DFields f, double eta, double* __restrict_
   for (int d = 0; d < D; ++d) out[d * f.n + i] = k * acc[d];
 }
 
-template <int D, int SCHEME, bool ORDERED>
-void launch_phase(const DevSystem& s, const DFields& f, const Phase& ph) {
-  const size_t smem = kSweepWarps * warp_smem_bytes<D>(ph.stride);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    CK(cudaFuncSetAttribute(k_sweep_phase<D, SCHEME, ORDERED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    configured = smem;
-  }
-  k_sweep_phase<D, SCHEME, ORDERED><<<grid_for(ph.ncol, kSweepWarps), kSweepWarps * kWarp, smem, s.stream>>>(
-      f, ph, s.scal.p);
-}
-
-template <int D>
-void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_scal) {
-  if (!s.stencil_ok)
-    throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
-                   "damping sweep needs every neighbour inside the 3^D cell stencil (neighbors.hpp:50-52)");
-  const DFields f = s.fields();
-  Phase ph{};
-  ph.eta = eta;
-  ph.dt = dt;
-  ph.dt_from_scalars = from_scal ? 1 : 0;
-  ph.stride = (std::max(s.max_stencil, 1) + 7) & ~7;  // keeps every staged array 8-byte aligned
-  const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED;
-  constexpr int nb = colour_count<D>();
-  for (int pass = 0; pass < 2; ++pass) {
-    ph.forward = pass == 0;
-    for (int bb = 0; bb < nb; ++bb) {
-      const int b = pass == 0 ? bb : nb - 1 - bb;
-      int rem = b;
-      long long total = 1;
-      for (int d = 0; d < 3; ++d) {
-        if (d < D) {
-          ph.res[d] = rem % 3;
-          rem /= 3;
-          ph.cnt[d] = s.dims[d] > ph.res[d] ? (s.dims[d] - ph.res[d] + 2) / 3 : 0;
-        } else {
-          ph.res[d] = 0;
-          ph.cnt[d] = 1;
-        }
-        total *= ph.cnt[d];
-      }
-      ph.ncol = total;
-      if (total == 0) continue;  // empty colour (neighbors.cpp:152)
-      if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
-        if (ord) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, true>(s, f, ph);
-        else launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, false>(s, f, ph);
-      } else {
-        launch_phase<D, TLSPH_SCHEME_PAIRWISE_SPLIT, false>(s, f, ph);
-      }
-    }
-  }
-  CK_LAUNCH("k_sweep_phase");
-}
-
 }  // namespace
-
-void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars) {
-  if (D == 2) enqueue_sweep_d<2>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
-  else enqueue_sweep_d<3>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
-}
 
 void DevSystem::damping_sweep(int scheme, double eta_tilde, double dt, int count) {
   if (eta_tilde == 0.0) return;  // damping.cpp:132

@@ -188,6 +188,8 @@ __global__ void k_gather_init(DFields f, const double* __restrict__ r0aos, const
   f.rho0[s] = dens;
   f.rho[s] = dens;
   f.flag[s] = cons ? cons[i] : 0;
+  const double r = 1.0 / f.m[s];
+  f.minvf[s] = f.flag[s] ? -r : r;
 }
 
 // ------------------------------------------------------------------ neighbourhoods
@@ -350,6 +352,20 @@ __global__ void k_soa_to_aos(double* __restrict__ dst, int comps, long long n, c
   for (int c = 0; c < comps; ++c) dst[i * comps + c] = src[c][s];
 }
 
+__global__ void k_minvf(const double* __restrict__ m, const uint8_t* __restrict__ flag, double* __restrict__ y,
+                        long long n) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double r = 1.0 / m[s];
+  y[s] = flag[s] ? -r : r;
+}
+
+__global__ void k_cell_slot(const long long* __restrict__ cell_start, const long long* __restrict__ offs,
+                            long long ncells, long long* __restrict__ out) {
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c <= ncells) out[c] = offs[cell_start[c]];
+}
+
 __global__ void k_flag_in(const double* __restrict__ src, long long n, const int* __restrict__ perm, uint8_t* flag) {
   const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
@@ -437,6 +453,17 @@ __global__ void k_csr_from_ref(DFields f, const long long* __restrict__ off_ref,
   }
 }
 
+// Sizes of the sweep's shared-memory tile: slots per cell and per particle.
+__global__ void k_sweep_stats(const long long* __restrict__ cell_start, long long ncells,
+                              const long long* __restrict__ offs, long long n, unsigned long long* out) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < ncells) {
+    const long long s = offs[cell_start[t + 1]] - offs[cell_start[t]];
+    atomicMax(&out[0], static_cast<unsigned long long>(s));
+  }
+  if (t < n) atomicMax(&out[1], static_cast<unsigned long long>(offs[t + 1] - offs[t]));
+}
+
 __global__ void k_nloc_valid(const uint16_t* nloc, long long n, int* bad) {
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < n && nloc[k] == kNoLocal) atomicOr(bad, 1);
@@ -482,6 +509,11 @@ DFields DevSystem::fields() const {
   }
   f.V0 = V0.p;
   f.m = m.p;
+  f.minvf = minvf.p;
+  f.cell_slot = cell_slot.p;
+  f.fdiag = fold_diag.p;
+  f.fden = fold_den.p;
+  f.fy = fold_y.p;
   f.rho0 = rho0.p;
   f.rho = rho.p;
   f.flag = flag.p;
@@ -516,6 +548,10 @@ void DevSystem::alloc_fields() {
   }
   V0.alloc(N);
   m.alloc(N);
+  minvf.alloc(N);
+  fold_diag.alloc(N);
+  fold_den.alloc(N);
+  fold_y.alloc(N);
   rho0.alloc(N);
   rho.alloc(N);
   flag.alloc(N);
@@ -649,7 +685,7 @@ void DevSystem::build_neighbourhoods() {
   dwdr0.alloc(S);
   pf.alloc(S);
   nloc.alloc(S);
-  stencil_ok = max_stencil < kNoLocal;
+  stencil_ok = max_stencil < 0x8000;  // bit 15 of a staged index carries the clamp flag
   f = fields();
   const int cap = std::max(max_stencil, 1);
   const int warps = 4;
@@ -663,6 +699,29 @@ void DevSystem::build_neighbourhoods() {
   }
   CK_LAUNCH("k_nbr_fill");
   sync();
+  compute_sweep_stats();
+}
+
+void DevSystem::refresh_minvf() {
+  k_minvf<<<grid_for(n, 256), 256, 0, stream>>>(m.p, flag.p, minvf.p, n);
+  CK_LAUNCH("k_minvf");
+}
+
+void DevSystem::compute_sweep_stats() {
+  cell_slot.alloc(static_cast<size_t>(ncells + 1));
+  k_cell_slot<<<grid_for(ncells + 1, 256), 256, 0, stream>>>(cell_start.p, offs.p, ncells, cell_slot.p);
+  CK_LAUNCH("k_cell_slot");
+  DBuf<unsigned long long> out;
+  out.alloc(2);
+  CK(cudaMemsetAsync(out.p, 0, 2 * sizeof(unsigned long long), stream));
+  const long long m = std::max(ncells, n);
+  k_sweep_stats<<<grid_for(m, 256), 256, 0, stream>>>(cell_start.p, ncells, offs.p, n, out.p);
+  CK_LAUNCH("k_sweep_stats");
+  unsigned long long h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  sync();
+  max_cell_slots = static_cast<long long>(h[0]);
+  max_row = static_cast<int>(h[1]);
 }
 
 void DevSystem::load_csr(const int64_t* offsets, const int32_t* neighbor, const double* r0_len_h, const double* e0_h,
@@ -729,7 +788,8 @@ void DevSystem::load_csr(const int64_t* offsets, const int32_t* neighbor, const 
   int hbad = 0;
   CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
   sync();
-  stencil_ok = (hbad == 0) && max_stencil < kNoLocal;
+  stencil_ok = (hbad == 0) && max_stencil < 0x8000;
+  compute_sweep_stats();
 }
 
 namespace {
@@ -779,6 +839,7 @@ void DevSystem::set_field(int field, const double* host) {
     CK(cudaMemcpyAsync(tmp.p, host, N * sizeof(double), cudaMemcpyHostToDevice, stream));
     k_flag_in<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, n, perm.p, flag.p);
     CK_LAUNCH("k_flag_in");
+    refresh_minvf();
     sync();
     return;
   }
@@ -793,6 +854,10 @@ void DevSystem::set_field(int field, const double* host) {
   k_aos_to_soa<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, ptrs.p);
   CK_LAUNCH("k_aos_to_soa");
   if (field == TLSPH_FIELD_BODY) has_body = true;
+  if (field == TLSPH_FIELD_M) {
+    refresh_minvf();
+    fold_valid = false;  // diag = sum b - m_i
+  }
   sync();
 }
 

@@ -1,0 +1,612 @@
+// Colour-scheduled, operator-split implicit viscous damping sweep (the hot kernel).
+//
+// Reference: proj/src/tlsph/damping.cpp:53-182 (particle_split_update,
+// pairwise_split_update, strang_damping_sweep), neighbors.cpp:143-174
+// (block_sweep), neighbors.cpp:61-77 (3^D residue colouring).
+//
+// Per sweep: k_sweep_folds forms, for every particle, the reference-order
+// folds sum b and sum b^2 (b = eta G dt/2), diag = sum b - m_i,
+// denom = diag^2 + sum b^2 and RN(1/denom). They do not depend on the
+// velocities, so they are computed once, fully parallel, and reused by all
+// 2 x 3^D colour phases (and by later sweeps with the same eta and dt).
+//
+// Per colour phase, one launch. Colour b holds the cells whose coordinates
+// are congruent to b's residues mod 3 on every axis; their 3^D stencils are
+// disjoint (neighbors.hpp:50-52), so every cell is an independent task and
+// one 128-thread CTA owns one cell:
+//   1. staging by TMA: lanes of warp 0 locate the 3^(D-1) x-rows of the
+//      cell's stencil (contiguous in the cell-sorted arrays); v, m and the
+//      signed reciprocal mass (sign = clamp flag) of every row, the cell's
+//      CSR slot block (pair factor, stencil-local neighbour index), its row
+//      offsets and the per-particle fold constants arrive through 1-D bulk
+//      copies (cp.async.bulk of 16-byte aligned supersets) on one mbarrier:
+//      one HBM latency per cell. The tile is sized so every cell of a colour
+//      is resident at once (one wave);
+//   2. the chain: the cell's particles in order (ascending id forward,
+//      descending on the reverse leg, damping.cpp:112-121). The particle-split
+//      update is separable per velocity component once diag and denom are
+//      known, so warp d runs the whole chain of component d with no
+//      synchronisation between warps. Lane l owns slots l, l+32, ... (K per
+//      lane, branch-free, next particle's slot metadata prefetched); the
+//      residual is reduced with warp shuffles (FAST) or folded by lane 0 in
+//      slot order (ORDERED, bit-exact with the reference); rate = residual /
+//      denom and the momentum-conserving neighbour correction follow from
+//      registers;
+//   3. write-back of the stencil velocities by all threads (disjoint
+//      stencils: no races).
+// Pairwise split: the same staging; warp d computes the per-slot
+// b/(m_i m_j - (m_i+m_j) b) of particle i and its lane 0 runs the palindromic
+// pair chain (damping.cpp:161-176) of component d (components never mix in
+// the 2x2 solve).
+//
+// Division. B200 IEEE fp64 division costs ~425 cycles of dependent latency
+// (tools/fp64_latency.cu), so no division sits on the chain:
+//   ORDERED: x/d with d known ahead uses y = RN(1/d) and one Markstein
+//            correction, q0 = RN(x y), r = fma(-d, q0, x) (exact),
+//            q = RN(q0 + r y) = RN(x/d) (Markstein's theorem for a correctly
+//            rounded reciprocal; checked bit-for-bit against IEEE division by
+//            tlsph_dev_selftest_division and the ORDERED parity tests);
+//   FAST:    x * y (<= 1 ulp), within the 1e-10 north_star class.
+#include <algorithm>
+#include <cmath>
+
+#include "system.cuh"
+#include "tma.cuh"
+
+namespace tlsph_cuda {
+
+namespace {
+
+constexpr int kThreads = 128;  // one CTA per cell
+
+struct Phase {
+  int res[3];      // colour residues per axis
+  int cnt[3];      // cells of this colour per axis
+  long long ncol;  // cells in the colour
+  int forward;
+  int S;           // padded stencil tile length, multiple of 8
+  int SC;          // max slots per cell, multiple of 8
+  int MC;          // max particles per cell, even
+  int MR;          // pairwise scratch per warp (max slots per particle), 0 for particle split
+  double eta;
+  double dt;       // used when dt_from_scalars == 0
+  int dt_from_scalars;
+};
+
+template <int D>
+__host__ __device__ constexpr int colour_count() { return D == 2 ? 9 : 27; }
+template <int D>
+__host__ __device__ constexpr int seg_count() { return D == 2 ? 3 : 9; }
+
+// Shared-memory tile of one cell; every section is a multiple of 16 bytes.
+template <int D>
+struct Tile {
+  uint64_t* bar;
+  long long* seg_start;  // per stencil row: first particle
+  int* seg_len;
+  int* seg_base;         // tile position of the first particle
+  double* sv[D];         // stencil velocities
+  double* sm;            // stencil masses
+  double* smf;           // stencil signed RN(1/m) (negative: clamped)
+  long long* soff;       // aligned superset of offs[p0..p1]
+  double* sdiag;         // aligned supersets of the fold constants of p0..p1-1
+  double* sden;
+  double* sy;
+  double* spf;           // aligned superset of the cell's pair factors
+  double* skf;           // pairwise scratch, D x MR
+  uint16_t* snl;         // aligned superset of stencil-local neighbour indices
+};
+
+__host__ __device__ inline int mco(int MC) { return (MC + 4) & ~1; }
+constexpr int kHeader = 16 + 16 * 9;  // barrier + spare word + segment table
+
+template <int D>
+__host__ __device__ inline size_t tile_bytes(int S, int SC, int MC, int MR) {
+  size_t b = kHeader;
+  b += sizeof(double) * (static_cast<size_t>(D + 2) * S);
+  b += sizeof(long long) * static_cast<size_t>(mco(MC));
+  b += sizeof(double) * static_cast<size_t>(3 * mco(MC));
+  b += sizeof(double) * static_cast<size_t>(SC + 2);
+  b += sizeof(double) * static_cast<size_t>(D * MR);
+  b += sizeof(uint16_t) * static_cast<size_t>(SC + 16);
+  return (b + 15) & ~static_cast<size_t>(15);
+}
+
+template <int D>
+__device__ inline Tile<D> carve(unsigned char* base, const Phase& ph) {
+  Tile<D> t;
+  const int mc = mco(ph.MC);
+  t.bar = reinterpret_cast<uint64_t*>(base);
+  t.seg_start = reinterpret_cast<long long*>(base + 16);
+  t.seg_len = reinterpret_cast<int*>(base + 16 + 8 * 9);
+  t.seg_base = reinterpret_cast<int*>(base + 16 + 12 * 9);
+  double* d = reinterpret_cast<double*>(base + kHeader);
+#pragma unroll
+  for (int k = 0; k < D; ++k) t.sv[k] = d + static_cast<size_t>(k) * ph.S;
+  t.sm = d + static_cast<size_t>(D) * ph.S;
+  t.smf = t.sm + ph.S;
+  t.soff = reinterpret_cast<long long*>(t.smf + ph.S);
+  t.sdiag = reinterpret_cast<double*>(t.soff + mc);
+  t.sden = t.sdiag + mc;
+  t.sy = t.sden + mc;
+  t.spf = t.sy + mc;
+  t.skf = t.spf + ph.SC + 2;
+  t.snl = reinterpret_cast<uint16_t*>(t.skf + static_cast<size_t>(D) * ph.MR);
+  return t;
+}
+
+// RN(x/d) from y = RN(1/d) (see the file comment).
+__device__ __forceinline__ double div_by(double x, double d, double y) {
+  const double q0 = x * y;
+  const double r = __fma_rn(-d, q0, x);
+  return r == 0.0 ? q0 : __fma_rn(r, y, q0);
+}
+
+template <bool ORDERED>
+__device__ __forceinline__ double quot(double x, double d, double y) {
+  return ORDERED ? div_by(x, d, y) : x * y;
+}
+
+constexpr unsigned kFull = 0xffffffffu;
+
+#ifdef TLSPH_SWEEP_TIMING
+// Debug build only: %globaltimer stamps of each cell task's stages.
+__device__ unsigned long long g_sweep_stamp[1 << 16][8];
+__device__ __forceinline__ void stamp(long long cell, int k) {
+  if (threadIdx.x == 0 && cell < (1 << 16)) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sweep_stamp[cell][k] = t;
+  }
+}
+#else
+__device__ __forceinline__ void stamp(long long, int) {}
+#endif
+
+// ------------------------------------------------------------------ per-sweep folds
+// damping.cpp:65-74: sum_b, sum_b2 in slot order, diag, denominator (its
+// reciprocal feeds the corrected division on the chain).
+__global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_from_scalars,
+                              const DScalars* __restrict__ sc) {
+  if (dt_from_scalars && sc->halt) return;
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  const double dt_half = 0.5 * (dt_from_scalars ? sc->dt : dt_fixed);
+  double sb = 0.0, sb2 = 0.0;
+  const long long hi = f.offs[i + 1];
+  for (long long s = f.offs[i]; s < hi; ++s) {
+    const double b = eta * f.pf[s] * dt_half;
+    sb = sb + b;
+    sb2 = sb2 + b * b;
+  }
+  const double diag = sb - f.m[i];
+  const double den = diag * diag + sb2;
+  f.fdiag[i] = diag;
+  f.fden[i] = den;
+  f.fy[i] = 1.0 / den;
+}
+
+// ------------------------------------------------------------------ colour phase
+// K > 0: rows up to 32 K slots run the branch-free register path; K = 0: generic loop only.
+template <int D, int SCHEME, bool ORDERED, int K>
+__global__ void __launch_bounds__(kThreads)
+k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
+  if (ph.dt_from_scalars && sc->halt) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid / kWarp, lane = tid % kWarp;
+  const long long k = blockIdx.x;
+  stamp(k, 0);
+  int c[3];
+  c[0] = ph.res[0] + 3 * static_cast<int>(k % ph.cnt[0]);
+  c[1] = ph.res[1] + 3 * static_cast<int>((k / ph.cnt[0]) % ph.cnt[1]);
+  c[2] = D == 3 ? ph.res[2] + 3 * static_cast<int>(k / (static_cast<long long>(ph.cnt[0]) * ph.cnt[1])) : 0;
+  constexpr int kSegs = seg_count<D>();
+  Tile<D> t = carve<D>(smem, ph);
+  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
+  const double dt_half = 0.5 * dt;
+  const double dt_op = SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT ? dt_half : 0.5 * dt_half;  // pair step dt/4
+  const double eta = ph.eta;
+
+  // ---- 1. staging. All index loads are issued before any of them is used.
+  const long long lin = cell_linear<D>(c, f.dims);
+  const long long p0 = f.cell_start[lin], p1 = f.cell_start[lin + 1];
+  const long long s0 = f.cell_slot[lin], s1 = f.cell_slot[lin + 1];
+  long long sstart = 0, send = 0;
+  if (warp == 0 && lane < kSegs) {  // lane q locates stencil row q
+    const int dy = (D == 2 ? lane : lane % 3) - 1;
+    const int dz = D == 2 ? 0 : lane / 3 - 1;
+    const int y = c[1] + dy;
+    const int z = c[2] + dz;
+    bool ok = y >= 0 && y < f.dims[1];
+    if (D == 3) ok = ok && z >= 0 && z < f.dims[2];
+    if (ok) {
+      const int xlo = c[0] > 0 ? c[0] - 1 : 0;
+      const int xhi = c[0] + 1 < f.dims[0] ? c[0] + 1 : f.dims[0] - 1;
+      const long long row = D == 3 ? (static_cast<long long>(z) * f.dims[1] + y) * f.dims[0]
+                                   : static_cast<long long>(y) * f.dims[0];
+      sstart = f.cell_start[row + xlo];
+      send = f.cell_start[row + xhi + 1];
+    }
+  }
+  if (p0 == p1) return;  // empty cell (uniform across the CTA)
+  stamp(k, 6);
+  const int np = static_cast<int>(p1 - p0);
+  const long long o0 = p0 & ~1ll, o1 = (p1 + 2) & ~1ll;  // offs[p0..p1] superset
+  const long long q0 = p0 & ~1ll, q1 = (p1 + 1) & ~1ll;  // fold constants of p0..p1-1
+  const long long f0 = s0 & ~1ll, f1 = (s1 + 1) & ~1ll;  // pair factors
+  const long long n0 = s0 & ~7ll, n1 = (s1 + 7) & ~7ll;  // u16 neighbour indices
+  if (warp == 0) {
+    const int slen = static_cast<int>(send - sstart);
+    // padded tile layout: exclusive scan of the 16-byte aligned row lengths (as stencil_segments)
+    const int par = static_cast<int>(sstart & 1);
+    const int plen = slen > 0 ? ((slen + par + 1) & ~1) : 0;
+    int incl = plen;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const int x = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += x;
+    }
+    const int sbase = incl - plen + par;
+    if (lane < kSegs) {
+      t.seg_start[lane] = sstart;
+      t.seg_len[lane] = slen;
+      t.seg_base[lane] = sbase;
+    }
+    const bool fold = SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT;
+    uint32_t mybytes = 0;
+    if (lane < kSegs && slen > 0) mybytes = static_cast<uint32_t>(plen * 8 * (D + 2));
+    else if (lane == kSegs) mybytes = static_cast<uint32_t>((o1 - o0) * 8);
+    else if (lane == kSegs + 1) mybytes = static_cast<uint32_t>((f1 - f0) * 8);
+    else if (lane == kSegs + 2) mybytes = static_cast<uint32_t>((n1 - n0) * 2);
+    else if (fold && lane == kSegs + 3) mybytes = static_cast<uint32_t>((q1 - q0) * 8 * 3);
+    uint32_t total = mybytes;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+    if (lane == 0) {
+      mbar_init(t.bar, 1);
+      fence_proxy_async_smem();  // the initialised barrier is visible to the TMA unit
+      mbar_arrive_expect_tx(t.bar, total);
+    }
+    __syncwarp();
+    if (lane < kSegs && slen > 0) {
+      const long long a0 = sstart - par;
+      const int dst = sbase - par;
+      const uint32_t nb = static_cast<uint32_t>(plen * 8);
+#pragma unroll
+      for (int d = 0; d < D; ++d) tma_load_1d(t.sv[d] + dst, f.v[d] + a0, nb, t.bar);
+      tma_load_1d(t.sm + dst, f.m + a0, nb, t.bar);
+      tma_load_1d(t.smf + dst, f.minvf + a0, nb, t.bar);
+    } else if (lane == kSegs) {
+      tma_load_1d(t.soff, f.offs + o0, mybytes, t.bar);
+    } else if (lane == kSegs + 1) {
+      tma_load_1d(t.spf, f.pf + f0, mybytes, t.bar);
+    } else if (lane == kSegs + 2) {
+      tma_load_1d(t.snl, f.nloc + n0, mybytes, t.bar);
+    } else if (fold && lane == kSegs + 3) {
+      const uint32_t nb = static_cast<uint32_t>((q1 - q0) * 8);
+      tma_load_1d(t.sdiag, f.fdiag + q0, nb, t.bar);
+      tma_load_1d(t.sden, f.fden + q0, nb, t.bar);
+      tma_load_1d(t.sy, f.fy + q0, nb, t.bar);
+    }
+    constexpr int center = D == 2 ? 1 : 4;
+    const int lbase = __shfl_sync(kFull, sbase, center) + static_cast<int>(p0 - __shfl_sync(kFull, sstart, center));
+    if (lane == 0) reinterpret_cast<int*>(t.bar + 1)[0] = lbase;  // the centre row holds the cell's particles
+  }
+  stamp(k, 1);
+  __syncthreads();  // barrier initialised before anyone waits on it
+  mbar_wait(t.bar, 0);
+  stamp(k, 2);
+  const int lbase = reinterpret_cast<const int*>(t.bar + 1)[0];
+  const long long* offc = t.soff + (p0 - o0);  // offc[k] = offs[p0 + k]
+  const double* pfc = t.spf + (s0 - f0);
+  const uint16_t* nlc = t.snl + (s0 - n0);
+  const double* fdg = t.sdiag + (p0 - q0);
+  const double* fdn = t.sden + (p0 - q0);
+  const double* fyy = t.sy + (p0 - q0);
+  stamp(k, 3);
+
+  // ---- 2. the chain: warp d owns velocity component d
+  if (warp < D) {
+    double* const vd = t.sv[0] + static_cast<size_t>(warp) * ph.S;
+    if (SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT) {
+      constexpr int KK = K > 0 ? K : 1;
+      // metadata of the next particle in chain order; none of it depends on the chain
+      int pk_n = ph.forward ? 0 : np - 1;
+      int lo_n = static_cast<int>(offc[pk_n] - s0), cnt_n = static_cast<int>(offc[pk_n + 1] - s0) - lo_n;
+      int jq_n[KK];
+      bool up_n[KK];
+      double b_n[KK], bm_n[KK];
+      auto meta = [&](int lo_, int cnt_, int li_, int* jq, bool* up, double* b, double* bm) {
+#pragma unroll
+        for (int u = 0; u < KK; ++u) {
+          const int s = lane + u * kWarp;
+          const bool v = s < cnt_;
+          const int j = v ? nlc[lo_ + s] : li_;  // invalid lanes point at i itself with b = 0
+          const double mf = t.smf[j];
+          jq[u] = j;
+          up[u] = v && mf > 0.0;  // clamped j: writes discarded (damping.cpp:84-86)
+          b[u] = v ? eta * pfc[lo_ + s] * dt_op : 0.0;
+          bm[u] = up[u] ? quot<ORDERED>(b[u], t.sm[j], mf) : 0.0;
+        }
+      };
+      meta(lo_n, cnt_n, lbase + pk_n, jq_n, up_n, b_n, bm_n);
+      for (int kk = 0; kk < np; ++kk) {
+        const int pk = pk_n, lo = lo_n, cnt = cnt_n;
+        int jq[KK];
+        bool up[KK];
+        double bq[KK], bmq[KK];
+#pragma unroll
+        for (int u = 0; u < KK; ++u) {
+          jq[u] = jq_n[u];
+          up[u] = up_n[u];
+          bq[u] = b_n[u];
+          bmq[u] = bm_n[u];
+        }
+        if (kk + 1 < np) {  // next particle's metadata, off the chain
+          pk_n = ph.forward ? kk + 1 : np - 2 - kk;
+          lo_n = static_cast<int>(offc[pk_n] - s0);
+          cnt_n = static_cast<int>(offc[pk_n + 1] - s0) - lo_n;
+          meta(lo_n, cnt_n, lbase + pk_n, jq_n, up_n, b_n, bm_n);
+        }
+        const int li = lbase + pk;
+        if (t.smf[li] < 0.0 || cnt == 0) continue;  // constrained i (damping.cpp:151) / no neighbours (:54)
+        const double diag = fdg[pk], den = fdn[pk], y = fyy[pk];
+        const double vi = vd[li];
+        double R = 0.0;
+        double rate, vnew;
+        if (K > 0 && cnt <= K * kWarp) {
+          double vq[KK];
+#pragma unroll
+          for (int u = 0; u < KK; ++u) vq[u] = vd[jq[u]];
+          if (ORDERED) {
+            if (lane == 0) {
+              for (int s = lo; s < lo + cnt; ++s) {
+                const double b = eta * pfc[s] * dt_op;
+                R = R - b * (vi - vd[nlc[s]]);
+              }
+            }
+            R = __shfl_sync(kFull, R, 0);
+          } else {
+            double r = 0.0;
+#pragma unroll
+            for (int u = 0; u < KK; ++u) r = r - bq[u] * (vi - vq[u]);
+            R = warp_sum(r);
+          }
+          rate = quot<ORDERED>(R, den, y);
+          vnew = vi + diag * rate;
+#pragma unroll
+          for (int u = 0; u < KK; ++u) {
+            const double pred = vq[u] - bq[u] * rate;
+            const double nv = vq[u] - bmq[u] * (vnew - pred);
+            if (up[u]) vd[jq[u]] = nv;
+          }
+        } else {
+          // long rows (irregular bodies): strided loop
+          if (ORDERED) {
+            if (lane == 0) {
+              for (int s = lo; s < lo + cnt; ++s) {
+                const double b = eta * pfc[s] * dt_op;
+                R = R - b * (vi - vd[nlc[s]]);
+              }
+            }
+            R = __shfl_sync(kFull, R, 0);
+          } else {
+            double r = 0.0;
+            for (int s = lo + lane; s < lo + cnt; s += kWarp) {
+              const double b = eta * pfc[s] * dt_op;
+              r = r - b * (vi - vd[nlc[s]]);
+            }
+            R = warp_sum(r);
+          }
+          rate = quot<ORDERED>(R, den, y);
+          vnew = vi + diag * rate;
+          __syncwarp();
+          for (int s = lo + lane; s < lo + cnt; s += kWarp) {
+            const int j = nlc[s];
+            const double mf = t.smf[j];
+            if (mf > 0.0) {
+              const double b = eta * pfc[s] * dt_op;
+              const double bm = quot<ORDERED>(b, t.sm[j], mf);
+              const double vj = vd[j];
+              const double pred = vj - b * rate;
+              vd[j] = vj - bm * (vnew - pred);
+            }
+          }
+        }
+        // i is not its own neighbour, so this store cannot race the scatter above
+        if (lane == 0) vd[li] = vnew;
+        __syncwarp();
+      }
+    } else {
+      // pairwise split (damping.cpp:91-106, palindrome :171-176): lane 0 of warp d runs component d
+      double* const kf_scr = t.skf + static_cast<size_t>(warp) * ph.MR;
+      for (int kk = 0; kk < np; ++kk) {
+        const int pk = ph.forward ? kk : np - 1 - kk;
+        const int li = lbase + pk;
+        if (t.smf[li] < 0.0) continue;
+        const int lo = static_cast<int>(offc[pk] - s0), cnt = static_cast<int>(offc[pk + 1] - s0) - lo;
+        const double mi = t.sm[li];
+        for (int s = lane; s < cnt; s += kWarp) {
+          const double b = eta * pfc[lo + s] * dt_op;
+          const double mj = t.sm[nlc[lo + s]];
+          const double denom = mi * mj - (mi + mj) * b;
+          kf_scr[s] = b / denom;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          double vi = vd[li];
+          for (int pass = 0; pass < 2; ++pass) {
+            for (int u = 0; u < cnt; ++u) {
+              const int s = pass == 0 ? u : cnt - 1 - u;
+              const int j = nlc[lo + s];
+              const double kf = kf_scr[s];
+              const double mj = t.sm[j];
+              const double vj = vd[j];
+              const double scaled = kf * (vi - vj);
+              vi = vi + mj * scaled;
+              if (t.smf[j] > 0.0) vd[j] = vj - mi * scaled;
+            }
+          }
+          vd[li] = vi;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  stamp(k, 4);
+  __syncthreads();
+
+  // ---- 3. write the stencil back (rows from the tile's segment table)
+  for (int q = 0; q < kSegs; ++q) {
+    const long long g0 = t.seg_start[q];
+    const int b = t.seg_base[q], len = t.seg_len[q];
+    for (int e = tid; e < len; e += kThreads) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) f.v[d][g0 + e] = t.sv[d][b + e];
+    }
+  }
+  stamp(k, 5);
+}
+
+template <int D, int SCHEME, bool ORDERED, int K>
+void launch_phase(const DevSystem& s, const DFields& f, const Phase& ph) {
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    CK(cudaFuncSetAttribute(k_sweep_phase<D, SCHEME, ORDERED, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    configured = smem;
+  }
+  k_sweep_phase<D, SCHEME, ORDERED, K><<<static_cast<unsigned>(ph.ncol), kThreads, smem, s.stream>>>(f, ph,
+                                                                                                    s.scal.p);
+}
+
+template <int D, bool ORDERED>
+void launch_particle_split(const DevSystem& s, const DFields& f, const Phase& ph) {
+  // slots per lane kept in registers: the smallest K that covers the longest row
+  const int K = (s.max_row + kWarp - 1) / kWarp;
+  if (K <= 1) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 1>(s, f, ph);
+  else if (K <= 2) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 2>(s, f, ph);
+  else if (K <= 3) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 3>(s, f, ph);
+  else if (K <= 4) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 4>(s, f, ph);
+  else launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 0>(s, f, ph);
+}
+
+constexpr size_t kSmemBudget = 220 * 1024;
+
+template <int D>
+void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_scal) {
+  if (!s.stencil_ok)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
+                   "damping sweep needs every neighbour inside the 3^D cell stencil (neighbors.hpp:50-52)");
+  const DFields f = s.fields();
+  Phase ph{};
+  ph.eta = eta;
+  ph.dt = dt;
+  ph.dt_from_scalars = from_scal ? 1 : 0;
+  ph.S = (std::max(s.max_stencil, 1) + 7) & ~7;
+  ph.SC = (std::max<int>(static_cast<int>(s.max_cell_slots), 1) + 7) & ~7;
+  ph.MC = (std::max(s.max_cell, 1) + 1) & ~1;
+  ph.MR = scheme == TLSPH_SCHEME_PAIRWISE_SPLIT ? ((std::max(s.max_row, 1) + 1) & ~1) : 0;
+  const size_t per_cell = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR);
+  if (per_cell > kSmemBudget)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
+                   "damping sweep: a cell's stencil and slot block (" + std::to_string(per_cell) +
+                       " bytes) exceed the shared-memory tile");
+  if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
+    // per-sweep fold constants; reused while (eta, dt) are unchanged
+    if (from_scal || !s.fold_valid || s.fold_eta != eta || s.fold_dt != dt) {
+      k_sweep_folds<<<static_cast<unsigned>((s.n + 127) / 128), 128, 0, s.stream>>>(f, eta, dt, from_scal ? 1 : 0,
+                                                                                    s.scal.p);
+      CK_LAUNCH("k_sweep_folds");
+      s.fold_valid = !from_scal;
+      s.fold_eta = eta;
+      s.fold_dt = dt;
+    }
+  }
+  const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED;
+  constexpr int nb = colour_count<D>();
+  for (int pass = 0; pass < 2; ++pass) {
+    ph.forward = pass == 0;
+    for (int bb = 0; bb < nb; ++bb) {
+      const int b = pass == 0 ? bb : nb - 1 - bb;
+      int rem = b;
+      long long total = 1;
+      for (int d = 0; d < 3; ++d) {
+        if (d < D) {
+          ph.res[d] = rem % 3;
+          rem /= 3;
+          ph.cnt[d] = s.dims[d] > ph.res[d] ? (s.dims[d] - ph.res[d] + 2) / 3 : 0;
+        } else {
+          ph.res[d] = 0;
+          ph.cnt[d] = 1;
+        }
+        total *= ph.cnt[d];
+      }
+      ph.ncol = total;
+      if (total == 0) continue;  // empty colour (neighbors.cpp:152)
+      if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
+        if (ord) launch_particle_split<D, true>(s, f, ph);
+        else launch_particle_split<D, false>(s, f, ph);
+      } else {
+        launch_phase<D, TLSPH_SCHEME_PAIRWISE_SPLIT, false, 0>(s, f, ph);
+      }
+    }
+  }
+  CK_LAUNCH("k_sweep_phase");
+}
+
+// Bit-for-bit check of div_by against IEEE division on the device.
+__global__ void k_selftest_division(unsigned long long seed, long long n, unsigned long long* bad) {
+  unsigned long long s = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1));
+  auto next = [&]() {
+    s ^= s << 13;
+    s ^= s >> 7;
+    s ^= s << 17;
+    return s;
+  };
+  unsigned long long local = 0;
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long ea = 1023 - 40 + next() % 81, eb = 1023 - 40 + next() % 81;
+    unsigned long long ma = next(), mb = next();
+    if (next() & 1) ma &= 0xFFFF;
+    if (next() & 1) mb |= 0xFFFFFFFFFFFF0ull;
+    const double a = __longlong_as_double(static_cast<long long>((ea << 52) | (ma & 0xFFFFFFFFFFFFFull) |
+                                                                 ((next() & 1) << 63)));
+    const double b = __longlong_as_double(static_cast<long long>((eb << 52) | (mb & 0xFFFFFFFFFFFFFull)));
+    const double y = 1.0 / b;
+    if (div_by(a, b, y) != a / b) ++local;
+  }
+  if (local) atomicAdd(bad, local);
+}
+
+}  // namespace
+
+void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars) {
+  if (D == 2) enqueue_sweep_d<2>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
+  else enqueue_sweep_d<3>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
+}
+
+unsigned long long selftest_division(long long n, unsigned long long seed) {
+  DBuf<unsigned long long> bad;
+  bad.alloc(1);
+  CK(cudaMemset(bad.p, 0, sizeof(unsigned long long)));
+  k_selftest_division<<<592, 256>>>(seed, n, bad.p);
+  CK_LAUNCH("k_selftest_division");
+  unsigned long long h = 0;
+  CK(cudaMemcpy(&h, bad.p, sizeof(h), cudaMemcpyDeviceToHost));
+  return h;
+}
+
+}  // namespace tlsph_cuda
+
+#ifdef TLSPH_SWEEP_TIMING
+extern "C" int tlsph_debug_sweep_stamps(unsigned long long* out, int cells) {
+  const int n = cells < (1 << 16) ? cells : (1 << 16);
+  return cudaMemcpyFromSymbol(out, tlsph_cuda::g_sweep_stamp, sizeof(unsigned long long) * 8 * n) == cudaSuccess
+             ? n
+             : -1;
+}
+#endif

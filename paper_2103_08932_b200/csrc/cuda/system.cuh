@@ -28,7 +28,9 @@ struct DBuf {
     release();
     n = count;
     cap = count;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    // 16 elements of slack: the sweep's TMA stages 16-byte aligned supersets
+    // of particle/slot ranges, which may read just past the last element.
+    if (count) CK(cudaMalloc(&p, (count + 16) * sizeof(T)));
   }
   void release() {
     if (p) cudaFree(p);
@@ -56,12 +58,19 @@ class DevSystem {
   long long ncells = 0;
   int max_cell = 0;     // max particles per cell
   int max_stencil = 0;  // max particles in a staged 3^D stencil
+  long long max_cell_slots = 0;  // max CSR slots owned by one cell
+  int max_row = 0;               // max slots of one particle
   bool stencil_ok = true;
 
   // fields (sorted order)
   DBuf<double> r0[3], r[3], v[3], a[3], body[3];
   DBuf<double> F[9], dFdt[9], B0[9], PB[9];
-  DBuf<double> V0, m, rho0, rho;
+  DBuf<double> V0, m, minvf, rho0, rho;
+  DBuf<long long> cell_slot;
+  // per-sweep particle-split constants and the (eta, dt) they were formed for
+  DBuf<double> fold_diag, fold_den, fold_y;
+  bool fold_valid = false;
+  double fold_eta = 0.0, fold_dt = 0.0;
   DBuf<uint8_t> flag;
   DBuf<int> perm, rank;
   DBuf<long long> cell_start;
@@ -93,6 +102,8 @@ class DevSystem {
   void build_neighbourhoods();
   void load_csr(const int64_t* offsets, const int32_t* neighbor, const double* r0_len_h, const double* e0_h,
                 const double* dwdr0_h, const double* pf_h);
+  void compute_sweep_stats();
+  void refresh_minvf();
 
   // transfers (state.cu)
   void set_field(int field, const double* host);
@@ -133,6 +144,7 @@ class DevSystem {
 };
 
 DMaterial to_dmat(const tlsph_dev_material& m);
+unsigned long long selftest_division(long long n, unsigned long long seed);  // sweep.cu
 
 // kernels shared across translation units
 void launch_reduce_state(const DevSystem& s, bool with_finite, bool with_ke, bool dt_mode);

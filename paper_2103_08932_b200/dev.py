@@ -26,7 +26,7 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_PKG, "lib")
-CUDA_LIB = os.path.join(LIB_DIR, "libtlsph_cuda.so")
+CUDA_LIB = os.environ.get("TLSPH_CUDA_LIB", os.path.join(LIB_DIR, "libtlsph_cuda.so"))
 
 STATUS = {0: "ok", 1: "invalid-argument", 2: "parse-error", 3: "degenerate-geometry", 4: "inverted-element",
           5: "numerical-failure", 6: "io-error", 7: "internal-error"}
@@ -129,6 +129,7 @@ def lib():
     L.tlsph_random_choice.argtypes = [C.c_double, C.c_double, C.c_uint64, S, D]
     L.tlsph_dev_last_elapsed.argtypes = [P]
     L.tlsph_dev_last_elapsed.restype = C.c_double
+    L.tlsph_dev_selftest_division.argtypes = [C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]
     _lib = L
     return L
 
@@ -149,6 +150,13 @@ def device_count() -> int:
 def select_device(ordinal: int) -> None:
     """Device for handles created afterwards (one process per GPU: LOCAL_RANK)."""
     _check(lib().tlsph_dev_select_device(ordinal))
+
+
+def selftest_division(n=1 << 26, seed=1):
+    """Mismatches of the corrected quotient against IEEE division on the device (expected 0)."""
+    out = C.c_uint64()
+    _check(lib().tlsph_dev_selftest_division(n, seed, C.byref(out)))
+    return int(out.value)
 
 
 def random_uniforms(seed, n):

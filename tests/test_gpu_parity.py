@@ -227,6 +227,11 @@ def test_check_finite_message():
 
 
 # ---------------------------------------------------------------- damping sweep
+def test_corrected_division_is_ieee_on_device():
+    # RN(x/d) via y = RN(1/d) + one Markstein correction, used off the chain
+    assert dev.selftest_division(1 << 26, 7) == 0
+
+
 @pytest.mark.parametrize("scheme", ["particle_split", "pairwise_split"])
 @pytest.mark.parametrize("dim", [2, 3])
 def test_sweep_ordered_bit_exact(scheme, dim):
