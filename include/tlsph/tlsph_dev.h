@@ -100,6 +100,11 @@ tlsph_status tlsph_dev_create_with_csr(int dim, size_t n, const double* r0, cons
                                        const int32_t* neighbor, const double* r0_len, const double* e0,
                                        const double* dwdr0, const double* pair_factor, tlsph_dev** out);
 
+/* Cell grid only (build_cell_grid, neighbors.cpp:24-59): bins `positions`
+ * with cell = cutoff; no neighbourhood is built, so coincident points are
+ * allowed. Query it with tlsph_dev_grid_info / tlsph_dev_grid_cells. */
+tlsph_status tlsph_dev_create_grid(int dim, size_t n, const double* positions, double cutoff, tlsph_dev** out);
+
 void tlsph_dev_destroy(tlsph_dev* dev);
 
 size_t tlsph_dev_size(const tlsph_dev* dev);
@@ -109,6 +114,12 @@ int64_t tlsph_dev_slot_count(const tlsph_dev* dev);
 tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const double* host);
 tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host);
 tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode);
+
+/* Penalty contact plane of ExternalAccel<D> (forces.hpp:13-39): a_i +=
+ * stiffness * max(0, -(r_i - point).normal) / m_i * normal, evaluated at the
+ * current position inside the momentum RHS. stiffness <= 0 removes it. */
+tlsph_status tlsph_dev_set_contact_plane(tlsph_dev* dev, const double* point, const double* normal,
+                                         double stiffness);
 
 /* CellGrid<D> (neighbors.hpp:18-48): dims[D], origin[D], cell_size, number of cells. */
 tlsph_status tlsph_dev_grid_info(const tlsph_dev* dev, int* dims, double* origin, double* cell_size,
@@ -162,6 +173,15 @@ typedef struct tlsph_dev_loop_params {
   int elastic;           /* 1: verlet_step every step; 0: damping-only loop */
   int ke_stop;           /* 1: stop at the first step with KE < ke_ratio * peak KE after the peak */
   double ke_ratio;
+  /* probe output (runner.cpp:381-390): every step whose t reaches the next
+   * output mark appends (t, r[probe] - r0[probe]) to `probe_out`
+   * (capacity `probe_capacity` samples of 4 doubles: t, u0, u1, u2). */
+  int64_t probe_index;   /* reference index; < 0 disables probe output */
+  double output_interval;
+  double* probe_out;
+  size_t probe_capacity;
+  int pause_on_mark;     /* 1: return after each recorded mark (snapshots "all"); resume with resume = 1 */
+  int resume;            /* 1: continue the paused loop (same eta~ stream, t, step count) */
 } tlsph_dev_loop_params;
 
 typedef struct tlsph_dev_loop_result {
@@ -175,6 +195,8 @@ typedef struct tlsph_dev_loop_result {
   double peak_ke;
   double final_ke;
   int stopped_on_ke;
+  size_t probe_samples;  /* samples written to probe_out (cumulative across resumes) */
+  int paused;            /* 1: stopped at an output mark with pause_on_mark set */
 } tlsph_dev_loop_result;
 
 /* Runs the loop with all state resident on the device; the eta~ sequence is

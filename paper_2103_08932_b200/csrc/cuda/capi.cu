@@ -114,6 +114,40 @@ tlsph_status tlsph_dev_create_with_csr(int dim, size_t n, const double* r0, cons
   });
 }
 
+tlsph_status tlsph_dev_create_grid(int dim, size_t n, const double* positions, double cutoff, tlsph_dev** out) {
+  if (!out) {
+    g_dev_err = "out must not be null";
+    return TLSPH_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (!(cutoff > 0.0)) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "cell grid cutoff must be positive");
+    if (n == 0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "cell grid needs at least one particle");
+    const std::vector<double> ones(n, 1.0);
+    auto d = new_handle();
+    d->sys.init_common(dim, n, positions, ones.data(), ones.data(), nullptr, 0.5 * cutoff);
+    *out = d.release();
+  });
+}
+
+tlsph_status tlsph_dev_set_contact_plane(tlsph_dev* dev, const double* point, const double* normal,
+                                         double stiffness) {
+  return guarded([&] {
+    DevSystem& s = sys(dev);
+    if (!(stiffness > 0.0)) {
+      s.contact = false;
+      return;
+    }
+    if (!point || !normal) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "point and normal must not be null");
+    for (int d = 0; d < 3; ++d) {
+      s.cp_point[d] = d < s.D ? point[d] : 0.0;
+      s.cp_normal[d] = d < s.D ? normal[d] : 0.0;
+    }
+    s.cp_k = stiffness;
+    s.contact = true;
+  });
+}
+
 void tlsph_dev_destroy(tlsph_dev* dev) { delete dev; }
 
 size_t tlsph_dev_size(const tlsph_dev* dev) { return dev ? static_cast<size_t>(dev->sys.n) : 0; }

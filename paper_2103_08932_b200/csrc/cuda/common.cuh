@@ -72,6 +72,15 @@ struct DScalars {
   double ke_ratio;
   int stopped_on_ke;
   double params[8];              // loop constants: h, c, viscous bound, fixed_dt, ...
+  // probe output at marks (runner.cpp:381-390)
+  double next_mark;
+  double interval;
+  long long probe;               // sorted index of the probe particle, < 0: none
+  double* probe_buf;             // 4 doubles per sample
+  long long probe_cap;
+  long long probe_count;
+  int pause_on_mark;
+  int paused;
 };
 
 // Device pointers of the sorted SoA system (passed by value to kernels).
@@ -114,6 +123,11 @@ struct DFields {
   double origin[3];
   double cell;
   int has_body;
+  // optional penalty contact plane (forces.hpp:13-39)
+  int contact;
+  double cp_point[3];
+  double cp_normal[3];
+  double cp_k;
 };
 
 constexpr int kWarp = 32;

@@ -3,9 +3,10 @@
 // Per step the GPU runs, with no host synchronisation:
 //   step_begin (one reduction kernel; its last block does the scalar work:
 //               accounting of the previous step, t += dt, ++steps, NaN check,
-//               end/KE stop test, stable_dt -> dt)
+//               probe sample at output marks, end/KE stop test,
+//               stable_dt -> dt)
 //   verlet passes A, B, C                      (elastic, captured as a graph)
-//   colour phases of the damping sweep          (damped steps only, a graph)
+//   folds + colour phases of the damping sweep (damped steps only, a graph)
 // The eta~ sequence is state independent (one RandomSource draw per step,
 // runner.cpp:358-360), so the host draws it up front and launches the
 // damped or undamped graph per step; every kernel reads dt from device
@@ -79,11 +80,27 @@ __global__ void k_step_begin(DFields f, DScalars* sc, double* __restrict__ parti
   sc->block_counter = 0;
   const double vm = from_ordered_bits(atomicExch(&sc->vmax_bits, 0ull));
   const double am = from_ordered_bits(atomicExch(&sc->amax_bits, 0ull));
+  const double end_time = sc->params[P_END];
+  bool mark = false;
   if (sc->pending) {  // accounting of the step that just finished (runner.cpp:376-379)
     sc->t = sc->t + sc->dt;
     sc->steps += 1;
     sc->last_dt = sc->dt;
     sc->pending = 0;
+    // probe output (runner.cpp:381-383); after check_finite, which is
+    // resolved below through `failed`
+    const double eps = 1e-12 * end_time;
+    if (sc->probe >= 0 && sc->interval > 0.0 && sc->t >= sc->next_mark - eps) {
+      if (sc->probe_count < sc->probe_cap) {
+        double* out = sc->probe_buf + 4 * sc->probe_count;
+        out[0] = sc->t;
+        for (int d = 0; d < 3; ++d)
+          out[1 + d] = d < D ? f.r[d][sc->probe] - f.r0[d][sc->probe] : 0.0;
+      }
+      sc->probe_count += 1;
+      while (sc->next_mark <= sc->t + eps) sc->next_mark += sc->interval;
+      mark = true;
+    }
   }
   if (*reinterpret_cast<volatile int*>(&sc->failed)) {
     sc->err_step = sc->steps;
@@ -103,11 +120,15 @@ __global__ void k_step_begin(DFields f, DScalars* sc, double* __restrict__ parti
       return;
     }
   }
+  if (mark && sc->pause_on_mark) {  // the host writes a snapshot, then resumes
+    sc->paused = 1;
+    sc->halt = 1;
+    return;
+  }
   if (finalize) {
     sc->halt = 1;
     return;
   }
-  const double end_time = sc->params[P_END];
   if (end_time > 0.0 && !(sc->t < end_time)) {  // while (t < end_time)
     sc->done = 1;
     sc->halt = 1;
@@ -163,26 +184,55 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   if (damping_active && !(p.alpha > 0.0 && p.alpha <= 1.0))
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "random-choice probability must lie in (0, 1], got " + std::to_string(p.alpha));
+  if (p.resume && !loop_paused) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "no paused loop to resume");
   const DMaterial mat = to_dmat(p.material);
+  const bool want_probe = p.probe_index >= 0 && p.output_interval > 0.0;
+  if (want_probe && (p.probe_index >= n || (p.probe_capacity > 0 && !p.probe_out)))
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "probe index or buffer invalid");
 
-  // loop scalars
-  DScalars init{};
-  for (int k = 0; k < ERR_SITES; ++k) init.err_key[k] = ~0ull;
-  init.ke_stop = p.ke_stop;
-  init.ke_ratio = p.ke_ratio;
-  init.params[P_H] = p.h;
-  init.params[P_C] = p.material.c;
-  init.params[P_FIXED_DT] = p.fixed_dt;
-  init.params[P_END] = p.end_time;
-  if (damping_active) {
-    // viscous_dt_bounds(h, eta/(alpha rho0), D) (damping.cpp:12-27, runner.cpp:317-320)
-    const double nu = p.eta / (p.alpha * p.material.rho0);
-    const double expl = 0.5 * p.h * p.h / (nu * D);
-    const double impl = 50.0 * p.h * p.h / (nu * D);
-    if (p.scheme == TLSPH_SCHEME_EXPLICIT) init.params[P_VISC] = expl;
-    else if (p.scheme == TLSPH_SCHEME_PARTICLE_SPLIT) init.params[P_VISC] = impl;
+  if (!p.resume) {
+    DScalars init{};
+    for (int k = 0; k < ERR_SITES; ++k) init.err_key[k] = ~0ull;
+    init.ke_stop = p.ke_stop;
+    init.ke_ratio = p.ke_ratio;
+    init.params[P_H] = p.h;
+    init.params[P_C] = p.material.c;
+    init.params[P_FIXED_DT] = p.fixed_dt;
+    init.params[P_END] = p.end_time;
+    if (damping_active) {
+      // viscous_dt_bounds(h, eta/(alpha rho0), D) (damping.cpp:12-27, runner.cpp:317-320)
+      const double nu = p.eta / (p.alpha * p.material.rho0);
+      const double expl = 0.5 * p.h * p.h / (nu * D);
+      const double impl = 50.0 * p.h * p.h / (nu * D);
+      if (p.scheme == TLSPH_SCHEME_EXPLICIT) init.params[P_VISC] = expl;
+      else if (p.scheme == TLSPH_SCHEME_PARTICLE_SPLIT) init.params[P_VISC] = impl;
+    }
+    init.interval = p.output_interval;
+    init.next_mark = p.output_interval;  // runner.cpp:337
+    init.probe = -1;
+    if (want_probe) {
+      int sp = 0;
+      CK(cudaMemcpy(&sp, rank.p + p.probe_index, sizeof(int), cudaMemcpyDeviceToHost));
+      init.probe = sp;
+      probe_dev.alloc(std::max<size_t>(p.probe_capacity, 1) * 4);
+      init.probe_buf = probe_dev.p;
+      init.probe_cap = static_cast<long long>(p.probe_capacity);
+    }
+    init.pause_on_mark = p.pause_on_mark;
+    CK(cudaMemcpyAsync(scal.p, &init, sizeof(DScalars), cudaMemcpyHostToDevice, stream));
+    loop_flags.clear();
+    loop_consumed = 0;
+    loop_el = loop_dm = loop_tot = 0.0;
+  } else {
+    // clear the pause; the accounting of the paused step is already done
+    DScalars hs;
+    CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
+    hs.paused = 0;
+    hs.halt = 0;
+    hs.pause_on_mark = p.pause_on_mark;
+    CK(cudaMemcpy(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice));
   }
-  CK(cudaMemcpyAsync(scal.p, &init, sizeof(DScalars), cudaMemcpyHostToDevice, stream));
+  loop_paused = false;
 
   const unsigned nb = std::min<unsigned>(592, grid_for(n, 256));
   red.alloc(nb);
@@ -206,30 +256,34 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     });
   }
 
-  std::mt19937_64 rng(p.seed);  // RandomSource (damping.hpp:41-50)
-  std::vector<unsigned char> damped_flags;
+  // RandomSource (damping.hpp:41-50): outcomes are regenerated from the seed
+  // so a resumed loop continues the same stream.
+  std::mt19937_64 rng(p.seed);
+  for (size_t k = 0; k < loop_flags.size(); ++k) rng();
+  auto outcome = [&](uint64_t step) -> bool {
+    while (loop_flags.size() <= step) {
+      const double phi = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+      loop_flags.push_back(phi < p.alpha ? 1 : 0);  // random_choice_eta (damping.cpp:29-34)
+    }
+    return loop_flags[step] != 0;
+  };
+
   const uint64_t chunk = 64;
   std::vector<cudaEvent_t> ev(3 * chunk + 2);
   for (auto& e : ev) CK(cudaEventCreate(&e));
-  double el_s = 0.0, dm_s = 0.0, tot_s = 0.0;
-  uint64_t enq = 0;
   DScalars hs{};
+  CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
+  uint64_t enq = static_cast<uint64_t>(hs.steps);  // next step index to enqueue
   bool finished = false;
   while (!finished) {
-    const uint64_t todo = p.max_steps ? std::min<uint64_t>(chunk, p.max_steps - enq) : chunk;
+    const uint64_t todo = p.max_steps ? std::min<uint64_t>(chunk, p.max_steps - std::min(p.max_steps, enq)) : chunk;
     CK(cudaEventRecord(ev[3 * chunk], stream));
     for (uint64_t k = 0; k < todo; ++k) {
       CK(cudaGraphLaunch(g_begin.e, stream));
       CK(cudaEventRecord(ev[3 * k], stream));
       if (p.elastic) CK(cudaGraphLaunch(g_elastic.e, stream));
       CK(cudaEventRecord(ev[3 * k + 1], stream));
-      bool damped = false;
-      if (damping_active) {
-        const double phi = static_cast<double>(rng() >> 11) * 0x1.0p-53;
-        damped = phi < p.alpha;  // random_choice_eta (damping.cpp:29-34)
-        if (damped) CK(cudaGraphLaunch(g_damp.e, stream));
-      }
-      damped_flags.push_back(damped ? 1 : 0);
+      if (damping_active && outcome(enq + k)) CK(cudaGraphLaunch(g_damp.e, stream));
       CK(cudaEventRecord(ev[3 * k + 2], stream));
     }
     enq += todo;
@@ -242,31 +296,35 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     float ms = 0.f;
     for (uint64_t k = 0; k < todo; ++k) {
       CK(cudaEventElapsedTime(&ms, ev[3 * k], ev[3 * k + 1]));
-      el_s += ms * 1e-3;
+      loop_el += ms * 1e-3;
       CK(cudaEventElapsedTime(&ms, ev[3 * k + 1], ev[3 * k + 2]));
-      dm_s += ms * 1e-3;
+      loop_dm += ms * 1e-3;
     }
     CK(cudaEventElapsedTime(&ms, ev[3 * chunk], ev[3 * chunk + 1]));
-    tot_s += ms * 1e-3;
+    loop_tot += ms * 1e-3;
     finished = hs.halt || last_chunk;
   }
   for (auto& e : ev) cudaEventDestroy(e);
-  if (!hs.halt) {  // max_steps reached: finalize already enqueued; refresh
-    CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
-  }
   res.steps = static_cast<uint64_t>(hs.steps);
   uint64_t damped = 0;
-  for (uint64_t k = 0; k < res.steps && k < damped_flags.size(); ++k) damped += damped_flags[k];
-  res.damped_steps = damped;
+  for (uint64_t k = 0; k < res.steps && k < loop_flags.size(); ++k) damped += loop_flags[k];
+  res.damped_steps = damping_active ? damped : 0;
   res.t = hs.t;
   res.last_dt = hs.last_dt;
-  res.elastic_seconds = el_s;
-  res.damping_seconds = dm_s;
-  res.total_seconds = tot_s;
+  res.elastic_seconds = loop_el;
+  res.damping_seconds = loop_dm;
+  res.total_seconds = loop_tot;
   res.peak_ke = hs.ke_peak;
   res.final_ke = hs.ke;
   res.stopped_on_ke = hs.stopped_on_ke;
-  last_elapsed = tot_s;
+  res.paused = hs.paused;
+  res.probe_samples = static_cast<size_t>(hs.probe_count);
+  if (want_probe && hs.probe_count > 0 && p.probe_out) {
+    const size_t ncopy = std::min<size_t>(static_cast<size_t>(hs.probe_count), p.probe_capacity);
+    CK(cudaMemcpy(p.probe_out, probe_dev.p, ncopy * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  last_elapsed = loop_tot;
+  loop_paused = hs.paused != 0 && !hs.failed;
   if (hs.failed) raise_if_failed("run");
 }
 

@@ -453,6 +453,21 @@ __global__ void k_csr_from_ref(DFields f, const long long* __restrict__ off_ref,
   }
 }
 
+// Largest padded 3^D stencil tile over the cells (sweep shared-memory sizing).
+template <int D>
+__global__ void k_stencil_max(DFields f, int* __restrict__ out) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = f.r0[d][i];
+  int c[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, c);
+  Stencil<D> st;
+  stencil_segments<D>(f.cell_start, f.dims, c, st);
+  atomicMax(out, st.total);
+}
+
 // Sizes of the sweep's shared-memory tile: slots per cell and per particle.
 __global__ void k_sweep_stats(const long long* __restrict__ cell_start, long long ncells,
                               const long long* __restrict__ offs, long long n, unsigned long long* out) {
@@ -528,6 +543,12 @@ DFields DevSystem::fields() const {
   f.cell_start = cell_start.p;
   f.cell = cutoff;
   f.has_body = has_body ? 1 : 0;
+  f.contact = contact ? 1 : 0;
+  for (int d = 0; d < 3; ++d) {
+    f.cp_point[d] = cp_point[d];
+    f.cp_normal[d] = cp_normal[d];
+  }
+  f.cp_k = cp_k;
   return f;
 }
 
@@ -760,19 +781,15 @@ void DevSystem::load_csr(const int64_t* offsets, const int32_t* neighbor, const 
   nloc.alloc(S);
   // staged-stencil size for the sweep kernels
   {
-    DBuf<int> counts, maxs;
-    counts.alloc(N);
+    DBuf<int> maxs;
     maxs.alloc(1);
     CK(cudaMemsetAsync(maxs.p, 0, sizeof(int), stream));
     f = fields();
-    // k_nbr_count also validates coincident pairs of the geometry; only the
-    // stencil size is consumed here.
-    if (D == 2) k_nbr_count<2><<<grid_for(n, 128), 128, 0, stream>>>(f, cutoff, counts.p, maxs.p, scal.p);
-    else k_nbr_count<3><<<grid_for(n, 128), 128, 0, stream>>>(f, cutoff, counts.p, maxs.p, scal.p);
-    CK_LAUNCH("k_nbr_count");
+    if (D == 2) k_stencil_max<2><<<grid_for(n, 128), 128, 0, stream>>>(f, maxs.p);
+    else k_stencil_max<3><<<grid_for(n, 128), 128, 0, stream>>>(f, maxs.p);
+    CK_LAUNCH("k_stencil_max");
     CK(cudaMemcpyAsync(&max_stencil, maxs.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
     sync();
-    reset_errors();
   }
   f = fields();
   if (D == 2) k_csr_from_ref<2><<<grid_for(n, 128), 128, 0, stream>>>(f, off_ref.p, nb_ref.p, ln_ref.p, e0_ref.p, dw_ref.p, pf_ref.p);

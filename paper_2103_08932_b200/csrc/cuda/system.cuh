@@ -75,6 +75,14 @@ class DevSystem {
   DBuf<int> perm, rank;
   DBuf<long long> cell_start;
   bool has_body = false;
+  bool contact = false;
+  double cp_point[3] = {0, 0, 0}, cp_normal[3] = {0, 0, 0}, cp_k = 0.0;
+  // resumable loop state (pause_on_mark)
+  bool loop_paused = false;
+  std::vector<unsigned char> loop_flags;  // drawn random-choice outcomes, one per step
+  uint64_t loop_consumed = 0;             // outcomes used by executed steps
+  double loop_el = 0.0, loop_dm = 0.0, loop_tot = 0.0;
+  DBuf<double> probe_dev;
 
   // CSR
   long long nslots = 0;

@@ -226,10 +226,22 @@ __global__ void k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
   }
   if (!active || l != 0) return;
   const double mi = f.m[i];
+  // ExternalAccel::eval (forces.hpp:34-38): body[i] (+ contact plane at the current position)
+  double ext[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) ext[d] = f.body[d][i];
+  if (f.contact) {
+    double gap = (f.r[0][i] - f.cp_point[0]) * f.cp_normal[0];
+#pragma unroll
+    for (int d = 1; d < D; ++d) gap = gap + (f.r[d][i] - f.cp_point[d]) * f.cp_normal[d];
+    const double kc = gap >= 0.0 ? 0.0 : f.cp_k * (-gap) / mi;
+#pragma unroll
+    for (int d = 0; d < D; ++d) ext[d] = ext[d] + (gap >= 0.0 ? 0.0 : kc * f.cp_normal[d]);
+  }
   double a[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    a[d] = acc[d] / mi + f.body[d][i];
+    a[d] = acc[d] / mi + ext[d];
     f.a[d][i] = a[d];
   }
   if (KICK) {
