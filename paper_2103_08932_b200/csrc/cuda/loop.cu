@@ -226,11 +226,12 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   } else {
     // clear the pause; the accounting of the paused step is already done
     DScalars hs;
-    CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost, stream));
+    sync();
     hs.paused = 0;
     hs.halt = 0;
     hs.pause_on_mark = p.pause_on_mark;
-    CK(cudaMemcpy(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice, stream));
   }
   loop_paused = false;
 
@@ -272,7 +273,8 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   std::vector<cudaEvent_t> ev(3 * chunk + 2);
   for (auto& e : ev) CK(cudaEventCreate(&e));
   DScalars hs{};
-  CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost, stream));
+  sync();
   uint64_t enq = static_cast<uint64_t>(hs.steps);  // next step index to enqueue
   bool finished = false;
   while (!finished) {
@@ -303,6 +305,8 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     CK(cudaEventElapsedTime(&ms, ev[3 * chunk], ev[3 * chunk + 1]));
     loop_tot += ms * 1e-3;
     finished = hs.halt || last_chunk;
+    if (!finished && static_cast<uint64_t>(hs.steps) + todo < enq)
+      throw DevError(TLSPH_ERR_INTERNAL, "device time loop stopped advancing");
   }
   for (auto& e : ev) cudaEventDestroy(e);
   res.steps = static_cast<uint64_t>(hs.steps);

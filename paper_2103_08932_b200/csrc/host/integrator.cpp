@@ -57,7 +57,9 @@ void update_density(ParticleSystem<D>& system, int threads) {
   host::put<D>(h.get(), TLSPH_FIELD_F, system.F);
   host::put(h.get(), TLSPH_FIELD_RHO, system.rho);
   const tlsph_status st = tlsph_dev_update_density(h.get());
+  const std::string msg = tlsph_dev_last_error();
   host::get(h.get(), TLSPH_FIELD_RHO, system.rho);  // non-inverted particles are updated before the throw
+  if (st == TLSPH_ERR_INVERTED_ELEMENT) throw Error(ErrorKind::InvertedElement, msg);
   host::check(st);
 }
 

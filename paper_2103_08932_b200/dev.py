@@ -72,13 +72,16 @@ class Material(C.Structure):
 class LoopParams(C.Structure):
     _fields_ = [("material", Material), ("h", C.c_double), ("eta", C.c_double), ("alpha", C.c_double),
                 ("scheme", C.c_int), ("seed", C.c_uint64), ("end_time", C.c_double), ("max_steps", C.c_uint64),
-                ("fixed_dt", C.c_double), ("elastic", C.c_int), ("ke_stop", C.c_int), ("ke_ratio", C.c_double)]
+                ("fixed_dt", C.c_double), ("elastic", C.c_int), ("ke_stop", C.c_int), ("ke_ratio", C.c_double),
+                ("probe_index", C.c_int64), ("output_interval", C.c_double), ("probe_out", C.POINTER(C.c_double)),
+                ("probe_capacity", C.c_size_t), ("pause_on_mark", C.c_int), ("resume", C.c_int)]
 
 
 class LoopResult(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("damped_steps", C.c_uint64), ("t", C.c_double), ("last_dt", C.c_double),
                 ("elastic_seconds", C.c_double), ("damping_seconds", C.c_double), ("total_seconds", C.c_double),
-                ("peak_ke", C.c_double), ("final_ke", C.c_double), ("stopped_on_ke", C.c_int)]
+                ("peak_ke", C.c_double), ("final_ke", C.c_double), ("stopped_on_ke", C.c_int),
+                ("probe_samples", C.c_size_t), ("paused", C.c_int)]
 
 
 _lib = None
@@ -326,7 +329,7 @@ class DeviceSystem:
             elastic=True, seed=0, ke_stop=False, ke_ratio=1e-8):
         """Device-resident loop of runner.cpp:341-391 (state must be prepared as :306-312 does)."""
         p = LoopParams(material, self.h, eta, alpha, SCHEMES[scheme], seed, end_time, steps, fixed_dt,
-                       1 if elastic else 0, 1 if ke_stop else 0, ke_ratio)
+                       1 if elastic else 0, 1 if ke_stop else 0, ke_ratio, -1, 0.0, None, 0, 0, 0)
         r = LoopResult()
         _check(lib().tlsph_dev_run(self._h, C.byref(p), C.byref(r)))
         return {"steps": r.steps, "damped": r.damped_steps, "t": r.t, "last_dt": r.last_dt,
