@@ -34,6 +34,15 @@ P_D = {3: 65, 2: 49}     # v r/w + m + flag + offset per free particle per half-
 P_S = {3: 1091, 2: 587}  # per particle-step minimal traffic
 
 
+def load_traffic():
+    """DRAM bytes per launch of the sweep phase from the committed ncu --set full capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return float(json.load(fh)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -216,7 +225,7 @@ def run_cfg2(args, ws, rank):
                    "l2": "inputs larger than L2 (CSR 200 MB + 20 MB state > 126 MB L2); no flush",
                    "reduction": "fast (warp-shuffle)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "k_sweep_phase (one colour phase)",
+                     "traffic": load_traffic(), "kernel": "k_sweep_phase (one colour phase)",
                      "bytes_per_launch": b_sweep / phase_launches, "avg_launch_s": avg_launch,
                      "peak_source": peak_src},
         "e2e": {"value": e2e, "unit": "DPU/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
