@@ -50,6 +50,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "sweep_chain.cuh"
 #include "system.cuh"
 #include "tma.cuh"
 
@@ -150,12 +151,15 @@ __device__ __forceinline__ double quot(double x, double d, double y) {
 constexpr unsigned kFull = 0xffffffffu;
 
 #ifdef TLSPH_SWEEP_TIMING
-// Debug build only: %globaltimer stamps of each cell task's stages.
-__device__ unsigned long long g_sweep_stamp[1 << 16][8];
+// Debug build only: per cell task, slot 0 %globaltimer at start, slots 1-7
+// clock64 at the stages of k_sweep_fast, slot 8 the particle count.
+constexpr int kStampSlots = 10;
+__device__ unsigned long long g_sweep_stamp[1 << 16][kStampSlots];
 __device__ __forceinline__ void stamp(long long cell, int k) {
   if (threadIdx.x == 0 && cell < (1 << 16)) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (k == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    else t = static_cast<unsigned long long>(clock64());
     g_sweep_stamp[cell][k] = t;
   }
 }
@@ -186,34 +190,21 @@ __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_fro
   f.fy[i] = 1.0 / den;
 }
 
-// ------------------------------------------------------------------ colour phase
-// K > 0: rows up to 32 K slots run the branch-free register path; K = 0: generic loop only.
-template <int D, int SCHEME, bool ORDERED, int K>
-__global__ void __launch_bounds__(kThreads)
-k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
-  if (ph.dt_from_scalars && sc->halt) return;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int tid = threadIdx.x;
-  const int warp = tid / kWarp, lane = tid % kWarp;
-  const long long k = blockIdx.x;
-  stamp(k, 0);
-  int c[3];
+// ------------------------------------------------------------------ staging (step 1)
+template <int D>
+__device__ __forceinline__ void phase_cell(const Phase& ph, long long k, int c[3]) {
   c[0] = ph.res[0] + 3 * static_cast<int>(k % ph.cnt[0]);
   c[1] = ph.res[1] + 3 * static_cast<int>((k / ph.cnt[0]) % ph.cnt[1]);
   c[2] = D == 3 ? ph.res[2] + 3 * static_cast<int>(k / (static_cast<long long>(ph.cnt[0]) * ph.cnt[1])) : 0;
-  constexpr int kSegs = seg_count<D>();
-  Tile<D> t = carve<D>(smem, ph);
-  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
-  const double dt_half = 0.5 * dt;
-  const double dt_op = SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT ? dt_half : 0.5 * dt_half;  // pair step dt/4
-  const double eta = ph.eta;
+}
 
-  // ---- 1. staging. All index loads are issued before any of them is used.
-  const long long lin = cell_linear<D>(c, f.dims);
-  const long long p0 = f.cell_start[lin], p1 = f.cell_start[lin + 1];
-  const long long s0 = f.cell_slot[lin], s1 = f.cell_slot[lin + 1];
-  long long sstart = 0, send = 0;
-  if (warp == 0 && lane < kSegs) {  // lane q locates stencil row q
+// Lane q < 3^(D-1) of the staging warp: particle extent [sstart, send) of stencil row q of cell c.
+template <int D>
+__device__ __forceinline__ void locate_row(const DFields& f, const int c[3], int lane, long long& sstart,
+                                           long long& send) {
+  sstart = 0;
+  send = 0;
+  if (lane < seg_count<D>()) {
     const int dy = (D == 2 ? lane : lane % 3) - 1;
     const int dz = D == 2 ? 0 : lane / 3 - 1;
     const int y = c[1] + dy;
@@ -229,82 +220,212 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
       send = f.cell_start[row + xhi + 1];
     }
   }
-  if (p0 == p1) return;  // empty cell (uniform across the CTA)
-  stamp(k, 6);
-  const int np = static_cast<int>(p1 - p0);
-  const long long o0 = p0 & ~1ll, o1 = (p1 + 2) & ~1ll;  // offs[p0..p1] superset
-  const long long q0 = p0 & ~1ll, q1 = (p1 + 1) & ~1ll;  // fold constants of p0..p1-1
-  const long long f0 = s0 & ~1ll, f1 = (s1 + 1) & ~1ll;  // pair factors
-  const long long n0 = s0 & ~7ll, n1 = (s1 + 7) & ~7ll;  // u16 neighbour indices
-  if (warp == 0) {
-    const int slen = static_cast<int>(send - sstart);
-    // padded tile layout: exclusive scan of the 16-byte aligned row lengths (as stencil_segments)
-    const int par = static_cast<int>(sstart & 1);
-    const int plen = slen > 0 ? ((slen + par + 1) & ~1) : 0;
-    int incl = plen;
+}
+
+// Aligned supersets of the cell's per-particle and per-slot ranges.
+struct CellSpan {
+  long long p0, p1, s0, s1;
+  __device__ long long o0() const { return p0 & ~1ll; }  // offs[p0..p1]
+  __device__ long long o1() const { return (p1 + 2) & ~1ll; }
+  __device__ long long q0() const { return p0 & ~1ll; }  // fold constants of p0..p1-1
+  __device__ long long q1() const { return (p1 + 1) & ~1ll; }
+  __device__ long long f0() const { return s0 & ~1ll; }  // pair factors
+  __device__ long long f1() const { return (s1 + 1) & ~1ll; }
+  __device__ long long n0() const { return s0 & ~7ll; }  // u16 neighbour indices
+  __device__ long long n1() const { return (s1 + 7) & ~7ll; }
+};
+
+// Stencil row table in registers: lane q < 3^(D-1) holds row q, as 16-byte
+// pairs (the tile keeps every row at the parity of its global position).
+struct RowPairs {
+  long long gp;  // global index of the row's first pair (element 2 gp)
+  int tp;        // tile index of the row's first pair
+  int npair;     // pairs staged for the row
+  int excl;      // exclusive prefix of npair over the rows
+  int total;     // pairs over all rows
+};
+
+__device__ __forceinline__ RowPairs row_pairs(long long sstart, int slen, int sbase, int lane) {
+  RowPairs r;
+  const int par = static_cast<int>(sstart & 1);
+  r.gp = (sstart - par) >> 1;
+  r.tp = (sbase - par) >> 1;
+  r.npair = slen > 0 ? (slen + par + 1) >> 1 : 0;
+  int incl = r.npair;
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-      const int x = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += x;
-    }
-    const int sbase = incl - plen + par;
-    if (lane < kSegs) {
-      t.seg_start[lane] = sstart;
-      t.seg_len[lane] = slen;
-      t.seg_base[lane] = sbase;
-    }
-    const bool fold = SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT;
-    uint32_t mybytes = 0;
-    if (lane < kSegs && slen > 0) mybytes = static_cast<uint32_t>(plen * 8 * (D + 2));
-    else if (lane == kSegs) mybytes = static_cast<uint32_t>((o1 - o0) * 8);
-    else if (lane == kSegs + 1) mybytes = static_cast<uint32_t>((f1 - f0) * 8);
-    else if (lane == kSegs + 2) mybytes = static_cast<uint32_t>((n1 - n0) * 2);
-    else if (fold && lane == kSegs + 3) mybytes = static_cast<uint32_t>((q1 - q0) * 8 * 3);
-    uint32_t total = mybytes;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
-    if (lane == 0) {
-      mbar_init(t.bar, 1);
-      fence_proxy_async_smem();  // the initialised barrier is visible to the TMA unit
-      mbar_arrive_expect_tx(t.bar, total);
-    }
-    __syncwarp();
-    if (lane < kSegs && slen > 0) {
-      const long long a0 = sstart - par;
-      const int dst = sbase - par;
-      const uint32_t nb = static_cast<uint32_t>(plen * 8);
-#pragma unroll
-      for (int d = 0; d < D; ++d) tma_load_1d(t.sv[d] + dst, f.v[d] + a0, nb, t.bar);
-      tma_load_1d(t.sm + dst, f.m + a0, nb, t.bar);
-      tma_load_1d(t.smf + dst, f.minvf + a0, nb, t.bar);
-    } else if (lane == kSegs) {
-      tma_load_1d(t.soff, f.offs + o0, mybytes, t.bar);
-    } else if (lane == kSegs + 1) {
-      tma_load_1d(t.spf, f.pf + f0, mybytes, t.bar);
-    } else if (lane == kSegs + 2) {
-      tma_load_1d(t.snl, f.nloc + n0, mybytes, t.bar);
-    } else if (fold && lane == kSegs + 3) {
-      const uint32_t nb = static_cast<uint32_t>((q1 - q0) * 8);
-      tma_load_1d(t.sdiag, f.fdiag + q0, nb, t.bar);
-      tma_load_1d(t.sden, f.fden + q0, nb, t.bar);
-      tma_load_1d(t.sy, f.fy + q0, nb, t.bar);
-    }
-    constexpr int center = D == 2 ? 1 : 4;
-    const int lbase = __shfl_sync(kFull, sbase, center) + static_cast<int>(p0 - __shfl_sync(kFull, sstart, center));
-    if (lane == 0) reinterpret_cast<int*>(t.bar + 1)[0] = lbase;  // the centre row holds the cell's particles
+  for (int o = 1; o < 16; o <<= 1) {
+    const int x = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += x;
   }
-  stamp(k, 1);
-  __syncthreads();  // barrier initialised before anyone waits on it
+  r.excl = incl - r.npair;
+  r.total = __shfl_sync(kFull, incl, 15);
+  return r;
+}
+
+// For pair p of the flattened row table: its row q and offset in the row.
+template <int D>
+__device__ __forceinline__ void locate_pair(const RowPairs& r, int p, int& q, int& off) {
+  q = 0;
+#pragma unroll
+  for (int k = 1; k < seg_count<D>(); ++k) q += p >= __shfl_sync(kFull, r.excl, k) ? 1 : 0;
+  off = p - __shfl_sync(kFull, r.excl, q);
+}
+
+// Executed by one whole warp: padded tile layout (exclusive scan of the
+// 16-byte aligned row lengths, as stencil_segments), segment table; the
+// stencil rows (v, 1/m and optionally m) by per-lane 16-byte cp.async over
+// the flattened row table, the cell's slot block, row offsets and fold
+// constants by bulk copies on the mbarrier. MASS: also stage m (ORDERED
+// divisions, pairwise).
+template <int D, bool FOLD, bool MASS, bool PDL = false>
+__device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
+                                              long long sstart, long long send, int lane) {
+  constexpr int kSegs = seg_count<D>();
+  const int slen = static_cast<int>(send - sstart);
+  const int par = static_cast<int>(sstart & 1);
+  const int plen = slen > 0 ? ((slen + par + 1) & ~1) : 0;
+  int incl = plen;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const int x = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += x;
+  }
+  const int sbase = incl - plen + par;
+  if (lane < kSegs) {
+    t.seg_start[lane] = sstart;
+    t.seg_len[lane] = slen;
+    t.seg_base[lane] = sbase;
+  }
+  uint32_t mybytes = 0;
+  if (lane == 0) mybytes = static_cast<uint32_t>((cs.o1() - cs.o0()) * 8);
+  else if (lane == 1) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
+  else if (lane == 2) mybytes = static_cast<uint32_t>((cs.n1() - cs.n0()) * 2);
+  else if (FOLD && lane == 3) mybytes = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8 * 3);
+  uint32_t total = mybytes;
+#pragma unroll
+  for (int o = 2; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+  if (lane == 0) {
+    mbar_init(t.bar, 1);
+    fence_proxy_async_smem();  // the initialised barrier is visible to the TMA unit
+    mbar_arrive_expect_tx(t.bar, total);
+  }
+  __syncwarp();
+  stamp(blockIdx.x, 9);
+  if (lane == 0) {
+    tma_load_1d(t.soff, f.offs + cs.o0(), mybytes, t.bar);
+  } else if (lane == 1) {
+    tma_load_1d(t.spf, f.pf + cs.f0(), mybytes, t.bar);
+  } else if (lane == 2) {
+    tma_load_1d(t.snl, f.nloc + cs.n0(), mybytes, t.bar);
+  } else if (FOLD && lane == 3) {
+    const uint32_t nb = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8);
+    tma_load_1d(t.sdiag, f.fdiag + cs.q0(), nb, t.bar);
+    tma_load_1d(t.sden, f.fden + cs.q0(), nb, t.bar);
+    tma_load_1d(t.sy, f.fy + cs.q0(), nb, t.bar);
+  }
+  stamp(blockIdx.x, 3);
+  // PDL: everything above is static; the velocities are written by the preceding phase
+  if (PDL) grid_dependency_wait();
+  const RowPairs rp = row_pairs(sstart, lane < kSegs ? slen : 0, sbase, lane);
+  for (int base = 0; base < rp.total; base += kWarp) {
+    const int p = base + lane;
+    int q, off;
+    locate_pair<D>(rp, p, q, off);
+    const long long g = 2 * (__shfl_sync(kFull, rp.gp, q) + off);
+    const int tt = 2 * (__shfl_sync(kFull, rp.tp, q) + off);
+    if (p < rp.total) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) cp_async16(t.sv[d] + tt, f.v[d] + g);
+      cp_async16(t.smf + tt, f.minvf + g);
+      if (MASS) cp_async16(t.sm + tt, f.m + g);
+    }
+  }
+  constexpr int center = D == 2 ? 1 : 4;
+  const int lbase =
+      __shfl_sync(kFull, sbase, center) + static_cast<int>(cs.p0 - __shfl_sync(kFull, sstart, center));
+  if (lane == 0) reinterpret_cast<int*>(t.bar + 1)[0] = lbase;  // the centre row holds the cell's particles
+}
+
+// Staging complete: bulk copies landed and this thread's cp.async copies done.
+template <int D>
+__device__ __forceinline__ void wait_staging(const Tile<D>& t) {
+  cp_async_wait_all();
   mbar_wait(t.bar, 0);
-  stamp(k, 2);
+}
+
+// Write the staged stencil rows back to v; one warp per call. Lane q < 3^(D-1)
+// writes the 16-byte aligned interior of row q with one bulk store per
+// component; ragged row ends (odd first or last element) by plain stores.
+template <int D>
+__device__ __forceinline__ void writeback_rows(const DFields& f, const Tile<D>& t, int lane) {
+  constexpr int kSegs = seg_count<D>();
+  fence_proxy_async_smem();  // the chain's shared-memory writes, visible to the bulk copies
+  __syncwarp();
+  if (lane < kSegs) {
+    const long long rs = t.seg_start[lane];
+    const int len = t.seg_len[lane];
+    const int tb = t.seg_base[lane];
+    if (len > 0) {
+      const long long re = rs + len;
+      const long long a0 = (rs + 1) & ~1ll, a1 = re & ~1ll;  // aligned interior [a0, a1)
+      const int ta = tb + static_cast<int>(a0 - rs);
+      if (a1 > a0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+          tma_store_1d(f.v[d] + a0, t.sv[d] + ta, static_cast<uint32_t>((a1 - a0) * 8));
+      }
+      if (rs & 1) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) f.v[d][rs] = t.sv[d][tb];
+      }
+      if ((re & 1) && re - 1 >= a0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) f.v[d][re - 1] = t.sv[d][tb + len - 1];
+      }
+      bulk_commit();
+      bulk_wait_read();  // the tile must outlive the copies' reads
+    }
+  }
+}
+
+// ------------------------------------------------------------------ colour phase
+// K > 0: rows up to 32 K slots run the branch-free register path; K = 0: generic loop only.
+template <int D, int SCHEME, bool ORDERED, int K>
+__global__ void __launch_bounds__(kThreads)
+k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
+  if (ph.dt_from_scalars && sc->halt) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid / kWarp, lane = tid % kWarp;
+  const long long k = blockIdx.x;
+  int c[3];
+  phase_cell<D>(ph, k, c);
+  constexpr int kSegs = seg_count<D>();
+  Tile<D> t = carve<D>(smem, ph);
+  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
+  const double dt_half = 0.5 * dt;
+  const double dt_op = SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT ? dt_half : 0.5 * dt_half;  // pair step dt/4
+  const double eta = ph.eta;
+
+  // ---- 1. staging. All index loads are issued before any of them is used.
+  const long long lin = cell_linear<D>(c, f.dims);
+  CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
+  long long sstart = 0, send = 0;
+  if (warp == 0) locate_row<D>(f, c, lane, sstart, send);
+  if (cs.p0 == cs.p1) return;  // empty cell (uniform across the CTA)
+  const long long p0 = cs.p0, p1 = cs.p1, s0 = cs.s0;
+  const int np = static_cast<int>(p1 - p0);
+  if (warp == 0) issue_staging<D, SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT, true>(f, t, cs, sstart, send, lane);
+  if (warp == 0) cp_async_wait_all();
+  __syncthreads();  // barrier initialised and row copies landed before anyone waits on it
+  mbar_wait(t.bar, 0);
   const int lbase = reinterpret_cast<const int*>(t.bar + 1)[0];
-  const long long* offc = t.soff + (p0 - o0);  // offc[k] = offs[p0 + k]
-  const double* pfc = t.spf + (s0 - f0);
-  const uint16_t* nlc = t.snl + (s0 - n0);
-  const double* fdg = t.sdiag + (p0 - q0);
-  const double* fdn = t.sden + (p0 - q0);
-  const double* fyy = t.sy + (p0 - q0);
-  stamp(k, 3);
+  const long long* offc = t.soff + (p0 - cs.o0());  // offc[k] = offs[p0 + k]
+  const double* pfc = t.spf + (s0 - cs.f0());
+  const uint16_t* nlc = t.snl + (s0 - cs.n0());
+  const double* fdg = t.sdiag + (p0 - cs.q0());
+  const double* fdn = t.sden + (p0 - cs.q0());
+  const double* fyy = t.sy + (p0 - cs.q0());
 
   // ---- 2. the chain: warp d owns velocity component d
   if (warp < D) {
@@ -454,7 +575,6 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
       }
     }
   }
-  stamp(k, 4);
   __syncthreads();
 
   // ---- 3. write the stencil back (rows from the tile's segment table)
@@ -466,7 +586,85 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
       for (int d = 0; d < D; ++d) f.v[d][g0 + e] = t.sv[d][b + e];
     }
   }
-  stamp(k, 5);
+}
+
+// ------------------------------------------------------------------ FAST particle split, one warp per cell
+// The whole chain of a cell in one warp (sweep_chain.cuh): every slot's
+// metadata is read once for all D components and the D residuals share one
+// shuffle tree.
+template <int D, int K>
+__global__ void __launch_bounds__(kWarp)
+k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
+  if (ph.dt_from_scalars && sc->halt) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  stamp(blockIdx.x, 0);
+  stamp(blockIdx.x, 1);
+  grid_launch_dependents();  // the next phase may stage its static data while this one runs
+  int c[3];
+  phase_cell<D>(ph, blockIdx.x, c);
+  Tile<D> t = carve<D>(smem, ph);
+  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
+  const double kb = ph.eta * (0.5 * dt);  // b = kb * pair_factor
+
+  const long long lin = cell_linear<D>(c, f.dims);
+  const CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
+  long long sstart, send;
+  locate_row<D>(f, c, lane, sstart, send);
+  if (cs.p0 == cs.p1) return;
+  stamp(blockIdx.x, 2);
+  issue_staging<D, true, false, true>(f, t, cs, sstart, send, lane);
+  stamp(blockIdx.x, 4);
+  wait_staging(t);
+  __syncwarp();
+  stamp(blockIdx.x, 5);
+  ChainTile<D> ct;
+#pragma unroll
+  for (int d = 0; d < D; ++d) ct.sv[d] = t.sv[d];
+  ct.smf = t.smf;
+  ct.pf = t.spf + (cs.s0 - cs.f0());
+  ct.nl = t.snl + (cs.s0 - cs.n0());
+  ct.offs = t.soff + (cs.p0 - cs.o0());
+  ct.s0 = cs.s0;
+  ct.diag = t.sdiag + (cs.p0 - cs.q0());
+  ct.y = t.sy + (cs.p0 - cs.q0());
+  ct.lbase = reinterpret_cast<const int*>(t.bar + 1)[0];
+  ct.np = static_cast<int>(cs.p1 - cs.p0);
+  ct.forward = ph.forward;
+  ct.kb = kb;
+  fast_chain<D, K>(ct, lane);
+  __syncwarp();
+  stamp(blockIdx.x, 6);
+
+  writeback_rows<D>(f, t, lane);
+  stamp(blockIdx.x, 7);
+#ifdef TLSPH_SWEEP_TIMING
+  if (lane == 0 && blockIdx.x < (1 << 16)) g_sweep_stamp[blockIdx.x][8] = static_cast<unsigned long long>(cs.p1 - cs.p0);
+#endif
+}
+
+template <int D, int K>
+void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    CK(cudaFuncSetAttribute(k_sweep_fast<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = smem;
+  }
+  // programmatic dependent launch: the phase's CTAs may start (and stage their
+  // static data) while the preceding kernel finishes; they wait on it before
+  // touching the velocities (griddepcontrol.wait in issue_staging)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(ph.ncol));
+  cfg.blockDim = dim3(kWarp);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_sweep_fast<D, K>, f, ph, s.scal.p));
 }
 
 template <int D, int SCHEME, bool ORDERED, int K>
@@ -486,6 +684,13 @@ template <int D, bool ORDERED>
 void launch_particle_split(const DevSystem& s, const DFields& f, const Phase& ph) {
   // slots per lane kept in registers: the smallest K that covers the longest row
   const int K = (s.max_row + kWarp - 1) / kWarp;
+  if (!ORDERED && K <= 4) {
+    if (K <= 1) launch_fast<D, 1>(s, f, ph);
+    else if (K == 2) launch_fast<D, 2>(s, f, ph);
+    else if (K == 3) launch_fast<D, 3>(s, f, ph);
+    else launch_fast<D, 4>(s, f, ph);
+    return;
+  }
   if (K <= 1) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 1>(s, f, ph);
   else if (K <= 2) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 2>(s, f, ph);
   else if (K <= 3) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 3>(s, f, ph);
@@ -605,7 +810,8 @@ unsigned long long selftest_division(long long n, unsigned long long seed) {
 #ifdef TLSPH_SWEEP_TIMING
 extern "C" int tlsph_debug_sweep_stamps(unsigned long long* out, int cells) {
   const int n = cells < (1 << 16) ? cells : (1 << 16);
-  return cudaMemcpyFromSymbol(out, tlsph_cuda::g_sweep_stamp, sizeof(unsigned long long) * 8 * n) == cudaSuccess
+  return cudaMemcpyFromSymbol(out, tlsph_cuda::g_sweep_stamp,
+                              sizeof(unsigned long long) * tlsph_cuda::kStampSlots * n) == cudaSuccess
              ? n
              : -1;
 }

@@ -1,0 +1,197 @@
+// The FAST particle-split Gauss-Seidel chain of one cell, run by one warp
+// (damping.cpp:53-89 particle_split_update, applied in cell order as
+// neighbors.cpp:143-174 block_sweep does). Shared by k_sweep_fast (sweep.cu)
+// and the microbenchmark tools/chain_fast.cu.
+//
+// Lane l owns slots l, l+32, ... (K per lane) of the current particle for all
+// D velocity components. Reassociated update (FAST tolerance class): with
+// Y = (1 + bm) v_j - bm v_i and C = -bm (diag + b),
+//   v_j' = v_j - bm (v_i + diag rate - (v_j - b rate)) = Y + C rate,
+// so one FMA per slot follows the residual reduction on the chain.
+//
+// Software pipeline. Everything but the stencil velocities is static during
+// the chain, so the slot metadata of the next particle is loaded while the
+// current one runs, in three stages that never stall the chain: (A) its
+// neighbour indices and pair factors, issued at the top of the iteration;
+// (C) the masses of those neighbours, issued after the chain's velocity
+// gathers; (D) the derived coefficients, formed after the scatter. Row
+// extents are read two particles ahead. A constrained particle or one without
+// neighbours (damping.cpp:54, :151) runs the same code with its writes
+// disabled, so the loop has no data-dependent branch.
+#pragma once
+#include <cstdint>
+
+namespace tlsph_cuda {
+
+template <int D>
+struct ChainTile {
+  double* sv[D];          // staged stencil velocities
+  const double* smf;      // staged signed RN(1/m) (negative: clamped)
+  const double* pf;       // the cell's pair factors, cell-relative slot index
+  const uint16_t* nl;     // the cell's stencil-local neighbour indices
+  const long long* offs;  // offs[p] - s0 = cell-relative first slot of particle p
+  long long s0;
+  const double* diag;     // per-particle fold constants
+  const double* y;        // RN(1 / denominator)
+  int lbase;              // tile index of the cell's first particle
+  int np;
+  int forward;
+  double kb;              // b = kb * pair_factor
+};
+
+// Sum of D doubles over the warp, result in every lane. Transposing
+// butterfly: the first levels exchange half of the remaining components
+// (lane bit 4 picks components {0,1} or {2,3}, bit 3 one of the pair), so
+// after two levels each lane carries one component and the last three levels
+// are a plain butterfly; one broadcast per component follows. 18 32-bit
+// shuffles for D = 3 instead of 30, and every level depends on all
+// components, so the reductions cannot be serialised by the scheduler.
+template <int D>
+__device__ __forceinline__ void warp_sum_vec(double (&x)[D], int lane) {
+  static_assert(D == 2 || D == 3, "D");
+  constexpr unsigned kAll = 0xffffffffu;
+  const bool b4 = lane & 16, b3 = lane & 8;
+  double c;
+  if constexpr (D == 3) {
+    const double a0 = b4 ? x[0] : x[2], a1 = b4 ? x[1] : 0.0;  // sent
+    const double k0 = b4 ? x[2] : x[0], k1 = b4 ? 0.0 : x[1];  // kept
+    const double r0 = __shfl_xor_sync(kAll, a0, 16), r1 = __shfl_xor_sync(kAll, a1, 16);
+    const double h0 = k0 + r0, h1 = k1 + r1;  // components 2 b4, 2 b4 + 1
+    const double r = __shfl_xor_sync(kAll, b3 ? h0 : h1, 8);
+    c = (b3 ? h1 : h0) + r;  // component 2 b4 + b3
+  } else {
+    const double r = __shfl_xor_sync(kAll, b4 ? x[0] : x[1], 16);
+    c = (b4 ? x[1] : x[0]) + r;  // component b4
+  }
+#pragma unroll
+  for (int o = D == 3 ? 4 : 8; o > 0; o >>= 1) c += __shfl_xor_sync(kAll, c, o);
+#pragma unroll
+  for (int d = 0; d < D; ++d) x[d] = __shfl_sync(kAll, c, D == 3 ? 8 * d : 16 * d);
+}
+
+template <int D, int K, bool SHUF = true, bool SCATTER = true>
+__device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
+  const int np = t.np;
+  auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
+  auto row = [&](int p, int& lo, int& cnt) {
+    lo = static_cast<int>(t.offs[p] - t.s0);
+    cnt = static_cast<int>(t.offs[p + 1] - t.s0) - lo;
+  };
+
+  // current particle: coefficients
+  int pk = pidx(0);
+  int jq[K];
+  double bq[K], bmq[K], c1[K], cq[K];
+  unsigned upm;
+  bool skip;
+  double diag, y;
+  // next particle: raw loads
+  int pk1 = np > 1 ? pidx(1) : pk, lo1, cnt1;
+  row(pk1, lo1, cnt1);
+  {
+    int lo, cnt;
+    row(pk, lo, cnt);
+    diag = t.diag[pk];
+    y = t.y[pk];
+    skip = t.smf[t.lbase + pk] < 0.0 || cnt == 0;
+    upm = 0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const int s = lane + u * 32;
+      const bool v = s < cnt;
+      const int j = v ? t.nl[lo + s] : t.lbase + pk;  // invalid lanes read i itself with b = 0
+      const double mf = t.smf[j];
+      const bool up = v && mf > 0.0;                 // clamped j: never written (damping.cpp:84-86)
+      jq[u] = j;
+      bq[u] = v ? t.kb * t.pf[lo + s] : 0.0;
+      bmq[u] = up ? bq[u] * mf : 0.0;
+      c1[u] = 1.0 + bmq[u];
+      cq[u] = -bmq[u] * (diag + bq[u]);
+      upm |= up ? (1u << u) : 0u;
+    }
+    if (skip) upm = 0;
+  }
+
+  for (int kk = 0; kk < np; ++kk) {
+    const int li = t.lbase + pk;
+    const int li1 = t.lbase + pk1;
+    // (A) next particle's indices and pair factors
+    int jn[K];
+    double pfn[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const int s = lane + u * 32;
+      const bool v = s < cnt1;
+      jn[u] = v ? t.nl[lo1 + s] : li1;
+      pfn[u] = v ? t.pf[lo1 + s] : 0.0;
+    }
+    // row extents two particles ahead
+    const int pk2 = kk + 2 < np ? pidx(kk + 2) : pk1;
+    int lo2, cnt2;
+    row(pk2, lo2, cnt2);
+
+    // the chain: gathers
+    double vi[D], vq[K][D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) vi[d] = t.sv[d][li];
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int d = 0; d < D; ++d) vq[u][d] = t.sv[d][jq[u]];
+    // (C) next particle's neighbour masses and fold constants
+    double mfn[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) mfn[u] = t.smf[jn[u]];
+    const double mfi1 = t.smf[li1];
+    const double diag1 = t.diag[pk1], y1 = t.y[pk1];
+
+    double P[D], Y[K][D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      P[d] = bq[0] * (vq[0][d] - vi[d]);
+#pragma unroll
+      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], vq[u][d] - vi[d], P[d]);
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(c1[u], vq[u][d], -bmq[u] * vi[d]);
+    if (SHUF) warp_sum_vec<D>(P, lane);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double rate = P[d] * y;
+      if (SCATTER) {
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+          if (upm & (1u << u)) t.sv[d][jq[u]] = __fma_rn(cq[u], rate, Y[u][d]);
+      }
+      // i is not its own neighbour, so this store cannot race the scatter above
+      if (lane == 0 && !skip) t.sv[d][li] = __fma_rn(diag, rate, vi[d]);
+    }
+    __syncwarp();
+
+    // (D) next particle's coefficients
+    diag = diag1;
+    y = y1;
+    skip = mfi1 < 0.0 || cnt1 == 0;
+    upm = 0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const bool v = lane + u * 32 < cnt1;
+      const bool up = v && mfn[u] > 0.0;
+      jq[u] = jn[u];
+      bq[u] = t.kb * pfn[u];
+      bmq[u] = up ? bq[u] * mfn[u] : 0.0;
+      c1[u] = 1.0 + bmq[u];
+      cq[u] = -bmq[u] * (diag + bq[u]);
+      upm |= up ? (1u << u) : 0u;
+    }
+    if (skip) upm = 0;
+    pk = pk1;
+    pk1 = pk2;
+    lo1 = lo2;
+    cnt1 = cnt2;
+  }
+}
+
+}  // namespace tlsph_cuda

@@ -20,19 +20,29 @@ for _ in range(3):
     d.damping_sweep("particle_split", eta_t, cfg["fixed_dt"])
 L = dev.lib()
 L.tlsph_debug_sweep_stamps.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+SLOTS = 10
 ncell = 579
-buf = (C.c_ulonglong * (8 * ncell))()
+buf = (C.c_ulonglong * (SLOTS * ncell))()
 n = L.tlsph_debug_sweep_stamps(buf, ncell)
-st = np.array(buf[: 8 * n], dtype=np.float64).reshape(n, 8)
-order = [0, 6, 1, 2, 3, 4, 5]
-names = ["start", "indices-loaded", "tma-issued", "tma-landed", "staged", "chain-done", "written"]
-st = st[:, order]
-t0 = st[:, 0].min()
-rel = (st - t0) / 1e3  # microseconds
-print(f"cells {n}; phase span {rel[:, -1].max():.2f} us")
-for k, name in enumerate(names):
-    print(f"{name:15s} min {rel[:, k].min():7.2f}  median {np.median(rel[:, k]):7.2f}  max {rel[:, k].max():7.2f} us")
-dur = np.diff(rel, axis=1)
+st = np.array(buf[: SLOTS * n], dtype=np.float64).reshape(n, SLOTS)
+ghz = float(os.environ.get("SM_GHZ", "1.965"))
+start_us = (st[:, 0] - st[:, 0].min()) / 1e3
+cyc = st[:, 1:8] - st[:, 1:2]  # clock64 relative to each cell's own start
+nps = st[:, 8]
+names = ["start", "indices", "bulk issued", "rows issued", "tma landed", "chain done", "written"]
+end_us = start_us + cyc[:, -1] / (ghz * 1e3)
+print(f"cells {n}; CTA start spread {start_us.max():.2f} us; phase span {end_us.max():.2f} us "
+      f"(median end {np.median(end_us):.2f})")
+dur = np.diff(cyc, axis=1)
 for k in range(len(names) - 1):
-    print(f"{names[k]:>15s} -> {names[k + 1]:15s} median {np.median(dur[:, k]):6.2f} us  max {dur[:, k].max():6.2f}")
-
+    print(f"{names[k]:>12s} -> {names[k + 1]:12s} median {np.median(dur[:, k]):7.0f} cyc "
+          f"({np.median(dur[:, k]) / ghz:6.0f} ns)  max {dur[:, k].max():7.0f} cyc")
+bar = st[:, 9] - st[:, 1]
+print(f"  (indices -> barrier initialised: median {np.median(bar - cyc[:, 1]):.0f} cyc)")
+chain = dur[:, 4]
+ok = nps > 0
+print(f"chain per particle: median {np.median(chain[ok] / nps[ok]):.0f} cycles (np median {np.median(nps[ok]):.0f}, "
+      f"max {nps.max():.0f}); by np:")
+for v in sorted(set(nps[ok].astype(int))):
+    m = nps == v
+    print(f"  np {v:3d}: {m.sum():4d} cells, chain {np.median(chain[m]):7.0f} cyc, end {np.median(end_us[m]):6.2f} us")
