@@ -23,16 +23,17 @@ struct Smem {
 
 // MODE bits: 1 = skip shuffles, 2 = skip scatter stores
 template <int MODE>
-__global__ void __launch_bounds__(32) chain(const uint16_t* nloc, const double* pf, double* out, long long* cyc,
+__global__ void __launch_bounds__(128) chain(const uint16_t* nloc, const double* pf, double* out, long long* cyc,
                                             int reps) {
   extern __shared__ __align__(16) unsigned char raw[];
   Smem& t = *reinterpret_cast<Smem*>(raw);
   const int lane = threadIdx.x;
-  for (int e = lane; e < S; e += 32) {
+  const int nthr = blockDim.x;
+  for (int e = lane; e < S; e += nthr) {
     for (int d = 0; d < D; ++d) t.sv[d][e] = 0.001 * e + d;
     t.smf[e] = (e % 97 == 5) ? -1.0 : 1.0 / (1.0 + e * 1e-3);
   }
-  for (int e = lane; e < NP * CNT; e += 32) {
+  for (int e = lane; e < NP * CNT; e += nthr) {
     t.nl[e] = nloc[e];
     t.pf[e] = pf[e];
   }
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(32) chain(const uint16_t* nloc, const double* 
     t.diag[lane] = -1.0 - 0.01 * lane;
     t.y[lane] = 0.3;
   }
-  __syncwarp();
+  __syncthreads();
   tlsph_cuda::ChainTile<D> ct;
   for (int d = 0; d < D; ++d) ct.sv[d] = t.sv[d];
   ct.smf = t.smf;
@@ -70,7 +71,8 @@ void run(const char* name, const uint16_t* nl, const double* pf, double* out, lo
   const size_t smem = sizeof(Smem);
   cudaFuncSetAttribute(chain<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int blocks : {1, 148 * 4}) {
-    for (int w = 0; w < 2; ++w) chain<MODE><<<blocks, 32, smem>>>(nl, pf, out, cyc, reps);
+    const int threads = 32;
+    for (int w = 0; w < 2; ++w) chain<MODE><<<blocks, threads, smem>>>(nl, pf, out, cyc, reps);
     cudaDeviceSynchronize();
     long long c = 0;
     cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
