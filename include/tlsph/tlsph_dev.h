@@ -105,6 +105,29 @@ tlsph_status tlsph_dev_create_with_csr(int dim, size_t n, const double* r0, cons
  * allowed. Query it with tlsph_dev_grid_info / tlsph_dev_grid_cells. */
 tlsph_status tlsph_dev_create_grid(int dim, size_t n, const double* positions, double cutoff, tlsph_dev** out);
 
+/* One x-slab of a decomposed body: the local particles
+ * (owned cell columns plus one halo column each side, ascending reference id)
+ * binned in the GLOBAL cell grid (origin, dims; cell = 2h) so cell indices,
+ * colours and in-cell order are those of the undivided body; neighbourhoods
+ * are built on the GPU from the local particles. */
+tlsph_status tlsph_dev_create_in_grid(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
+                                      const uint8_t* constrained, double h, const double* origin, const int* dims,
+                                      tlsph_dev** out);
+/* Sweep tasks are the cells with x in [x0, x1) (default: the whole grid). */
+tlsph_status tlsph_dev_set_task_range(tlsph_dev* dev, int x0, int x1);
+/* One colour phase of strang_damping_sweep (damping.cpp:125-182): pass 0 is
+ * the forward leg (colour `index` ascending), pass 1 the reverse leg; the
+ * 2 * 3^D phases in order equal tlsph_dev_damping_sweep. Synchronous. */
+tlsph_status tlsph_dev_damping_phase(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt, int pass,
+                                     int index);
+/* Halo exchange of a slab system: velocities of the particles of cell column
+ * x, component-major (D x count doubles), in (z, y, in-cell) order, which is
+ * the same on every slab that holds the column. Device buffers; synchronous.
+ * tlsph_dev_column_count returns -1 on error. */
+int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x);
+tlsph_status tlsph_dev_pack_column(tlsph_dev* dev, int x, double* device_dst);
+tlsph_status tlsph_dev_unpack_column(tlsph_dev* dev, int x, const double* device_src);
+
 void tlsph_dev_destroy(tlsph_dev* dev);
 
 size_t tlsph_dev_size(const tlsph_dev* dev);

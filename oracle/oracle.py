@@ -127,9 +127,12 @@ class OracleSystem:
                                 self.h, 1 if build else 0, C.byref(self._h)))
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            lib().orc_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                lib().orc_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     # ---- fields
     def _shape(self, name):

@@ -130,6 +130,64 @@ tlsph_status tlsph_dev_create_grid(int dim, size_t n, const double* positions, d
   });
 }
 
+tlsph_status tlsph_dev_create_in_grid(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
+                                      const uint8_t* constrained, double h, const double* origin, const int* dims,
+                                      tlsph_dev** out) {
+  if (!out) {
+    g_dev_err = "out must not be null";
+    return TLSPH_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    if (!origin || !dims) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "origin and dims must not be null");
+    auto d = new_handle();
+    d->sys.grid_given = true;
+    for (int k = 0; k < dim && k < 3; ++k) {
+      d->sys.given_origin[k] = origin[k];
+      d->sys.given_dims[k] = dims[k];
+    }
+    d->sys.init_common(dim, n, r0, V0, rho0, constrained, h);
+    d->sys.build_neighbourhoods();
+    *out = d.release();
+  });
+}
+
+tlsph_status tlsph_dev_set_task_range(tlsph_dev* dev, int x0, int x1) {
+  return guarded([&] {
+    DevSystem& s = sys(dev);
+    if (x0 < 0 || x1 > s.dims[0] || x0 >= x1)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "task range must satisfy 0 <= x0 < x1 <= dims[0]");
+    s.task_x0 = x0;
+    s.task_x1 = x1;
+  });
+}
+
+tlsph_status tlsph_dev_damping_phase(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt, int pass,
+                                     int index) {
+  return guarded([&] {
+    DevSystem& s = sys(dev);
+    if (eta_tilde == 0.0) return;  // damping.cpp:132
+    if (scheme != TLSPH_SCHEME_PARTICLE_SPLIT && scheme != TLSPH_SCHEME_PAIRWISE_SPLIT)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "only the split schemes are swept");
+    s.enqueue_sweep_phase(scheme, eta_tilde, dt, pass, index);
+    s.sync();
+  });
+}
+
+int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x) {
+  int64_t c = -1;
+  const tlsph_status st = guarded([&] { c = sys(dev).column_count(x); });
+  return st == TLSPH_OK ? c : -1;
+}
+
+tlsph_status tlsph_dev_pack_column(tlsph_dev* dev, int x, double* device_dst) {
+  return guarded([&] { sys(dev).pack_column(x, device_dst); });
+}
+
+tlsph_status tlsph_dev_unpack_column(tlsph_dev* dev, int x, const double* device_src) {
+  return guarded([&] { sys(dev).unpack_column(x, device_src); });
+}
+
 tlsph_status tlsph_dev_set_contact_plane(tlsph_dev* dev, const double* point, const double* normal,
                                          double stiffness) {
   return guarded([&] {

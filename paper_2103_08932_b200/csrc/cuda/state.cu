@@ -643,7 +643,13 @@ void DevSystem::init_common(int dim, size_t n_, const double* r0_h, const double
   }
   ncells = 1;
   for (int d = 0; d < 3; ++d) {
-    if (d < D) {
+    if (d < D && grid_given) {
+      // slab of a global grid: every local particle must lie inside it
+      origin[d] = given_origin[d];
+      dims[d] = given_dims[d];
+      if (dims[d] < 1 || lo[d] < origin[d] || std::floor((hi[d] - origin[d]) / cutoff) >= dims[d])
+        throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "particle outside the given cell grid");
+    } else if (d < D) {
       origin[d] = lo[d];
       const double extent = hi[d] - lo[d];
       dims[d] = std::max(1, static_cast<int>(std::floor(extent / cutoff)) + 1);  // neighbors.cpp:45-48
@@ -679,6 +685,11 @@ void DevSystem::init_common(int dim, size_t n_, const double* r0_h, const double
   else k_gather_init<3><<<grid_for(n, 256), 256, 0, stream>>>(f, r0aos.p, V0d.p, rho0d.p, cons_h ? consd.p : nullptr);
   CK_LAUNCH("k_gather_init");
   CK(cudaMemcpyAsync(&max_cell, maxc.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (grid_given) {
+    cell_start_h.resize(static_cast<size_t>(ncells + 1));
+    CK(cudaMemcpyAsync(cell_start_h.data(), cell_start.p, cell_start_h.size() * sizeof(long long),
+                       cudaMemcpyDeviceToHost, stream));
+  }
   sync();
 }
 

@@ -62,7 +62,8 @@ constexpr int kThreads = 128;  // one CTA per cell
 
 struct Phase {
   int res[3];      // colour residues per axis
-  int cnt[3];      // cells of this colour per axis
+  int cnt[3];      // cells of this colour per axis (x: inside the task range)
+  int xfirst;      // first task cell x of this colour
   long long ncol;  // cells in the colour
   int forward;
   int S;           // padded stencil tile length, multiple of 8
@@ -193,7 +194,7 @@ __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_fro
 // ------------------------------------------------------------------ staging (step 1)
 template <int D>
 __device__ __forceinline__ void phase_cell(const Phase& ph, long long k, int c[3]) {
-  c[0] = ph.res[0] + 3 * static_cast<int>(k % ph.cnt[0]);
+  c[0] = ph.xfirst + 3 * static_cast<int>(k % ph.cnt[0]);
   c[1] = ph.res[1] + 3 * static_cast<int>((k / ph.cnt[0]) % ph.cnt[1]);
   c[2] = D == 3 ? ph.res[2] + 3 * static_cast<int>(k / (static_cast<long long>(ph.cnt[0]) * ph.cnt[1])) : 0;
 }
@@ -700,8 +701,9 @@ void launch_particle_split(const DevSystem& s, const DFields& f, const Phase& ph
 
 constexpr size_t kSmemBudget = 220 * 1024;
 
+// Shared part of a sweep's launches: tile sizes and the fold constants.
 template <int D>
-void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_scal) {
+Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_scal) {
   if (!s.stencil_ok)
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "damping sweep needs every neighbour inside the 3^D cell stencil (neighbors.hpp:50-52)");
@@ -730,36 +732,71 @@ void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_
       s.fold_dt = dt;
     }
   }
-  const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED;
+  return ph;
+}
+
+// Colour phase `index` of pass `pass` (0: forward, colours ascending; 1:
+// reverse, damping.cpp:112-121); tasks are the colour's cells whose x lies in
+// the task range [task_x0, task_x1) (the whole grid unless a slab is set).
+template <int D>
+void enqueue_phase(DevSystem& s, int scheme, Phase ph, int pass, int index) {
   constexpr int nb = colour_count<D>();
-  for (int pass = 0; pass < 2; ++pass) {
-    ph.forward = pass == 0;
-    for (int bb = 0; bb < nb; ++bb) {
-      const int b = pass == 0 ? bb : nb - 1 - bb;
-      int rem = b;
-      long long total = 1;
-      for (int d = 0; d < 3; ++d) {
-        if (d < D) {
-          ph.res[d] = rem % 3;
-          rem /= 3;
-          ph.cnt[d] = s.dims[d] > ph.res[d] ? (s.dims[d] - ph.res[d] + 2) / 3 : 0;
-        } else {
-          ph.res[d] = 0;
-          ph.cnt[d] = 1;
-        }
-        total *= ph.cnt[d];
-      }
-      ph.ncol = total;
-      if (total == 0) continue;  // empty colour (neighbors.cpp:152)
-      if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
-        if (ord) launch_particle_split<D, true>(s, f, ph);
-        else launch_particle_split<D, false>(s, f, ph);
+  const int b = pass == 0 ? index : nb - 1 - index;
+  ph.forward = pass == 0;
+  int rem = b;
+  long long total = 1;
+  const int x0 = s.task_x0, x1 = s.task_x1 < 0 ? s.dims[0] : std::min(s.task_x1, s.dims[0]);
+  for (int d = 0; d < 3; ++d) {
+    if (d < D) {
+      ph.res[d] = rem % 3;
+      rem /= 3;
+      if (d == 0) {
+        ph.xfirst = x0 + ((ph.res[0] - x0 % 3) + 3) % 3;
+        ph.cnt[0] = x1 > ph.xfirst ? (x1 - ph.xfirst + 2) / 3 : 0;
       } else {
-        launch_phase<D, TLSPH_SCHEME_PAIRWISE_SPLIT, false, 0>(s, f, ph);
+        ph.cnt[d] = s.dims[d] > ph.res[d] ? (s.dims[d] - ph.res[d] + 2) / 3 : 0;
       }
+    } else {
+      ph.res[d] = 0;
+      ph.cnt[d] = 1;
     }
+    total *= ph.cnt[d];
   }
+  ph.ncol = total;
+  if (total == 0) return;  // empty colour (neighbors.cpp:152)
+  const DFields f = s.fields();
+  if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
+    if (s.reduction == TLSPH_REDUCTION_ORDERED) launch_particle_split<D, true>(s, f, ph);
+    else launch_particle_split<D, false>(s, f, ph);
+  } else {
+    launch_phase<D, TLSPH_SCHEME_PAIRWISE_SPLIT, false, 0>(s, f, ph);
+  }
+}
+
+template <int D>
+void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_scal) {
+  const Phase ph = prepare_sweep<D>(s, scheme, eta, dt, from_scal);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int bb = 0; bb < colour_count<D>(); ++bb) enqueue_phase<D>(s, scheme, ph, pass, bb);
   CK_LAUNCH("k_sweep_phase");
+}
+
+// ------------------------------------------------------------------ x-slab halo columns
+// Particles of cell column x in (z, y, cell order): the same sequence on every
+// rank that holds the column (cells keep ascending reference ids).
+__global__ void k_column_copy(const long long* __restrict__ cell_start, const long long* __restrict__ col_off,
+                              int x, int dims0, int ncol_cells, DFields f, double* __restrict__ buf, long long count,
+                              int D, int pack) {
+  const int q = blockIdx.x;  // (y, z) cell of the column
+  if (q >= ncol_cells) return;
+  const long long lin = static_cast<long long>(q) * dims0 + x;
+  const long long p0 = cell_start[lin], p1 = cell_start[lin + 1];
+  const long long o = col_off[q];
+  for (long long e = threadIdx.x; e < p1 - p0; e += blockDim.x)
+    for (int d = 0; d < D; ++d) {
+      if (pack) buf[d * count + o + e] = f.v[d][p0 + e];
+      else f.v[d][p0 + e] = buf[d * count + o + e];
+    }
 }
 
 // Bit-for-bit check of div_by against IEEE division on the device.
@@ -793,6 +830,48 @@ void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, boo
   if (D == 2) enqueue_sweep_d<2>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
   else enqueue_sweep_d<3>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
 }
+
+void DevSystem::enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index) {
+  const int nb = D == 2 ? 9 : 27;
+  if (pass < 0 || pass > 1 || index < 0 || index >= nb)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "colour phase out of range");
+  if (D == 2) enqueue_phase<2>(*this, scheme, prepare_sweep<2>(*this, scheme, eta_tilde, dt_fixed, false), pass, index);
+  else enqueue_phase<3>(*this, scheme, prepare_sweep<3>(*this, scheme, eta_tilde, dt_fixed, false), pass, index);
+  CK_LAUNCH("k_sweep_phase");
+}
+
+namespace {
+// cell count of a column and the exclusive prefix of its cells' particle counts
+std::vector<long long> column_offsets(const DevSystem& s, int x) {
+  if (!s.grid_given) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "column transfer needs a slab system (given grid)");
+  if (x < 0 || x >= s.dims[0]) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "column out of range");
+  const int nq = static_cast<int>(s.ncells / s.dims[0]);
+  std::vector<long long> off(static_cast<size_t>(nq) + 1, 0);
+  for (int q = 0; q < nq; ++q) {
+    const long long lin = static_cast<long long>(q) * s.dims[0] + x;
+    off[q + 1] = off[q] + (s.cell_start_h[lin + 1] - s.cell_start_h[lin]);
+  }
+  return off;
+}
+
+void column_copy(DevSystem& s, int x, double* buf, bool pack) {
+  const std::vector<long long> off = column_offsets(s, x);
+  const int nq = static_cast<int>(off.size()) - 1;
+  const long long count = off.back();
+  if (count == 0) return;
+  DBuf<long long> doff;
+  doff.alloc(off.size());
+  CK(cudaMemcpyAsync(doff.p, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice, s.stream));
+  k_column_copy<<<static_cast<unsigned>(nq), 64, 0, s.stream>>>(s.cell_start.p, doff.p, x, s.dims[0], nq, s.fields(),
+                                                                buf, count, s.D, pack ? 1 : 0);
+  CK_LAUNCH("k_column_copy");
+  s.sync();  // the buffer is handed to another stream / library (NCCL, torch)
+}
+}  // namespace
+
+long long DevSystem::column_count(int x) const { return column_offsets(*this, x).back(); }
+void DevSystem::pack_column(int x, double* dev_dst) { column_copy(*this, x, dev_dst, true); }
+void DevSystem::unpack_column(int x, const double* dev_src) { column_copy(*this, x, const_cast<double*>(dev_src), false); }
 
 unsigned long long selftest_division(long long n, unsigned long long seed) {
   DBuf<unsigned long long> bad;

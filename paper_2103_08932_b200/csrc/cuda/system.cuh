@@ -61,6 +61,13 @@ class DevSystem {
   long long max_cell_slots = 0;  // max CSR slots owned by one cell
   int max_row = 0;               // max slots of one particle
   bool stencil_ok = true;
+  // x-slab decomposition: an explicit (global) grid instead of the bounding
+  // box of the local particles, and the cell-x range whose cells are sweep tasks
+  bool grid_given = false;
+  double given_origin[3] = {0, 0, 0};
+  int given_dims[3] = {1, 1, 1};
+  int task_x0 = 0, task_x1 = -1;  // -1: dims[0]
+  std::vector<long long> cell_start_h;  // host copy, for column packing
 
   // fields (sorted order)
   DBuf<double> r0[3], r[3], v[3], a[3], body[3];
@@ -140,6 +147,12 @@ class DevSystem {
   // damping (damping.cu)
   void damping_sweep(int scheme, double eta_tilde, double dt, int count);
   void enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars);
+  // one colour phase (pass 0 forward / 1 reverse, index-th colour of the pass)
+  void enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index);
+  // x-slab halo columns (sweep.cu)
+  long long column_count(int x) const;
+  void pack_column(int x, double* dev_dst);
+  void unpack_column(int x, const double* dev_src);
   void particle_split_update(long long i, double eta, double dt_half);
   void pairwise_split_update(long long i, long long slot, double eta, double dt_half);
   void explicit_damping_accel(double eta, double* out_host);

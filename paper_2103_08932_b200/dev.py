@@ -102,6 +102,14 @@ def lib():
     L.tlsph_dev_create.argtypes = [I, S, D, D, D, C.POINTER(C.c_uint8), C.c_double, C.POINTER(P)]
     L.tlsph_dev_create_with_csr.argtypes = [I, S, D, D, D, C.POINTER(C.c_uint8), C.c_double,
                                             C.POINTER(C.c_int64), C.POINTER(C.c_int32), D, D, D, D, C.POINTER(P)]
+    L.tlsph_dev_create_in_grid.argtypes = [I, S, D, D, D, C.POINTER(C.c_uint8), C.c_double, D, C.POINTER(I),
+                                           C.POINTER(P)]
+    L.tlsph_dev_set_task_range.argtypes = [P, I, I]
+    L.tlsph_dev_damping_phase.argtypes = [P, I, C.c_double, C.c_double, I, I]
+    L.tlsph_dev_column_count.argtypes = [P, I]
+    L.tlsph_dev_column_count.restype = C.c_int64
+    L.tlsph_dev_pack_column.argtypes = [P, I, C.c_void_p]
+    L.tlsph_dev_unpack_column.argtypes = [P, I, C.c_void_p]
     L.tlsph_dev_destroy.argtypes = [P]
     L.tlsph_dev_size.argtypes = [P]
     L.tlsph_dev_size.restype = S
@@ -177,7 +185,9 @@ def random_choice(eta, alpha, seed, n):
 class DeviceSystem:
     """Device-resident ParticleSystem<D> + CellGrid + ReferenceNeighborhood (sorted SoA on the GPU)."""
 
-    def __init__(self, r0, V0, rho0, h, constrained=None, csr=None):
+    def __init__(self, r0, V0, rho0, h, constrained=None, csr=None, grid=None):
+        """grid=(origin, dims): bin into that (global) cell grid instead of the
+        bounding box of r0 -- one x-slab of a decomposed body (tlsph_dev_create_in_grid)."""
         r0 = np.ascontiguousarray(r0, dtype=np.float64)
         self.n, self.dim = r0.shape
         V0 = np.ascontiguousarray(np.broadcast_to(np.asarray(V0, dtype=np.float64), (self.n,)))
@@ -186,7 +196,13 @@ class DeviceSystem:
         cons_p = cons.ctypes.data_as(C.POINTER(C.c_uint8)) if cons is not None else None
         self.h = float(h)
         self._h = C.c_void_p()
-        if csr is None:
+        if grid is not None:
+            origin = np.zeros(3)
+            origin[: self.dim] = np.asarray(grid[0], dtype=np.float64)[: self.dim]
+            dims = (C.c_int * 3)(*[int(x) for x in list(grid[1])[: self.dim]] + [1] * (3 - self.dim))
+            _check(lib().tlsph_dev_create_in_grid(self.dim, self.n, _dp(r0), _dp(V0), _dp(rho0), cons_p, self.h,
+                                                  _dp(origin), dims, C.byref(self._h)))
+        elif csr is None:
             _check(lib().tlsph_dev_create(self.dim, self.n, _dp(r0), _dp(V0), _dp(rho0), cons_p, self.h,
                                           C.byref(self._h)))
         else:
@@ -313,6 +329,27 @@ class DeviceSystem:
         else:
             _check(lib().tlsph_dev_damping_sweeps(self._h, SCHEMES[scheme], eta_tilde, dt, count))
         return float(lib().tlsph_dev_last_elapsed(self._h))
+
+    # ---- x-slab decomposition (paper_2103_08932_b200/slabs.py)
+    def set_task_range(self, x0, x1):
+        _check(lib().tlsph_dev_set_task_range(self._h, int(x0), int(x1)))
+
+    def damping_phase(self, scheme, eta_tilde, dt, pass_, index):
+        _check(lib().tlsph_dev_damping_phase(self._h, SCHEMES[scheme], float(eta_tilde), float(dt), int(pass_),
+                                             int(index)))
+
+    def column_count(self, x):
+        c = int(lib().tlsph_dev_column_count(self._h, int(x)))
+        if c < 0:
+            raise TlsphError(1, lib().tlsph_dev_last_error().decode())
+        return c
+
+    def pack_column(self, x, device_ptr):
+        """Velocities of cell column x into the device buffer at device_ptr (D x count doubles)."""
+        _check(lib().tlsph_dev_pack_column(self._h, int(x), C.c_void_p(int(device_ptr))))
+
+    def unpack_column(self, x, device_ptr):
+        _check(lib().tlsph_dev_unpack_column(self._h, int(x), C.c_void_p(int(device_ptr))))
 
     def particle_split_update(self, i, eta, dt_half):
         _check(lib().tlsph_dev_particle_split_update(self._h, i, eta, dt_half))
