@@ -360,6 +360,14 @@ __global__ void k_minvf(const double* __restrict__ m, const uint8_t* __restrict_
   y[s] = flag[s] ? -r : r;
 }
 
+__global__ void k_qf(const double* __restrict__ pf, const int* __restrict__ nbr, const double* __restrict__ minvf,
+                     double* __restrict__ qf, long long nslots) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nslots) return;
+  const double y = minvf[nbr[s]];
+  qf[s] = y > 0.0 ? pf[s] * y : 0.0;
+}
+
 __global__ void k_cell_slot(const long long* __restrict__ cell_start, const long long* __restrict__ offs,
                             long long ncells, long long* __restrict__ out) {
   const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -539,6 +547,7 @@ DFields DevSystem::fields() const {
   f.r0_len = r0_len.p;
   f.dwdr0 = dwdr0.p;
   f.pf = pf.p;
+  f.qf = qf.p;
   f.nloc = nloc.p;
   f.cell_start = cell_start.p;
   f.cell = cutoff;
@@ -737,9 +746,16 @@ void DevSystem::build_neighbourhoods() {
 void DevSystem::refresh_minvf() {
   k_minvf<<<grid_for(n, 256), 256, 0, stream>>>(m.p, flag.p, minvf.p, n);
   CK_LAUNCH("k_minvf");
+  if (nslots > 0) {
+    qf.alloc(static_cast<size_t>(nslots));
+    k_qf<<<grid_for(nslots, 256), 256, 0, stream>>>(pf.p, nbr.p, minvf.p, qf.p, nslots);
+    CK_LAUNCH("k_qf");
+  }
+  fold_valid = false;  // constrained particles are marked in the fold constants
 }
 
 void DevSystem::compute_sweep_stats() {
+  refresh_minvf();
   cell_slot.alloc(static_cast<size_t>(ncells + 1));
   k_cell_slot<<<grid_for(ncells + 1, 256), 256, 0, stream>>>(cell_start.p, offs.p, ncells, cell_slot.p);
   CK_LAUNCH("k_cell_slot");

@@ -70,6 +70,7 @@ struct Phase {
   int SC;          // max slots per cell, multiple of 8
   int MC;          // max particles per cell, even
   int MR;          // pairwise scratch per warp (max slots per particle), 0 for particle split
+  int fast;        // FAST particle-split tile: no masses, per-slot mass factors instead
   double eta;
   double dt;       // used when dt_from_scalars == 0
   int dt_from_scalars;
@@ -95,6 +96,7 @@ struct Tile {
   double* sden;
   double* sy;
   double* spf;           // aligned superset of the cell's pair factors
+  double* sqf;           // FAST: aligned superset of the cell's pair_factor / m_j (0: clamped j)
   double* skf;           // pairwise scratch, D x MR
   uint16_t* snl;         // aligned superset of stencil-local neighbour indices
 };
@@ -103,17 +105,19 @@ __host__ __device__ inline int mco(int MC) { return (MC + 4) & ~1; }
 constexpr int kHeader = 16 + 16 * 9;  // barrier + spare word + segment table
 
 template <int D>
-__host__ __device__ inline size_t tile_bytes(int S, int SC, int MC, int MR) {
+__host__ __device__ inline size_t tile_bytes(int S, int SC, int MC, int MR, int fast) {
   size_t b = kHeader;
-  b += sizeof(double) * (static_cast<size_t>(D + 2) * S);
+  b += sizeof(double) * (static_cast<size_t>(fast ? D : D + 2) * S);
   b += sizeof(long long) * static_cast<size_t>(mco(MC));
   b += sizeof(double) * static_cast<size_t>(3 * mco(MC));
-  b += sizeof(double) * static_cast<size_t>(SC + 2);
+  b += sizeof(double) * static_cast<size_t>(SC + 2) * (fast ? 2 : 1);
   b += sizeof(double) * static_cast<size_t>(D * MR);
   b += sizeof(uint16_t) * static_cast<size_t>(SC + 16);
   return (b + 15) & ~static_cast<size_t>(15);
 }
 
+// Tile layout: header | v[D][S] | (m[S] | 1/m[S]) | offs | diag | den | y | pf | (qf) | pairwise scratch | nloc
+// (the bracketed sections: masses for ORDERED / pairwise, qf for FAST)
 template <int D>
 __device__ inline Tile<D> carve(unsigned char* base, const Phase& ph) {
   Tile<D> t;
@@ -125,14 +129,22 @@ __device__ inline Tile<D> carve(unsigned char* base, const Phase& ph) {
   double* d = reinterpret_cast<double*>(base + kHeader);
 #pragma unroll
   for (int k = 0; k < D; ++k) t.sv[k] = d + static_cast<size_t>(k) * ph.S;
-  t.sm = d + static_cast<size_t>(D) * ph.S;
-  t.smf = t.sm + ph.S;
-  t.soff = reinterpret_cast<long long*>(t.smf + ph.S);
+  double* after_v = d + static_cast<size_t>(D) * ph.S;
+  if (ph.fast) {
+    t.sm = nullptr;
+    t.smf = nullptr;
+    t.soff = reinterpret_cast<long long*>(after_v);
+  } else {
+    t.sm = after_v;
+    t.smf = t.sm + ph.S;
+    t.soff = reinterpret_cast<long long*>(t.smf + ph.S);
+  }
   t.sdiag = reinterpret_cast<double*>(t.soff + mc);
   t.sden = t.sdiag + mc;
   t.sy = t.sden + mc;
   t.spf = t.sy + mc;
-  t.skf = t.spf + ph.SC + 2;
+  t.sqf = ph.fast ? t.spf + ph.SC + 2 : nullptr;
+  t.skf = (ph.fast ? t.sqf : t.spf) + ph.SC + 2;
   t.snl = reinterpret_cast<uint16_t*>(t.skf + static_cast<size_t>(D) * ph.MR);
   return t;
 }
@@ -186,7 +198,9 @@ __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_fro
   }
   const double diag = sb - f.m[i];
   const double den = diag * diag + sb2;
-  f.fdiag[i] = diag;
+  // a constrained particle is never updated as i (damping.cpp:151); the FAST
+  // chain reads the mark from its diagonal
+  f.fdiag[i] = f.flag[i] ? __longlong_as_double(0x7ff8000000000000ll) : diag;
   f.fden[i] = den;
   f.fy[i] = 1.0 / den;
 }
@@ -278,7 +292,7 @@ __device__ __forceinline__ void locate_pair(const RowPairs& r, int p, int& q, in
 // the flattened row table, the cell's slot block, row offsets and fold
 // constants by bulk copies on the mbarrier. MASS: also stage m (ORDERED
 // divisions, pairwise).
-template <int D, bool FOLD, bool MASS, bool PDL = false>
+template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false>
 __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
                                               long long sstart, long long send, int lane) {
   constexpr int kSegs = seg_count<D>();
@@ -302,9 +316,10 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   else if (lane == 1) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
   else if (lane == 2) mybytes = static_cast<uint32_t>((cs.n1() - cs.n0()) * 2);
   else if (FOLD && lane == 3) mybytes = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8 * 3);
+  else if (QF && lane == 4) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
   uint32_t total = mybytes;
 #pragma unroll
-  for (int o = 2; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+  for (int o = 4; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
   if (lane == 0) {
     mbar_init(t.bar, 1);
     fence_proxy_async_smem();  // the initialised barrier is visible to the TMA unit
@@ -323,6 +338,8 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
     tma_load_1d(t.sdiag, f.fdiag + cs.q0(), nb, t.bar);
     tma_load_1d(t.sden, f.fden + cs.q0(), nb, t.bar);
     tma_load_1d(t.sy, f.fy + cs.q0(), nb, t.bar);
+  } else if (QF && lane == 4) {
+    tma_load_1d(t.sqf, f.qf + cs.f0(), mybytes, t.bar);
   }
   stamp(blockIdx.x, 3);
   // PDL: everything above is static; the velocities are written by the preceding phase
@@ -337,7 +354,7 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
     if (p < rp.total) {
 #pragma unroll
       for (int d = 0; d < D; ++d) cp_async16(t.sv[d] + tt, f.v[d] + g);
-      cp_async16(t.smf + tt, f.minvf + g);
+      if (!QF) cp_async16(t.smf + tt, f.minvf + g);
       if (MASS) cp_async16(t.sm + tt, f.m + g);
     }
   }
@@ -614,7 +631,7 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   locate_row<D>(f, c, lane, sstart, send);
   if (cs.p0 == cs.p1) return;
   stamp(blockIdx.x, 2);
-  issue_staging<D, true, false, true>(f, t, cs, sstart, send, lane);
+  issue_staging<D, true, false, true, true>(f, t, cs, sstart, send, lane);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
@@ -622,8 +639,8 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   ChainTile<D> ct;
 #pragma unroll
   for (int d = 0; d < D; ++d) ct.sv[d] = t.sv[d];
-  ct.smf = t.smf;
   ct.pf = t.spf + (cs.s0 - cs.f0());
+  ct.qf = t.sqf + (cs.s0 - cs.f0());
   ct.nl = t.snl + (cs.s0 - cs.n0());
   ct.offs = t.soff + (cs.p0 - cs.o0());
   ct.s0 = cs.s0;
@@ -646,7 +663,7 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 
 template <int D, int K>
 void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
-  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR);
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     CK(cudaFuncSetAttribute(k_sweep_fast<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -670,7 +687,7 @@ void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
 
 template <int D, int SCHEME, bool ORDERED, int K>
 void launch_phase(const DevSystem& s, const DFields& f, const Phase& ph) {
-  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR);
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     CK(cudaFuncSetAttribute(k_sweep_phase<D, SCHEME, ORDERED, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -716,7 +733,10 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
   ph.SC = (std::max<int>(static_cast<int>(s.max_cell_slots), 1) + 7) & ~7;
   ph.MC = (std::max(s.max_cell, 1) + 1) & ~1;
   ph.MR = scheme == TLSPH_SCHEME_PAIRWISE_SPLIT ? ((std::max(s.max_row, 1) + 1) & ~1) : 0;
-  const size_t per_cell = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR);
+  // the single-warp FAST kernel (launch_particle_split) uses the mass-free tile
+  ph.fast = scheme == TLSPH_SCHEME_PARTICLE_SPLIT && s.reduction != TLSPH_REDUCTION_ORDERED &&
+            (std::max(s.max_row, 1) + kWarp - 1) / kWarp <= 4;
+  const size_t per_cell = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
   if (per_cell > kSmemBudget)
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "damping sweep: a cell's stencil and slot block (" + std::to_string(per_cell) +

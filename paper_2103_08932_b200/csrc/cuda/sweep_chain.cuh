@@ -11,13 +11,13 @@
 //
 // Software pipeline. Everything but the stencil velocities is static during
 // the chain, so the slot metadata of the next particle is loaded while the
-// current one runs, in three stages that never stall the chain: (A) its
-// neighbour indices and pair factors, issued at the top of the iteration;
-// (C) the masses of those neighbours, issued after the chain's velocity
-// gathers; (D) the derived coefficients, formed after the scatter. Row
-// extents are read two particles ahead. A constrained particle or one without
-// neighbours (damping.cpp:54, :151) runs the same code with its writes
-// disabled, so the loop has no data-dependent branch.
+// current one runs: (A) its neighbour indices, pair factors and per-slot mass
+// factors pair_factor / m_j (precomputed per body, so no gather through the
+// neighbour index), issued at the top of the iteration; (C) its fold
+// constants; (D) the derived coefficients, formed after the scatter. Row
+// extents are read two particles ahead. A constrained particle (NaN
+// diagonal) or one without neighbours (damping.cpp:54, :151) runs the same
+// code with its writes disabled, so the loop has no data-dependent branch.
 #pragma once
 #include <cstdint>
 
@@ -26,12 +26,12 @@ namespace tlsph_cuda {
 template <int D>
 struct ChainTile {
   double* sv[D];          // staged stencil velocities
-  const double* smf;      // staged signed RN(1/m) (negative: clamped)
   const double* pf;       // the cell's pair factors, cell-relative slot index
+  const double* qf;       // pair_factor / m_j per slot (0: clamped j, never written)
   const uint16_t* nl;     // the cell's stencil-local neighbour indices
   const long long* offs;  // offs[p] - s0 = cell-relative first slot of particle p
   long long s0;
-  const double* diag;     // per-particle fold constants
+  const double* diag;     // per-particle fold constants (NaN: constrained particle)
   const double* y;        // RN(1 / denominator)
   int lbase;              // tile index of the cell's first particle
   int np;
@@ -93,18 +93,18 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     row(pk, lo, cnt);
     diag = t.diag[pk];
     y = t.y[pk];
-    skip = t.smf[t.lbase + pk] < 0.0 || cnt == 0;
+    skip = diag != diag || cnt == 0;
     upm = 0;
 #pragma unroll
     for (int u = 0; u < K; ++u) {
       const int s = lane + u * 32;
       const bool v = s < cnt;
       const int j = v ? t.nl[lo + s] : t.lbase + pk;  // invalid lanes read i itself with b = 0
-      const double mf = t.smf[j];
-      const bool up = v && mf > 0.0;                 // clamped j: never written (damping.cpp:84-86)
+      const double q = v ? t.qf[lo + s] : 0.0;
+      const bool up = q != 0.0;                      // clamped j: never written (damping.cpp:84-86)
       jq[u] = j;
       bq[u] = v ? t.kb * t.pf[lo + s] : 0.0;
-      bmq[u] = up ? bq[u] * mf : 0.0;
+      bmq[u] = t.kb * q;
       c1[u] = 1.0 + bmq[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
       upm |= up ? (1u << u) : 0u;
@@ -117,13 +117,14 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     const int li1 = t.lbase + pk1;
     // (A) next particle's indices and pair factors
     int jn[K];
-    double pfn[K];
+    double pfn[K], qfn[K];
 #pragma unroll
     for (int u = 0; u < K; ++u) {
       const int s = lane + u * 32;
       const bool v = s < cnt1;
       jn[u] = v ? t.nl[lo1 + s] : li1;
       pfn[u] = v ? t.pf[lo1 + s] : 0.0;
+      qfn[u] = v ? t.qf[lo1 + s] : 0.0;
     }
     // row extents two particles ahead
     const int pk2 = kk + 2 < np ? pidx(kk + 2) : pk1;
@@ -138,11 +139,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     for (int u = 0; u < K; ++u)
 #pragma unroll
       for (int d = 0; d < D; ++d) vq[u][d] = t.sv[d][jq[u]];
-    // (C) next particle's neighbour masses and fold constants
-    double mfn[K];
-#pragma unroll
-    for (int u = 0; u < K; ++u) mfn[u] = t.smf[jn[u]];
-    const double mfi1 = t.smf[li1];
+    // (C) next particle's fold constants
     const double diag1 = t.diag[pk1], y1 = t.y[pk1];
 
     double P[D], Y[K][D];
@@ -173,15 +170,14 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     // (D) next particle's coefficients
     diag = diag1;
     y = y1;
-    skip = mfi1 < 0.0 || cnt1 == 0;
+    skip = diag != diag || cnt1 == 0;
     upm = 0;
 #pragma unroll
     for (int u = 0; u < K; ++u) {
-      const bool v = lane + u * 32 < cnt1;
-      const bool up = v && mfn[u] > 0.0;
+      const bool up = qfn[u] != 0.0;
       jq[u] = jn[u];
       bq[u] = t.kb * pfn[u];
-      bmq[u] = up ? bq[u] * mfn[u] : 0.0;
+      bmq[u] = t.kb * qfn[u];
       c1[u] = 1.0 + bmq[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
       upm |= up ? (1u << u) : 0u;

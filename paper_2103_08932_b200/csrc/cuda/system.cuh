@@ -96,6 +96,7 @@ class DevSystem {
   DBuf<long long> offs;
   DBuf<int> nbr;
   DBuf<double> r0_len, e0[3], dwdr0, pf;
+  DBuf<double> qf;  // pf * RN(1/m_j), 0 for clamped j: the FAST sweep's per-slot mass factor
   DBuf<uint16_t> nloc;
 
   // scratch
@@ -118,7 +119,7 @@ class DevSystem {
   void load_csr(const int64_t* offsets, const int32_t* neighbor, const double* r0_len_h, const double* e0_h,
                 const double* dwdr0_h, const double* pf_h);
   void compute_sweep_stats();
-  void refresh_minvf();
+  void refresh_minvf();  // also refreshes qf once the CSR exists
 
   // transfers (state.cu)
   void set_field(int field, const double* host);

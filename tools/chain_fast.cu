@@ -14,8 +14,8 @@ constexpr int S = 512, NP = 18, K = 3, D = 3, CNT = 76;
 
 struct Smem {
   double sv[D][S];
-  double smf[S];
   double pf[NP * CNT];
+  double qf[NP * CNT];
   uint16_t nl[NP * CNT];
   long long offs[NP + 2];
   double diag[NP], y[NP];
@@ -31,11 +31,11 @@ __global__ void __launch_bounds__(128) chain(const uint16_t* nloc, const double*
   const int nthr = blockDim.x;
   for (int e = lane; e < S; e += nthr) {
     for (int d = 0; d < D; ++d) t.sv[d][e] = 0.001 * e + d;
-    t.smf[e] = (e % 97 == 5) ? -1.0 : 1.0 / (1.0 + e * 1e-3);
   }
   for (int e = lane; e < NP * CNT; e += nthr) {
     t.nl[e] = nloc[e];
     t.pf[e] = pf[e];
+    t.qf[e] = (nloc[e] % 97 == 5) ? 0.0 : pf[e] / (1.0 + nloc[e] * 1e-3);
   }
   if (lane <= NP) t.offs[lane] = lane * CNT;
   if (lane < NP) {
@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(128) chain(const uint16_t* nloc, const double*
   __syncthreads();
   tlsph_cuda::ChainTile<D> ct;
   for (int d = 0; d < D; ++d) ct.sv[d] = t.sv[d];
-  ct.smf = t.smf;
   ct.pf = t.pf;
+  ct.qf = t.qf;
   ct.nl = t.nl;
   ct.offs = t.offs;
   ct.s0 = 0;
