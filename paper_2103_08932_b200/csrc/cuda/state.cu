@@ -336,20 +336,25 @@ __global__ void k_nbr_fill(DFields f, double cutoff, double h, double sigma, int
 }
 
 // ------------------------------------------------------------------ transfers
+// Component arrays of one field, passed by value (no device-side pointer table).
+struct FieldPtrs {
+  double* p[9];
+};
+
 __global__ void k_aos_to_soa(const double* __restrict__ src, int comps, long long n, const int* __restrict__ perm,
-                             double** dst) {
+                             FieldPtrs dst) {
   const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const long long i = perm[s];
-  for (int c = 0; c < comps; ++c) dst[c][s] = src[i * comps + c];
+  for (int c = 0; c < comps; ++c) dst.p[c][s] = src[i * comps + c];
 }
 
 __global__ void k_soa_to_aos(double* __restrict__ dst, int comps, long long n, const int* __restrict__ perm,
-                             double* const* src) {
+                             FieldPtrs src) {
   const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const long long i = perm[s];
-  for (int c = 0; c < comps; ++c) dst[i * comps + c] = src[c][s];
+  for (int c = 0; c < comps; ++c) dst[i * comps + c] = src.p[c][s];
 }
 
 __global__ void k_minvf(const double* __restrict__ m, const uint8_t* __restrict__ flag, double* __restrict__ y,
@@ -840,6 +845,11 @@ namespace {
 struct FieldSpec {
   int comps;
   std::vector<double*> ptrs;
+  FieldPtrs pack() const {
+    FieldPtrs fp{};
+    for (size_t k = 0; k < ptrs.size() && k < 9; ++k) fp.p[k] = ptrs[k];
+    return fp;
+  }
 };
 }  // namespace
 
@@ -891,11 +901,8 @@ void DevSystem::set_field(int field, const double* host) {
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "r0 is fixed at construction (the cell grid is built from it)");
   FieldSpec fs = field_spec(*this, field);
   tmp.alloc(N * fs.comps);
-  DBuf<double*> ptrs;
-  ptrs.alloc(fs.ptrs.size());
-  CK(cudaMemcpyAsync(ptrs.p, fs.ptrs.data(), fs.ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, stream));
   CK(cudaMemcpyAsync(tmp.p, host, N * fs.comps * sizeof(double), cudaMemcpyHostToDevice, stream));
-  k_aos_to_soa<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, ptrs.p);
+  k_aos_to_soa<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, fs.pack());
   CK_LAUNCH("k_aos_to_soa");
   if (field == TLSPH_FIELD_BODY) has_body = true;
   if (field == TLSPH_FIELD_M) {
@@ -919,10 +926,7 @@ void DevSystem::get_field(int field, double* host) const {
   }
   FieldSpec fs = field_spec(*this, field);
   self->tmp.alloc(N * fs.comps);
-  DBuf<double*> ptrs;
-  ptrs.alloc(fs.ptrs.size());
-  CK(cudaMemcpyAsync(ptrs.p, fs.ptrs.data(), fs.ptrs.size() * sizeof(double*), cudaMemcpyHostToDevice, stream));
-  k_soa_to_aos<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, ptrs.p);
+  k_soa_to_aos<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, fs.pack());
   CK_LAUNCH("k_soa_to_aos");
   CK(cudaMemcpyAsync(host, tmp.p, N * fs.comps * sizeof(double), cudaMemcpyDeviceToHost, stream));
   sync();

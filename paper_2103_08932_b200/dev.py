@@ -240,8 +240,12 @@ class DeviceSystem:
             return (self.n, self.dim, self.dim)
         return (self.n,)
 
-    def get(self, name):
-        out = np.empty(self._shape(name))
+    def get(self, name, out=None):
+        """Field in reference order; `out` (e.g. a pinned host array) receives it when given."""
+        if out is None:
+            out = np.empty(self._shape(name))
+        elif out.shape != self._shape(name) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous float64 array of shape {self._shape(name)}")
         _check(lib().tlsph_dev_get_field(self._h, FIELDS[name], _dp(out)))
         return out
 
