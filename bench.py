@@ -54,32 +54,58 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed region: NVML every
+    few milliseconds (nvidia-ml-py), nvidia-smi as the fallback."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period=0.002):
         self.index = index
-        self.samples = []
+        self.period = period
+        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = get_reasons(h)
+            self.samples.append((float(sm), float(mx), {k for k, b in self.REASONS.items() if bits & b}))
+            self._stop.wait(self.period)
+
+    def _smi(self):
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                names = list(self.REASONS)
+                self.samples.append((float(f[0]), float(f[1]),
+                                     {names[k] for k in range(4) if f[2 + k].lower().startswith("active")}))
             except Exception:
                 pass
             self._stop.wait(0.2)
 
+    def _run(self):
+        try:
+            self._nvml()
+        except Exception:
+            self._smi()
+
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.05)  # first sample before the timed region starts
         return self
 
     def __exit__(self, *exc):
@@ -88,19 +114,13 @@ class ClockSampler:
             self._t.join(timeout=6)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            try:
-                sm.append(float(s[0]))
-                mx = float(s[1])
-                for k, name in enumerate(names):
-                    if s[3 + k].lower().startswith("active"):
-                        reasons.add(name)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = [x[0] for x in self.samples]
+        reasons = set()
+        for x in self.samples:
+            reasons |= x[2]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": self.samples[-1][1] if self.samples else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 def dist_env():
@@ -136,8 +156,7 @@ def cuda_sync():
 
 
 # ----------------------------------------------------------------------------- cfg2 (headline)
-def free_slots(nb, cons):
-    off = nb["offsets"]
+def free_slots(off, cons):
     if cons is None:
         return int(off[-1]), len(off) - 1
     counts = off[1:] - off[:-1]
@@ -168,8 +187,8 @@ def run_cfg2(args, ws, rank):
     from paper_2103_08932_b200 import scenarios as S
     cfg = S.cfg2()
     d = S.build_device(cfg, prepare=False)
-    nb = d.neighborhood()
-    s_free, n_free = free_slots(nb, cfg["constrained"])
+    offsets = d.row_offsets()
+    s_free, n_free = free_slots(offsets, cfg["constrained"])
     dpu_per_sweep = 2 * s_free
     b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_free)
     eta_t = cfg["eta"] / cfg["alpha"]
@@ -224,12 +243,12 @@ def run_cfg2(args, ws, rank):
         "dtype": "f64",
         "data": "synthetic (seeded 64^3 lattice, v ~ N(0,1) Box-Muller from RandomSource(1))",
         "config": {"workload": "cfg2: 3D damping-only sweep, 64^3 lattice, 27-colour particle-split, alpha=1",
-                   "particles": int(d.n), "slots": int(nb["offsets"][-1]), "dpu_per_step": dpu_per_sweep,
+                   "particles": int(d.n), "slots": int(offsets[-1]), "dpu_per_step": dpu_per_sweep,
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (CSR 200 MB + 20 MB state > 126 MB L2); no flush",
                    "reduction": "fast (warp-shuffle)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": load_traffic(), "kernel": "k_sweep_phase (one colour phase)",
+                     "traffic": load_traffic(), "kernel": "k_sweep_fast (one colour phase)",
                      "bytes_per_launch": b_sweep / phase_launches, "avg_launch_s": avg_launch,
                      "peak_source": peak_src},
         "e2e": {"value": e2e, "unit": "DPU/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -292,7 +311,7 @@ def run_reference(args, ws, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg2"])

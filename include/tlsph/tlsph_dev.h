@@ -151,7 +151,9 @@ tlsph_status tlsph_dev_grid_info(const tlsph_dev* dev, int* dims, double* origin
  * reference ids of each cell in ascending order. */
 tlsph_status tlsph_dev_grid_cells(const tlsph_dev* dev, int32_t* cell_of, int64_t* cell_start,
                                   int32_t* cell_particles);
-/* ReferenceNeighborhood<D> (neighbors.hpp:67-82) in reference order. */
+/* ReferenceNeighborhood<D> (neighbors.hpp:67-82) in reference order. Any
+ * output may be null; with every slot array null only the row offsets are
+ * produced (no per-slot conversion). */
 tlsph_status tlsph_dev_get_neighborhood(const tlsph_dev* dev, int64_t* offsets, int32_t* neighbor, double* r0_len,
                                         double* e0, double* dwdr0, double* pair_factor);
 

@@ -958,6 +958,11 @@ void DevSystem::get_neighborhood(int64_t* offsets, int32_t* neighbor, double* r0
   k_row_counts_ref<<<grid_for(n, 256), 256, 0, stream>>>(f, cnt.p);
   CK_LAUNCH("k_row_counts_ref");
   exclusive_scan<long long>(cnt.p, n, off_ref.p, stream);
+  if (!neighbor && !r0_len_h && !e0_h && !dwdr0_h && !pf_h) {  // row offsets only
+    if (offsets) CK(cudaMemcpyAsync(offsets, off_ref.p, (N + 1) * sizeof(long long), cudaMemcpyDeviceToHost, stream));
+    sync();
+    return;
+  }
   DBuf<int> nb;
   DBuf<double> ln, e, dw, p;
   nb.alloc(S);

@@ -284,6 +284,13 @@ class DeviceSystem:
             stride *= 3
         return [lin[colour == b].tolist() for b in range(3 ** self.dim)]
 
+    def row_offsets(self):
+        """Reference-order CSR row offsets only (no slot arrays transferred)."""
+        off = np.empty(self.n + 1, dtype=np.int64)
+        _check(lib().tlsph_dev_get_neighborhood(self._h, off.ctypes.data_as(C.POINTER(C.c_int64)), None, None, None,
+                                                None, None))
+        return off
+
     def neighborhood(self):
         S = self.slot_count
         off = np.empty(self.n + 1, dtype=np.int64)
