@@ -267,6 +267,63 @@ def run_cfg2(args, ws, rank):
     return out
 
 
+def particle_steps(args, ws, rank):
+    """Second half of BASELINE.json's metric: particle-steps/s of the full device-resident loop
+    (TL-SPH step + random-choice splitting damping, runner.cpp:341-391) on cfg3, the 3D cantilever
+    beam (640,000 particles), FAST reductions; the reference CPU path (oracle port, OpenMP) timed on
+    a bounded sample of the same loop."""
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg3()
+    steps = max(50, min(args.ps_steps, 2000))
+    d = S.build_device(cfg, prepare=True)
+    d.set_reduction("fast")
+    r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=steps, seed=cfg["seed"])
+    t_max = barrier_and_max(r["total_s"], ws)
+    n = int(d.n)
+    slots = int(d.slot_count)
+    # BASELINE.md §4: B_step = S*2*(4+8+8D) + N*P_s (+ B_sweep on damped steps), P_s = 1,091 B (3D)
+    b_elastic = slots * 2 * (4 + 8 + 8 * 3) + n * 1091
+    t_el = r["elastic_s"] / max(r["steps"], 1)
+    peak, peak_src = load_peaks()
+    out = {"metric": "particle-steps/s (fp64 TL-SPH step + splitting damping, random choice)",
+           "value": n * r["steps"] * ws / t_max, "unit": "PS/s", "steps": r["steps"], "damped_steps": r["damped"],
+           "ms_per_step": t_max / max(r["steps"], 1) * 1e3, "elastic_ms_per_step": t_el * 1e3,
+           "damping_ms_per_damped_step": r["damping_s"] / max(r["damped"], 1) * 1e3,
+           "config": {"workload": "cfg3: 3D cantilever beam 400x40x40, neo-Hookean, gravity, 5-layer clamp, "
+                                  "alpha=0.2", "particles": n, "slots": slots, "reduction": "fast"},
+           "roofline": {"bound": "hbm", "kernel": "TL-SPH step (passes A-C + step-begin reduction)",
+                        "achieved": b_elastic / t_el / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": b_elastic / t_el / 1e9 / peak, "bytes_per_step": b_elastic, "peak_source": peak_src}}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        from oracle import oracle as O
+        out["cpu_baseline"] = cfg3_oracle_steps(min(os.cpu_count() or 1, O.openmp_threads()), 10)
+    return out
+
+
+def cfg3_oracle_steps(threads, steps):
+    """Reference CPU path (oracle port, OpenMP) over the first `steps` cfg3 loop steps."""
+    from oracle import oracle as O
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg3()
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+    o.set_material(S.E_MOD, S.NU, S.RHO0)
+    o.set("v", cfg["v0"])
+    o.set("body", cfg["body"])
+    o.prepare(threads=threads)
+    ro = o.run(eta=cfg["eta"], alpha=cfg["alpha"], steps=steps, seed=cfg["seed"], threads=threads)
+    n = len(cfg["r0"])
+    return {"value": n * ro["steps"] / ro["total_s"], "unit": "PS/s", "cores": threads, "kind": "port",
+            "sample": f"first {ro['steps']} cfg3 loop steps, oracle OpenMP"}
+
+
+def reference_particle_steps():
+    from oracle import oracle as O
+    threads = min(os.cpu_count() or 1, O.openmp_threads())
+    b = cfg3_oracle_steps(threads, 10)
+    return {"metric": "particle-steps/s (fp64 TL-SPH step + splitting damping, random choice)",
+            "value": b["value"], "unit": "PS/s", "impl": "reference", "cpu_baseline": b}
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the reference CPU path (oracle port; the reference itself cannot be built here)."""
     if rank != 0:
@@ -317,6 +374,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=["cfg2"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sampling")
+    ap.add_argument("--ps-steps", type=int, default=300, help="loop steps of the particle-steps/s leg (cfg3)")
+    ap.add_argument("--no-ps", action="store_true", help="skip the particle-steps/s leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     ws, rank, local = dist_env()
@@ -327,10 +386,14 @@ def main():
         dist.init_process_group("nccl")
     if args.impl == "reference":
         out = run_reference(args, ws, rank)
+        if out is not None and not args.no_ps:
+            out["particle_steps"] = reference_particle_steps()
     else:
         from paper_2103_08932_b200 import dev
         dev.select_device(local)
         out = run_cfg2(args, ws, rank)
+        if not args.no_ps:
+            out["particle_steps"] = particle_steps(args, ws, rank)
     if rank == 0 and out is not None:
         print(json.dumps(out))
     if ws > 1:
