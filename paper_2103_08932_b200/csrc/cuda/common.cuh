@@ -95,7 +95,8 @@ struct DFields {
   double* F[9];
   double* dFdt[9];
   double* B0[9];
-  double* PB[9];
+  // per particle, packed for the momentum gather: P(F) B0 row-major (D x D), V0, padding to 16 B
+  double* pbv;
   double* V0;
   double* m;
   double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
@@ -380,6 +381,10 @@ __device__ __forceinline__ M<D> second_pk(const M<D>& F, double J, const DMateri
     for (int k = 0; k < D; ++k) S.c[r][k] = mat.mu * ((r == k ? 1.0 : 0.0) - Ci.c[r][k]) + ll * Ci.c[r][k];
   return S;
 }
+
+// doubles per packed record of DFields::pbv
+template <int D>
+__host__ __device__ constexpr int pbv_stride() { return D == 3 ? 10 : 6; }
 
 template <int D>
 __device__ __forceinline__ M<D> load_mat(double* const* arr, long long i) {

@@ -180,9 +180,11 @@ __global__ void k_gather_init(DFields f, const double* __restrict__ r0aos, const
     f.F[k][s] = id;
     f.dFdt[k][s] = 0.0;
     f.B0[k][s] = id;
-    f.PB[k][s] = 0.0;
   }
   const double vol = V0h[i], dens = rho0h[i];
+#pragma unroll
+  for (int k = 0; k < pbv_stride<D>(); ++k) f.pbv[s * pbv_stride<D>() + k] = 0.0;
+  f.pbv[s * pbv_stride<D>() + D * D] = vol;
   f.V0[s] = vol;
   f.m[s] = dens * vol;  // particle_system.hpp:40
   f.rho0[s] = dens;
@@ -533,9 +535,9 @@ DFields DevSystem::fields() const {
     f.F[k] = F[k].p;
     f.dFdt[k] = dFdt[k].p;
     f.B0[k] = B0[k].p;
-    f.PB[k] = PB[k].p;
   }
   f.V0 = V0.p;
+  f.pbv = pbv.p;
   f.m = m.p;
   f.minvf = minvf.p;
   f.cell_slot = cell_slot.p;
@@ -579,8 +581,8 @@ void DevSystem::alloc_fields() {
     F[k].alloc(N);
     dFdt[k].alloc(N);
     B0[k].alloc(N);
-    PB[k].alloc(N);
   }
+  pbv.alloc(N * static_cast<size_t>(D == 3 ? pbv_stride<3>() : pbv_stride<2>()));
   V0.alloc(N);
   m.alloc(N);
   minvf.alloc(N);

@@ -50,6 +50,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "stencil_tile.cuh"
 #include "sweep_chain.cuh"
 #include "system.cuh"
 #include "tma.cuh"
@@ -78,9 +79,6 @@ struct Phase {
 
 template <int D>
 __host__ __device__ constexpr int colour_count() { return D == 2 ? 9 : 27; }
-template <int D>
-__host__ __device__ constexpr int seg_count() { return D == 2 ? 3 : 9; }
-
 // Shared-memory tile of one cell; every section is a multiple of 16 bytes.
 template <int D>
 struct Tile {
@@ -161,8 +159,6 @@ __device__ __forceinline__ double quot(double x, double d, double y) {
   return ORDERED ? div_by(x, d, y) : x * y;
 }
 
-constexpr unsigned kFull = 0xffffffffu;
-
 #ifdef TLSPH_SWEEP_TIMING
 // Debug build only: per cell task, slot 0 %globaltimer at start, slots 1-7
 // clock64 at the stages of k_sweep_fast, slot 8 the particle count.
@@ -213,30 +209,6 @@ __device__ __forceinline__ void phase_cell(const Phase& ph, long long k, int c[3
   c[2] = D == 3 ? ph.res[2] + 3 * static_cast<int>(k / (static_cast<long long>(ph.cnt[0]) * ph.cnt[1])) : 0;
 }
 
-// Lane q < 3^(D-1) of the staging warp: particle extent [sstart, send) of stencil row q of cell c.
-template <int D>
-__device__ __forceinline__ void locate_row(const DFields& f, const int c[3], int lane, long long& sstart,
-                                           long long& send) {
-  sstart = 0;
-  send = 0;
-  if (lane < seg_count<D>()) {
-    const int dy = (D == 2 ? lane : lane % 3) - 1;
-    const int dz = D == 2 ? 0 : lane / 3 - 1;
-    const int y = c[1] + dy;
-    const int z = c[2] + dz;
-    bool ok = y >= 0 && y < f.dims[1];
-    if (D == 3) ok = ok && z >= 0 && z < f.dims[2];
-    if (ok) {
-      const int xlo = c[0] > 0 ? c[0] - 1 : 0;
-      const int xhi = c[0] + 1 < f.dims[0] ? c[0] + 1 : f.dims[0] - 1;
-      const long long row = D == 3 ? (static_cast<long long>(z) * f.dims[1] + y) * f.dims[0]
-                                   : static_cast<long long>(y) * f.dims[0];
-      sstart = f.cell_start[row + xlo];
-      send = f.cell_start[row + xhi + 1];
-    }
-  }
-}
-
 // Aligned supersets of the cell's per-particle and per-slot ranges.
 struct CellSpan {
   long long p0, p1, s0, s1;
@@ -249,42 +221,6 @@ struct CellSpan {
   __device__ long long n0() const { return s0 & ~7ll; }  // u16 neighbour indices
   __device__ long long n1() const { return (s1 + 7) & ~7ll; }
 };
-
-// Stencil row table in registers: lane q < 3^(D-1) holds row q, as 16-byte
-// pairs (the tile keeps every row at the parity of its global position).
-struct RowPairs {
-  long long gp;  // global index of the row's first pair (element 2 gp)
-  int tp;        // tile index of the row's first pair
-  int npair;     // pairs staged for the row
-  int excl;      // exclusive prefix of npair over the rows
-  int total;     // pairs over all rows
-};
-
-__device__ __forceinline__ RowPairs row_pairs(long long sstart, int slen, int sbase, int lane) {
-  RowPairs r;
-  const int par = static_cast<int>(sstart & 1);
-  r.gp = (sstart - par) >> 1;
-  r.tp = (sbase - par) >> 1;
-  r.npair = slen > 0 ? (slen + par + 1) >> 1 : 0;
-  int incl = r.npair;
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const int x = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += x;
-  }
-  r.excl = incl - r.npair;
-  r.total = __shfl_sync(kFull, incl, 15);
-  return r;
-}
-
-// For pair p of the flattened row table: its row q and offset in the row.
-template <int D>
-__device__ __forceinline__ void locate_pair(const RowPairs& r, int p, int& q, int& off) {
-  q = 0;
-#pragma unroll
-  for (int k = 1; k < seg_count<D>(); ++k) q += p >= __shfl_sync(kFull, r.excl, k) ? 1 : 0;
-  off = p - __shfl_sync(kFull, r.excl, q);
-}
 
 // Executed by one whole warp: padded tile layout (exclusive scan of the
 // 16-byte aligned row lengths, as stencil_segments), segment table; the

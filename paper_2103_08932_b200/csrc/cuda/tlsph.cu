@@ -183,7 +183,13 @@ __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int 
     const M<D> S = second_pk<D>(F, J, mat);
     PB = matmul(matmul(F, S), load_mat<D>(f.B0, i));
   }
-  store_mat<D>(f.PB, i, PB);
+  // packed record for the momentum gather: P B0 row-major, then V0 (common.cuh)
+  double* rec = f.pbv + i * pbv_stride<D>();
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int q = 0; q < D; ++q) rec[r * D + q] = PB.c[r][q];
+  rec[D * D] = f.V0[i];
 }
 
 // ------------------------------------------------------------------ momentum RHS (integrator.cpp:105-115)
@@ -200,22 +206,39 @@ __global__ void k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
 #pragma unroll
   for (int d = 0; d < D; ++d) acc[d] = 0.0;
   if (active) {
-    double pbi[D * D];
+    constexpr int W = pbv_stride<D>();
+    double pbi[W];
+    {
+      const double2* ri = reinterpret_cast<const double2*>(f.pbv + i * W);
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) pbi[k] = f.PB[k][i];
-    const double V0i = f.V0[i];
+      for (int k = 0; k < W / 2; ++k) {
+        const double2 x = ri[k];
+        pbi[2 * k] = x.x;
+        pbi[2 * k + 1] = x.y;
+      }
+    }
+    const double V0i = pbi[D * D];
     const long long hi = f.offs[i + 1];
     for (long long s = f.offs[i] + l; s < hi; s += G) {
       const int j = f.nbr[s];
-      const double k = V0i * f.V0[j] * f.dwdr0[s];
+      // P B0 and V0 of j in W/2 16-byte loads from one packed record
+      double pbj[W];
+      const double2* rj = reinterpret_cast<const double2*>(f.pbv + static_cast<long long>(j) * W);
+#pragma unroll
+      for (int k = 0; k < W / 2; ++k) {
+        const double2 x = __ldg(rj + k);
+        pbj[2 * k] = x.x;
+        pbj[2 * k + 1] = x.y;
+      }
+      const double k = V0i * pbj[D * D] * f.dwdr0[s];
       double e[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) e[d] = f.e0[d][s];
 #pragma unroll
       for (int r = 0; r < D; ++r) {
-        double t = (k * (pbi[r * D] + f.PB[r * D][j])) * e[0];
+        double t = (k * (pbi[r * D] + pbj[r * D])) * e[0];
 #pragma unroll
-        for (int q = 1; q < D; ++q) t = t + (k * (pbi[r * D + q] + f.PB[r * D + q][j])) * e[q];
+        for (int q = 1; q < D; ++q) t = t + (k * (pbi[r * D + q] + pbj[r * D + q])) * e[q];
         acc[r] = acc[r] + t;
       }
     }
