@@ -510,17 +510,35 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
         }
         __syncwarp();
         if (lane == 0) {
+          // The chain carries only v_i. A row's j are distinct, so the operands of
+          // kPairBatch consecutive pairs are loaded before any of them is solved;
+          // the loads of a batch follow the previous batch's stores, and the reverse
+          // leg starts after the forward leg's last store.
+          constexpr int kPairBatch = 8;
           double vi = vd[li];
           for (int pass = 0; pass < 2; ++pass) {
-            for (int u = 0; u < cnt; ++u) {
-              const int s = pass == 0 ? u : cnt - 1 - u;
-              const int j = nlc[lo + s];
-              const double kf = kf_scr[s];
-              const double mj = t.sm[j];
-              const double vj = vd[j];
-              const double scaled = kf * (vi - vj);
-              vi = vi + mj * scaled;
-              if (t.smf[j] > 0.0) vd[j] = vj - mi * scaled;
+            for (int u0 = 0; u0 < cnt; u0 += kPairBatch) {
+              int jb[kPairBatch];
+              double kfb[kPairBatch], mjb[kPairBatch], vjb[kPairBatch];
+              bool upb[kPairBatch];
+#pragma unroll
+              for (int q = 0; q < kPairBatch; ++q) {
+                const int u = u0 + q < cnt ? u0 + q : cnt - 1;
+                const int s = pass == 0 ? u : cnt - 1 - u;
+                const int j = nlc[lo + s];
+                jb[q] = j;
+                kfb[q] = kf_scr[s];
+                mjb[q] = t.sm[j];
+                vjb[q] = vd[j];
+                upb[q] = t.smf[j] > 0.0;
+              }
+#pragma unroll
+              for (int q = 0; q < kPairBatch; ++q) {
+                if (u0 + q >= cnt) break;
+                const double scaled = kfb[q] * (vi - vjb[q]);
+                vi = vi + mjb[q] * scaled;
+                if (upb[q]) vd[jb[q]] = vjb[q] - mi * scaled;
+              }
             }
           }
           vd[li] = vi;
