@@ -262,9 +262,34 @@ def run_cfg2(args, ws, rank):
         threads = min(threads, O.openmp_threads())
         times, _ = cpu_sweep_sample(cfg, threads, budget_s=args.cpu_budget)
         t_cpu = statistics.median(times)
+        times1, _ = cpu_sweep_sample(cfg, 1, budget_s=min(args.cpu_budget, 5.0))
         out["cpu_baseline"] = {"value": dpu_per_sweep / t_cpu, "unit": "DPU/s", "cores": threads, "kind": "port",
-                               "sample": f"{len(times)} full cfg2 sweeps (median), oracle OpenMP over same-colour cells"}
+                               "sample": f"{len(times)} full cfg2 sweeps (median), oracle OpenMP over same-colour cells",
+                               "value_1_thread": dpu_per_sweep / statistics.median(times1),
+                               "sample_1_thread": f"{len(times1)} full cfg2 sweeps (median), 1 thread"}
+        if args.parity_sweeps > 0:
+            out["parity"] = cfg2_parity(cfg, d, args.parity_sweeps, threads)
     return out
+
+
+def cfg2_parity(cfg, d, sweeps, threads):
+    """BASELINE cfg2's check: velocity-variance decay over `sweeps` sweeps from v0, GPU (FAST) against
+    the oracle (reference arithmetic), plus the relative L2 distance of the final velocity fields."""
+    import numpy as np
+    from oracle import oracle as O
+    eta_t, dt = cfg["eta"] / cfg["alpha"], cfg["fixed_dt"]
+    d.set("v", cfg["v0"])
+    d.damping_sweep("particle_split", eta_t, dt, count=sweeps)
+    vg = d.get("v")
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+    o.set("v", cfg["v0"])
+    for _ in range(sweeps):
+        o.damping_sweep("particle_split", eta_t, dt, threads=threads)
+    vo = o.get("v")
+    var0 = float(np.var(cfg["v0"]))
+    return {"sweeps": sweeps, "var_v0": var0, "var_gpu": float(np.var(vg)), "var_oracle": float(np.var(vo)),
+            "rel_l2_v": float(np.linalg.norm(vg - vo) / np.linalg.norm(vo)), "tolerance": 1e-10,
+            "mode": "fast (warp-shuffle reductions) vs oracle"}
 
 
 def particle_steps(args, ws, rank):
@@ -376,6 +401,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sampling")
     ap.add_argument("--ps-steps", type=int, default=300, help="loop steps of the particle-steps/s leg (cfg3)")
     ap.add_argument("--no-ps", action="store_true", help="skip the particle-steps/s leg")
+    ap.add_argument("--parity-sweeps", type=int, default=500, help="cfg2 sweeps of the GPU-vs-oracle check (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     ws, rank, local = dist_env()
