@@ -70,7 +70,7 @@ struct Phase {
   int S;           // padded stencil tile length, multiple of 8
   int SC;          // max slots per cell, multiple of 8
   int MC;          // max particles per cell, even
-  int MR;          // pairwise scratch per warp (max slots per particle), 0 for particle split
+  int MR;          // per-warp scratch (max slots per particle): pairwise k, ORDERED residual terms
   int fast;        // FAST particle-split tile: no masses, per-slot mass factors instead
   double eta;
   double dt;       // used when dt_from_scalars == 0
@@ -435,11 +435,22 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 #pragma unroll
           for (int u = 0; u < KK; ++u) vq[u] = vd[jq[u]];
           if (ORDERED) {
+            // every lane forms its slots' terms b (v_i - v_j) exactly as the reference does;
+            // lane 0 folds them in slot order (damping.cpp:65-71) from the warp's scratch
+            double* const term = t.skf + static_cast<size_t>(warp) * ph.MR;
+#pragma unroll
+            for (int u = 0; u < KK; ++u)
+              if (lane + u * kWarp < cnt) term[lane + u * kWarp] = bq[u] * (vi - vq[u]);
+            __syncwarp();
             if (lane == 0) {
-              for (int s = lo; s < lo + cnt; ++s) {
-                const double b = eta * pfc[s] * dt_op;
-                R = R - b * (vi - vd[nlc[s]]);
+              int s = 0;
+#pragma unroll 4
+              for (; s + 1 < cnt; s += 2) {
+                const double2 tt = *reinterpret_cast<const double2*>(term + s);
+                R = R - tt.x;
+                R = R - tt.y;
               }
+              if (s < cnt) R = R - term[s];
             }
             R = __shfl_sync(kFull, R, 0);
           } else {
@@ -686,7 +697,10 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
   ph.S = (std::max(s.max_stencil, 1) + 7) & ~7;
   ph.SC = (std::max<int>(static_cast<int>(s.max_cell_slots), 1) + 7) & ~7;
   ph.MC = (std::max(s.max_cell, 1) + 1) & ~1;
-  ph.MR = scheme == TLSPH_SCHEME_PAIRWISE_SPLIT ? ((std::max(s.max_row, 1) + 1) & ~1) : 0;
+  // per-warp scratch of max_row doubles: pairwise k factors, ORDERED particle-split residual terms
+  ph.MR = (scheme == TLSPH_SCHEME_PAIRWISE_SPLIT || s.reduction == TLSPH_REDUCTION_ORDERED)
+              ? ((std::max(s.max_row, 1) + 1) & ~1)
+              : 0;
   // the single-warp FAST kernel (launch_particle_split) uses the mass-free tile
   ph.fast = scheme == TLSPH_SCHEME_PARTICLE_SPLIT && s.reduction != TLSPH_REDUCTION_ORDERED &&
             (std::max(s.max_row, 1) + kWarp - 1) / kWarp <= 4;
