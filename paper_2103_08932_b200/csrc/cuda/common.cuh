@@ -101,6 +101,8 @@ struct DFields {
   double* m;
   double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
   double* qf;     // per slot: pair_factor * RN(1/m_j), 0 for clamped j (FAST sweep)
+  double* pfsum;  // per particle: sum of its pair factors, and of their squares, in slot order
+  double* pfsq;   //   (FAST fold constants without a pass over the slots)
   long long* cell_slot;  // offs[cell_start[c]]: first CSR slot of cell c (ncells+1)
   // per-sweep particle-split constants (sweep.cu, k_sweep_folds)
   double* fdiag;  // sum_j b_ij - m_i

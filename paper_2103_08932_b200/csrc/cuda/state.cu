@@ -375,6 +375,19 @@ __global__ void k_qf(const double* __restrict__ pf, const int* __restrict__ nbr,
   qf[s] = y > 0.0 ? pf[s] * y : 0.0;
 }
 
+__global__ void k_pf_sums(DFields f) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  double a = 0.0, b = 0.0;
+  for (long long s = f.offs[i]; s < f.offs[i + 1]; ++s) {
+    const double p = f.pf[s];
+    a = a + p;
+    b = b + p * p;
+  }
+  f.pfsum[i] = a;
+  f.pfsq[i] = b;
+}
+
 __global__ void k_cell_slot(const long long* __restrict__ cell_start, const long long* __restrict__ offs,
                             long long ncells, long long* __restrict__ out) {
   const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -555,6 +568,8 @@ DFields DevSystem::fields() const {
   f.dwdr0 = dwdr0.p;
   f.pf = pf.p;
   f.qf = qf.p;
+  f.pfsum = pf_sum.p;
+  f.pfsq = pf_sq.p;
   f.nloc = nloc.p;
   f.cell_start = cell_start.p;
   f.cell = cutoff;
@@ -763,6 +778,10 @@ void DevSystem::refresh_minvf() {
 
 void DevSystem::compute_sweep_stats() {
   refresh_minvf();
+  pf_sum.alloc(static_cast<size_t>(n));
+  pf_sq.alloc(static_cast<size_t>(n));
+  k_pf_sums<<<grid_for(n, 256), 256, 0, stream>>>(fields());
+  CK_LAUNCH("k_pf_sums");
   cell_slot.alloc(static_cast<size_t>(ncells + 1));
   k_cell_slot<<<grid_for(ncells + 1, 256), 256, 0, stream>>>(cell_start.p, offs.p, ncells, cell_slot.p);
   CK_LAUNCH("k_cell_slot");

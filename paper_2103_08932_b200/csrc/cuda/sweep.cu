@@ -179,6 +179,10 @@ __device__ __forceinline__ void stamp(long long, int) {}
 // ------------------------------------------------------------------ per-sweep folds
 // damping.cpp:65-74: sum_b, sum_b2 in slot order, diag, denominator (its
 // reciprocal feeds the corrected division on the chain).
+// ORDERED: the reference's slot-order folds of b = eta G dt/2. FAST: from the
+// static per-particle sums of G and G^2 (sum b = kb sum G, sum b^2 = kb^2 sum G^2,
+// kb = eta dt/2; reassociation, FAST tolerance class), one read per particle.
+template <bool ORDERED>
 __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_from_scalars,
                               const DScalars* __restrict__ sc) {
   if (dt_from_scalars && sc->halt) return;
@@ -186,11 +190,17 @@ __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_fro
   if (i >= f.n) return;
   const double dt_half = 0.5 * (dt_from_scalars ? sc->dt : dt_fixed);
   double sb = 0.0, sb2 = 0.0;
-  const long long hi = f.offs[i + 1];
-  for (long long s = f.offs[i]; s < hi; ++s) {
-    const double b = eta * f.pf[s] * dt_half;
-    sb = sb + b;
-    sb2 = sb2 + b * b;
+  if (ORDERED) {
+    const long long hi = f.offs[i + 1];
+    for (long long s = f.offs[i]; s < hi; ++s) {
+      const double b = eta * f.pf[s] * dt_half;
+      sb = sb + b;
+      sb2 = sb2 + b * b;
+    }
+  } else {
+    const double kb = eta * dt_half;
+    sb = kb * f.pfsum[i];
+    sb2 = (kb * kb) * f.pfsq[i];
   }
   const double diag = sb - f.m[i];
   const double den = diag * diag + sb2;
@@ -711,13 +721,18 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
                        " bytes) exceed the shared-memory tile");
   if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
     // per-sweep fold constants; reused while (eta, dt) are unchanged
-    if (from_scal || !s.fold_valid || s.fold_eta != eta || s.fold_dt != dt) {
-      k_sweep_folds<<<static_cast<unsigned>((s.n + 127) / 128), 128, 0, s.stream>>>(f, eta, dt, from_scal ? 1 : 0,
-                                                                                    s.scal.p);
+    const int mode = static_cast<int>(s.reduction);
+    if (from_scal || !s.fold_valid || s.fold_eta != eta || s.fold_dt != dt || s.fold_mode != mode) {
+      const unsigned grid = static_cast<unsigned>((s.n + 127) / 128);
+      if (s.reduction == TLSPH_REDUCTION_ORDERED)
+        k_sweep_folds<true><<<grid, 128, 0, s.stream>>>(f, eta, dt, from_scal ? 1 : 0, s.scal.p);
+      else
+        k_sweep_folds<false><<<grid, 128, 0, s.stream>>>(f, eta, dt, from_scal ? 1 : 0, s.scal.p);
       CK_LAUNCH("k_sweep_folds");
       s.fold_valid = !from_scal;
       s.fold_eta = eta;
       s.fold_dt = dt;
+      s.fold_mode = mode;
     }
   }
   return ph;

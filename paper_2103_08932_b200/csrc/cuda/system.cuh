@@ -79,6 +79,7 @@ class DevSystem {
   DBuf<double> fold_diag, fold_den, fold_y;
   bool fold_valid = false;
   double fold_eta = 0.0, fold_dt = 0.0;
+  int fold_mode = -1;  // reduction mode the fold constants were formed in
   DBuf<uint8_t> flag;
   DBuf<int> perm, rank;
   DBuf<long long> cell_start;
@@ -98,6 +99,7 @@ class DevSystem {
   DBuf<int> nbr;
   DBuf<double> r0_len, e0[3], dwdr0, pf;
   DBuf<double> qf;  // pf * RN(1/m_j), 0 for clamped j: the FAST sweep's per-slot mass factor
+  DBuf<double> pf_sum, pf_sq;  // per-particle sums of pf and pf^2 (static)
   DBuf<uint16_t> nloc;
 
   // scratch
