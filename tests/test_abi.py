@@ -55,6 +55,13 @@ def test_c_abi_host_paths_without_gpu():
     args = (C.c_char_p * 2)(b"case=bending_cantilever", b"nonsense_key=1")
     assert L.tlsph_sim_create(None, args, 2, C.byref(sim)) == 2
     assert b"nonsense_key" in L.tlsph_last_error()
+    # this build's extra key: GPU reduction mode
+    args = (C.c_char_p * 2)(b"case=bending_cantilever", b"gpu.reduction=sideways")
+    assert L.tlsph_sim_create(None, args, 2, C.byref(sim)) == 2
+    assert b"gpu.reduction" in L.tlsph_last_error()
+    args = (C.c_char_p * 2)(b"case=bending_cantilever", b"gpu.reduction=ordered")
+    assert L.tlsph_sim_create(None, args, 2, C.byref(sim)) == 0
+    L.tlsph_sim_destroy(sim)
     args = (C.c_char_p * 3)(b"case=bending_cantilever", b"resolution=6", b"threads=4")
     assert L.tlsph_sim_create(None, args, 3, C.byref(sim)) == 0
     assert L.tlsph_sim_dim(sim) == 3 and L.tlsph_sim_thread_count(sim) == 4
