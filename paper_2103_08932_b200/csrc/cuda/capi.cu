@@ -159,6 +159,7 @@ tlsph_status tlsph_dev_set_task_range(tlsph_dev* dev, int x0, int x1) {
       throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "task range must satisfy 0 <= x0 < x1 <= dims[0]");
     s.task_x0 = x0;
     s.task_x1 = x1;
+    s.build_colour_lists();
   });
 }
 

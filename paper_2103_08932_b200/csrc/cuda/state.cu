@@ -796,6 +796,7 @@ void DevSystem::compute_sweep_stats() {
   sync();
   max_cell_slots = static_cast<long long>(h[0]);
   max_row = static_cast<int>(h[1]);
+  build_colour_lists();
 }
 
 void DevSystem::load_csr(const int64_t* offsets, const int32_t* neighbor, const double* r0_len_h, const double* e0_h,

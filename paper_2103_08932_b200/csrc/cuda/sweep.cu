@@ -62,10 +62,8 @@ namespace {
 constexpr int kThreads = 128;  // one CTA per cell
 
 struct Phase {
-  int res[3];      // colour residues per axis
-  int cnt[3];      // cells of this colour per axis (x: inside the task range)
-  int xfirst;      // first task cell x of this colour
-  long long ncol;  // cells in the colour
+  const int* cells;  // this colour's task cells (linear index), fuller first; blockIdx -> cell
+  long long ncol;    // cells in the colour
   int forward;
   int S;           // padded stencil tile length, multiple of 8
   int SC;          // max slots per cell, multiple of 8
@@ -213,10 +211,12 @@ __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_fro
 
 // ------------------------------------------------------------------ staging (step 1)
 template <int D>
-__device__ __forceinline__ void phase_cell(const Phase& ph, long long k, int c[3]) {
-  c[0] = ph.xfirst + 3 * static_cast<int>(k % ph.cnt[0]);
-  c[1] = ph.res[1] + 3 * static_cast<int>((k / ph.cnt[0]) % ph.cnt[1]);
-  c[2] = D == 3 ? ph.res[2] + 3 * static_cast<int>(k / (static_cast<long long>(ph.cnt[0]) * ph.cnt[1])) : 0;
+__device__ __forceinline__ long long phase_cell(const Phase& ph, const DFields& f, long long k, int c[3]) {
+  const long long lin = ph.cells[k];
+  c[0] = static_cast<int>(lin % f.dims[0]);
+  c[1] = static_cast<int>((lin / f.dims[0]) % f.dims[1]);
+  c[2] = D == 3 ? static_cast<int>(lin / (static_cast<long long>(f.dims[0]) * f.dims[1])) : 0;
+  return lin;
 }
 
 // Aligned supersets of the cell's per-particle and per-slot ranges.
@@ -363,7 +363,7 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   const int warp = tid / kWarp, lane = tid % kWarp;
   const long long k = blockIdx.x;
   int c[3];
-  phase_cell<D>(ph, k, c);
+  const long long lin = phase_cell<D>(ph, f, k, c);
   constexpr int kSegs = seg_count<D>();
   Tile<D> t = carve<D>(smem, ph);
   const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
@@ -372,7 +372,6 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   const double eta = ph.eta;
 
   // ---- 1. staging. All index loads are issued before any of them is used.
-  const long long lin = cell_linear<D>(c, f.dims);
   CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
   long long sstart = 0, send = 0;
   if (warp == 0) locate_row<D>(f, c, lane, sstart, send);
@@ -595,12 +594,11 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   stamp(blockIdx.x, 1);
   grid_launch_dependents();  // the next phase may stage its static data while this one runs
   int c[3];
-  phase_cell<D>(ph, blockIdx.x, c);
+  const long long lin = phase_cell<D>(ph, f, blockIdx.x, c);
   Tile<D> t = carve<D>(smem, ph);
   const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
   const double kb = ph.eta * (0.5 * dt);  // b = kb * pair_factor
 
-  const long long lin = cell_linear<D>(c, f.dims);
   const CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
   long long sstart, send;
   locate_row<D>(f, c, lane, sstart, send);
@@ -699,6 +697,7 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
   if (!s.stencil_ok)
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "damping sweep needs every neighbour inside the 3^D cell stencil (neighbors.hpp:50-52)");
+  if (s.colour_start.empty()) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "damping sweep needs a neighbourhood");
   const DFields f = s.fields();
   Phase ph{};
   ph.eta = eta;
@@ -746,27 +745,9 @@ void enqueue_phase(DevSystem& s, int scheme, Phase ph, int pass, int index) {
   constexpr int nb = colour_count<D>();
   const int b = pass == 0 ? index : nb - 1 - index;
   ph.forward = pass == 0;
-  int rem = b;
-  long long total = 1;
-  const int x0 = s.task_x0, x1 = s.task_x1 < 0 ? s.dims[0] : std::min(s.task_x1, s.dims[0]);
-  for (int d = 0; d < 3; ++d) {
-    if (d < D) {
-      ph.res[d] = rem % 3;
-      rem /= 3;
-      if (d == 0) {
-        ph.xfirst = x0 + ((ph.res[0] - x0 % 3) + 3) % 3;
-        ph.cnt[0] = x1 > ph.xfirst ? (x1 - ph.xfirst + 2) / 3 : 0;
-      } else {
-        ph.cnt[d] = s.dims[d] > ph.res[d] ? (s.dims[d] - ph.res[d] + 2) / 3 : 0;
-      }
-    } else {
-      ph.res[d] = 0;
-      ph.cnt[d] = 1;
-    }
-    total *= ph.cnt[d];
-  }
-  ph.ncol = total;
-  if (total == 0) return;  // empty colour (neighbors.cpp:152)
+  ph.cells = s.colour_cells.p + s.colour_start[b];
+  ph.ncol = s.colour_start[b + 1] - s.colour_start[b];
+  if (ph.ncol == 0) return;  // empty colour (neighbors.cpp:152)
   const DFields f = s.fields();
   if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
     if (s.reduction == TLSPH_REDUCTION_ORDERED) launch_particle_split<D, true>(s, f, ph);
@@ -832,6 +813,37 @@ __global__ void k_selftest_division(unsigned long long seed, long long n, unsign
 void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars) {
   if (D == 2) enqueue_sweep_d<2>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
   else enqueue_sweep_d<3>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
+}
+
+void DevSystem::build_colour_lists() {
+  std::vector<long long> cst(static_cast<size_t>(ncells + 1));
+  CK(cudaMemcpyAsync(cst.data(), cell_start.p, cst.size() * sizeof(long long), cudaMemcpyDeviceToHost, stream));
+  sync();
+  const int x0 = task_x0, x1 = task_x1 < 0 ? dims[0] : std::min(task_x1, dims[0]);
+  const int nb = D == 2 ? 9 : 27;
+  std::vector<int> cells;
+  colour_start.assign(static_cast<size_t>(nb + 1), 0);
+  std::vector<std::pair<long long, int>> col;  // (-count, cell)
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = b % 3, r1 = (b / 3) % 3, r2 = D == 3 ? b / 9 : 0;
+    col.clear();
+    for (int z = r2; z < (D == 3 ? dims[2] : 1); z += 3)
+      for (int y = r1; y < dims[1]; y += 3)
+        for (int x = r0; x < dims[0]; x += 3) {
+          if (x < x0 || x >= x1) continue;
+          const long long lin = (static_cast<long long>(z) * dims[1] + y) * dims[0] + x;
+          const long long cnt = cst[lin + 1] - cst[lin];
+          if (cnt > 0) col.emplace_back(-cnt, static_cast<int>(lin));
+        }
+    std::stable_sort(col.begin(), col.end());
+    colour_start[b] = static_cast<long long>(cells.size());
+    for (const auto& c : col) cells.push_back(c.second);
+  }
+  colour_start[nb] = static_cast<long long>(cells.size());
+  colour_cells.alloc(std::max<size_t>(cells.size(), 1));
+  if (!cells.empty())
+    CK(cudaMemcpyAsync(colour_cells.p, cells.data(), cells.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+  sync();
 }
 
 void DevSystem::enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index) {

@@ -68,6 +68,10 @@ class DevSystem {
   int given_dims[3] = {1, 1, 1};
   int task_x0 = 0, task_x1 = -1;  // -1: dims[0]
   std::vector<long long> cell_start_h;  // host copy, for column packing
+  // per colour: the non-empty task cells (x in the task range), fuller cells first, so a
+  // phase's longest chains get the first SM slots; colour b's list starts at colour_start[b]
+  DBuf<int> colour_cells;
+  std::vector<long long> colour_start;
 
   // fields (sorted order)
   DBuf<double> r0[3], r[3], v[3], a[3], body[3];
@@ -153,6 +157,7 @@ class DevSystem {
   void enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars);
   // one colour phase (pass 0 forward / 1 reverse, index-th colour of the pass)
   void enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index);
+  void build_colour_lists();  // host sync: at construction and when the task range changes
   // x-slab halo columns (sweep.cu)
   long long column_count(int x) const;
   void pack_column(int x, double* dev_dst);
