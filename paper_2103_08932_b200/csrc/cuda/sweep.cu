@@ -288,20 +288,49 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
     tma_load_1d(t.sqf, f.qf + cs.f0(), mybytes, t.bar);
   }
   stamp(blockIdx.x, 3);
-  // PDL: everything above is static; the velocities are written by the preceding phase
-  if (PDL) grid_dependency_wait();
   const RowPairs rp = row_pairs(sstart, lane < kSegs ? slen : 0, sbase, lane);
-  for (int base = 0; base < rp.total; base += kWarp) {
-    const int p = base + lane;
-    int q, off;
-    locate_pair<D>(rp, p, q, off);
-    const long long g = 2 * (__shfl_sync(kFull, rp.gp, q) + off);
-    const int tt = 2 * (__shfl_sync(kFull, rp.tp, q) + off);
-    if (p < rp.total) {
+  auto copy_pair = [&](long long g, int tt) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) cp_async16(t.sv[d] + tt, f.v[d] + g);
-      if (!QF) cp_async16(t.smf + tt, f.minvf + g);
-      if (MASS) cp_async16(t.sm + tt, f.m + g);
+    for (int d = 0; d < D; ++d) cp_async16(t.sv[d] + tt, f.v[d] + g);
+    if (!QF) cp_async16(t.smf + tt, f.minvf + g);
+    if (MASS) cp_async16(t.sm + tt, f.m + g);
+  };
+  // The copy addresses are static: with PDL they are formed before waiting for
+  // the preceding phase (stencils of up to kPreIter x 32 pairs), so only the
+  // copies themselves follow the wait.
+  constexpr int kPreIter = 16;
+  if (PDL && rp.total <= kPreIter * kWarp) {
+    long long gp[kPreIter];
+    int tp[kPreIter];
+#pragma unroll
+    for (int it = 0; it < kPreIter; ++it) {
+      gp[it] = -1;
+      tp[it] = 0;
+      if (it * kWarp < rp.total) {  // warp-uniform
+        const int p = it * kWarp + lane;
+        int q, off;
+        locate_pair<D>(rp, p, q, off);
+        const long long g = 2 * (__shfl_sync(kFull, rp.gp, q) + off);
+        const int tt = 2 * (__shfl_sync(kFull, rp.tp, q) + off);
+        if (p < rp.total) {
+          gp[it] = g;
+          tp[it] = tt;
+        }
+      }
+    }
+    grid_dependency_wait();  // the velocities are written by the preceding phase
+#pragma unroll
+    for (int it = 0; it < kPreIter; ++it)
+      if (gp[it] >= 0) copy_pair(gp[it], tp[it]);
+  } else {
+    if (PDL) grid_dependency_wait();
+    for (int base = 0; base < rp.total; base += kWarp) {
+      const int p = base + lane;
+      int q, off;
+      locate_pair<D>(rp, p, q, off);
+      const long long g = 2 * (__shfl_sync(kFull, rp.gp, q) + off);
+      const int tt = 2 * (__shfl_sync(kFull, rp.tp, q) + off);
+      if (p < rp.total) copy_pair(g, tt);
     }
   }
   constexpr int center = D == 2 ? 1 : 4;
