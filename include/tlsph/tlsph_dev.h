@@ -124,6 +124,12 @@ tlsph_status tlsph_dev_damping_phase(tlsph_dev* dev, tlsph_dev_scheme scheme, do
  * x, component-major (D x count doubles), in (z, y, in-cell) order, which is
  * the same on every slab that holds the column. Device buffers; synchronous.
  * tlsph_dev_column_count returns -1 on error. */
+/* Fused exchange: after this call the sweep phases of `dev` also store the new
+ * velocities of the columns it shares with `peer` (side 0: the slab to its
+ * left, 1: to its right) directly into `peer`'s arrays (peer access over
+ * NVLink when the slabs live on different GPUs), so no pack/unpack is needed;
+ * the caller only orders the phases of all slabs (a barrier per phase). */
+tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer);
 int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x);
 tlsph_status tlsph_dev_pack_column(tlsph_dev* dev, int x, double* device_dst);
 tlsph_status tlsph_dev_unpack_column(tlsph_dev* dev, int x, const double* device_src);

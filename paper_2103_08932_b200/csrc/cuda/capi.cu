@@ -175,6 +175,24 @@ tlsph_status tlsph_dev_damping_phase(tlsph_dev* dev, tlsph_dev_scheme scheme, do
   });
 }
 
+tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer) {
+  return guarded([&] {
+    if (!peer) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer must not be null");
+    DevSystem& s = sys(dev);
+    DevSystem& p = sys(peer);
+    if (s.device != p.device) {  // NVLink peer access for the fused stores
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, s.device, p.device));
+      if (!ok) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer device is not reachable by peer access");
+      CK(cudaSetDevice(s.device));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(p.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+      cudaGetLastError();
+    }
+    s.link_peer(side, p);
+  });
+}
+
 int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x) {
   int64_t c = -1;
   const tlsph_status st = guarded([&] { c = sys(dev).column_count(x); });

@@ -101,6 +101,12 @@ struct DFields {
   double* m;
   double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
   double* qf;     // per slot: pair_factor * RN(1/m_j), 0 for clamped j (FAST sweep)
+  // x-slab peers (slabs.py): per particle of a column shared with a neighbouring slab, the
+  // particle's index in that slab's arrays (-1: not shared; >= 0: right peer; <= -2: left
+  // peer at -2 - index); the peers' velocity arrays (device memory reachable from here)
+  int* peer_idx;
+  double* peer_v[2][3];
+  int peer_x[2];  // the columns adjoining each peer (left: x0, right: x1 - 1), -1 if none
   double* pfsum;  // per particle: sum of its pair factors, and of their squares, in slot order
   double* pfsq;   //   (FAST fold constants without a pass over the slots)
   long long* cell_slot;  // offs[cell_start[c]]: first CSR slot of cell c (ncells+1)

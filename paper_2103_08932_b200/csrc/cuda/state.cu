@@ -569,6 +569,11 @@ DFields DevSystem::fields() const {
   f.pf = pf.p;
   f.qf = qf.p;
   f.pfsum = pf_sum.p;
+  f.peer_idx = peer_idx.p;
+  for (int k = 0; k < 2; ++k) {
+    f.peer_x[k] = peer_x[k];
+    for (int d = 0; d < 3; ++d) f.peer_v[k][d] = peer_v[k][d];
+  }
   f.pfsq = pf_sq.p;
   f.nloc = nloc.p;
   f.cell_start = cell_start.p;

@@ -381,6 +381,33 @@ __device__ __forceinline__ void writeback_rows(const DFields& f, const Tile<D>& 
   }
 }
 
+// Fused halo exchange of a slab: a cell task whose stencil
+// reaches a column shared with a neighbouring slab also stores those particles'
+// new velocities straight into the peer's arrays (over NVLink when the peer is
+// another GPU). Same-phase stencils are disjoint, so the peer does not write
+// these particles in this phase and reads them only after the phase barrier.
+template <int D>
+__device__ __forceinline__ void writeback_peers(const DFields& f, const Tile<D>& t, const int c[3], int tid,
+                                                int nthreads) {
+  if (!f.peer_idx) return;
+  const bool near = (f.peer_x[0] >= 0 && c[0] - 1 <= f.peer_x[0] + 1) ||
+                    (f.peer_x[1] >= 0 && c[0] + 1 >= f.peer_x[1] - 1);  // uniform per cell
+  if (!near) return;
+  constexpr int kSegs = seg_count<D>();
+  for (int q = 0; q < kSegs; ++q) {
+    const long long g0 = t.seg_start[q];
+    const int b = t.seg_base[q], len = t.seg_len[q];
+    for (int e = tid; e < len; e += nthreads) {
+      const int pi = f.peer_idx[g0 + e];
+      if (pi == -1) continue;
+      const int side = pi >= 0 ? 1 : 0;
+      const int idx = pi >= 0 ? pi : -2 - pi;
+#pragma unroll
+      for (int d = 0; d < D; ++d) f.peer_v[side][d][idx] = t.sv[d][b + e];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ colour phase
 // K > 0: rows up to 32 K slots run the branch-free register path; K = 0: generic loop only.
 template <int D, int SCHEME, bool ORDERED, int K>
@@ -607,6 +634,7 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
       for (int d = 0; d < D; ++d) f.v[d][g0 + e] = t.sv[d][b + e];
     }
   }
+  writeback_peers<D>(f, t, c, tid, kThreads);
 }
 
 // ------------------------------------------------------------------ FAST particle split, one warp per cell
@@ -656,6 +684,7 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   __syncwarp();
   stamp(blockIdx.x, 6);
 
+  writeback_peers<D>(f, t, c, lane, kWarp);
   writeback_rows<D>(f, t, lane);
   stamp(blockIdx.x, 7);
 #ifdef TLSPH_SWEEP_TIMING
@@ -842,6 +871,37 @@ __global__ void k_selftest_division(unsigned long long seed, long long n, unsign
 void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars) {
   if (D == 2) enqueue_sweep_d<2>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
   else enqueue_sweep_d<3>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
+}
+
+// Peer indices for the columns this slab shares with `peer` on `side` (0: left,
+// 1: right): both hold the columns' particles, binned in the same global cells
+// with the same in-cell order, so the k-th particle of a cell maps to the k-th.
+void DevSystem::link_peer(int side, DevSystem& peer) {
+  if (side != 0 && side != 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer side must be 0 (left) or 1 (right)");
+  if (!grid_given || !peer.grid_given || peer.D != D || peer.ncells != ncells)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peers must be slabs of the same global grid");
+  const int x0 = task_x0, x1 = task_x1 < 0 ? dims[0] : task_x1;
+  // shared columns: left x0-1 (peer owns) and x0 (we own); right x1-1 (we own) and x1 (peer owns)
+  const int ca = side == 0 ? x0 - 1 : x1 - 1, cb = ca + 1;
+  if (ca < 0 || cb >= dims[0]) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "no neighbouring slab on that side");
+  std::vector<int> idx(static_cast<size_t>(n), -1);
+  if (peer_idx.p) CK(cudaMemcpy(idx.data(), peer_idx.p, idx.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  const int nq = static_cast<int>(ncells / dims[0]);
+  for (int x : {ca, cb})
+    for (int q = 0; q < nq; ++q) {
+      const long long lin = static_cast<long long>(q) * dims[0] + x;
+      const long long a0 = cell_start_h[lin], a1 = cell_start_h[lin + 1];
+      const long long b0 = peer.cell_start_h[lin], b1 = peer.cell_start_h[lin + 1];
+      if (a1 - a0 != b1 - b0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer slabs disagree on a shared cell");
+      for (long long k = 0; k < a1 - a0; ++k) {
+        const long long j = b0 + k;
+        idx[static_cast<size_t>(a0 + k)] = side == 1 ? static_cast<int>(j) : -2 - static_cast<int>(j);
+      }
+    }
+  peer_idx.alloc(idx.size());
+  CK(cudaMemcpy(peer_idx.p, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice));
+  for (int d = 0; d < 3; ++d) peer_v[side][d] = d < D ? peer.v[d].p : nullptr;
+  peer_x[side] = side == 0 ? x0 : x1 - 1;
 }
 
 void DevSystem::build_colour_lists() {

@@ -70,6 +70,10 @@ class DevSystem {
   std::vector<long long> cell_start_h;  // host copy, for column packing
   // per colour: the non-empty task cells (x in the task range), fuller cells first, so a
   // phase's longest chains get the first SM slots; colour b's list starts at colour_start[b]
+  // fused halo exchange with neighbouring slabs (tlsph_dev_link_peer)
+  DBuf<int> peer_idx;
+  double* peer_v[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  int peer_x[2] = {-1, -1};
   DBuf<int> colour_cells;
   std::vector<long long> colour_start;
 
@@ -158,6 +162,7 @@ class DevSystem {
   // one colour phase (pass 0 forward / 1 reverse, index-th colour of the pass)
   void enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index);
   void build_colour_lists();  // host sync: at construction and when the task range changes
+  void link_peer(int side, DevSystem& peer);  // sweep.cu
   // x-slab halo columns (sweep.cu)
   long long column_count(int x) const;
   void pack_column(int x, double* dev_dst);

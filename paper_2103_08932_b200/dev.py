@@ -106,6 +106,7 @@ def lib():
                                            C.POINTER(P)]
     L.tlsph_dev_set_task_range.argtypes = [P, I, I]
     L.tlsph_dev_damping_phase.argtypes = [P, I, C.c_double, C.c_double, I, I]
+    L.tlsph_dev_link_peer.argtypes = [P, I, P]
     L.tlsph_dev_column_count.argtypes = [P, I]
     L.tlsph_dev_column_count.restype = C.c_int64
     L.tlsph_dev_pack_column.argtypes = [P, I, C.c_void_p]
@@ -348,6 +349,10 @@ class DeviceSystem:
     def damping_phase(self, scheme, eta_tilde, dt, pass_, index):
         _check(lib().tlsph_dev_damping_phase(self._h, SCHEMES[scheme], float(eta_tilde), float(dt), int(pass_),
                                              int(index)))
+
+    def link_peer(self, side, peer):
+        """Fused exchange: this slab's phases also store the shared columns into `peer` (0 left, 1 right)."""
+        _check(lib().tlsph_dev_link_peer(self._h, int(side), peer._h))
 
     def column_count(self, x):
         c = int(lib().tlsph_dev_column_count(self._h, int(x)))

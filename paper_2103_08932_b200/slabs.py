@@ -16,6 +16,10 @@ columns are therefore written every phase, each by one side, and the writer send
 whole column to the other side after the phase (``phase_transfers``). Slabs are at least
 two columns wide so a rank's tasks never reach past its neighbour's halo.
 
+The fused form (``link_peers`` / ``sweep_fused``): each slab's phase kernels store the shared
+columns straight into the neighbouring slab's arrays (NVLink peer access between GPUs), so the
+only inter-slab operation left is the per-phase ordering.
+
 The driver is independent of the engine and the transport: an engine runs a slab's colour
 phases and packs/unpacks halo columns (``DeviceSlabEngine`` over a ``DeviceSystem``);
 ``SlabSweep`` exchanges the columns through ``torch.distributed`` (NCCL between GPUs, gloo
@@ -191,6 +195,24 @@ def sweep_in_process(engines, ranges, scheme, eta_tilde, dt, dim):
             e.phase(scheme, eta_tilde, dt, p, index)
         for t in phase_transfers(ranges, rx):
             engines[t.dst].unpack(t.column, engines[t.src].pack(t.column))
+
+
+def link_peers(systems):
+    """Fused form of the exchange: each slab's phase kernels store the columns it shares with its
+    x-neighbours straight into their arrays (tlsph_dev_link_peer; NVLink peer access across GPUs)."""
+    for r in range(len(systems) - 1):
+        systems[r].link_peer(1, systems[r + 1])
+        systems[r + 1].link_peer(0, systems[r])
+
+
+def sweep_fused(systems, scheme, eta_tilde, dt, dim):
+    """One strang_damping_sweep over peer-linked slabs held by this process (one per GPU or all on
+    one): the phases of all slabs, then the next phase; the exchange happens inside the kernels."""
+    if eta_tilde == 0.0:
+        return
+    for p, index, _ in colour_schedule(dim):
+        for d in systems:  # each call returns after its kernel: the phase barrier
+            d.damping_phase(scheme, eta_tilde, dt, p, index)
 
 
 class SlabSweep:

@@ -244,6 +244,36 @@ def test_device_slabs_equal_undivided_device(dim, world, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("dim,world,mode", [(2, 3, "ordered"), (3, 2, "fast"), (3, 3, "ordered"),
+                                            (3, 3, "fast")])
+def test_fused_peer_slabs_equal_undivided_device(dim, world, mode):
+    """Fused exchange: phase kernels store shared columns into the neighbouring slab directly."""
+    from paper_2103_08932_b200 import dev
+
+    r0, cons, v = body(dim, [40, 9] if dim == 2 else [24, 6, 5])
+    whole = dev.DeviceSystem(r0, DP ** dim, RHO, H, cons)
+    whole.set_reduction(mode)
+    whole.set("v", v)
+    grid, parts = slabs.decompose(r0, H, world)
+    systems = [slabs.make_device_slab(grid, s, r0, DP ** dim, RHO, H, cons) for s in parts]
+    for s, d in zip(parts, systems):
+        d.set_reduction(mode)
+        d.set("v", v[s.ids])
+    slabs.link_peers(systems)
+    for _ in range(3):
+        whole.damping_sweep("particle_split", 160.0, 1e-4)
+        slabs.sweep_fused(systems, "particle_split", 160.0, 1e-4, dim)
+    ref = whole.get("v")
+    cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
+    for s, d in zip(parts, systems):
+        vv = d.get("v")
+        own = (cols[s.ids] >= s.x0) & (cols[s.ids] < s.x1)
+        assert np.array_equal(vv[own], ref[s.ids[own]])
+        # halo columns hold the neighbours' current values too
+        assert np.array_equal(vv, ref[s.ids])
+
+
+@pytest.mark.gpu
 def test_device_phases_compose_to_sweep():
     from paper_2103_08932_b200 import dev
 
