@@ -753,7 +753,7 @@ void DevSystem::build_neighbourhoods() {
   dwdr0.alloc(S);
   pf.alloc(S);
   nloc.alloc(S);
-  stencil_ok = max_stencil < 0x8000;  // bit 15 of a staged index carries the clamp flag
+  stencil_ok = max_stencil < 0x8000;  // staged stencil positions fit the u16 nloc
   f = fields();
   const int cap = std::max(max_stencil, 1);
   const int warps = 4;

@@ -4,40 +4,38 @@
 // pairwise_split_update, strang_damping_sweep), neighbors.cpp:143-174
 // (block_sweep), neighbors.cpp:61-77 (3^D residue colouring).
 //
-// Per sweep: k_sweep_folds forms, for every particle, the reference-order
-// folds sum b and sum b^2 (b = eta G dt/2), diag = sum b - m_i,
-// denom = diag^2 + sum b^2 and RN(1/denom). They do not depend on the
-// velocities, so they are computed once, fully parallel, and reused by all
-// 2 x 3^D colour phases (and by later sweeps with the same eta and dt).
+// Per sweep: k_sweep_folds forms, for every particle, sum b and sum b^2
+// (b = eta G dt/2), diag = sum b - m_i, denom = diag^2 + sum b^2 and
+// RN(1/denom) -- in slot order (ORDERED) or from static per-particle sums of G
+// and G^2 (FAST). They do not depend on the velocities, so they are computed
+// once, fully parallel, and reused by all 2 x 3^D colour phases (and by later
+// sweeps with the same eta, dt and mode). A constrained particle gets a NaN
+// diagonal (never updated as i, damping.cpp:151).
 //
-// Per colour phase, one launch. Colour b holds the cells whose coordinates
-// are congruent to b's residues mod 3 on every axis; their 3^D stencils are
-// disjoint (neighbors.hpp:50-52), so every cell is an independent task and
-// one 128-thread CTA owns one cell:
-//   1. staging by TMA: lanes of warp 0 locate the 3^(D-1) x-rows of the
-//      cell's stencil (contiguous in the cell-sorted arrays); v, m and the
-//      signed reciprocal mass (sign = clamp flag) of every row, the cell's
-//      CSR slot block (pair factor, stencil-local neighbour index), its row
-//      offsets and the per-particle fold constants arrive through 1-D bulk
-//      copies (cp.async.bulk of 16-byte aligned supersets) on one mbarrier:
-//      one HBM latency per cell. The tile is sized so every cell of a colour
-//      is resident at once (one wave);
-//   2. the chain: the cell's particles in order (ascending id forward,
-//      descending on the reverse leg, damping.cpp:112-121). The particle-split
-//      update is separable per velocity component once diag and denom are
-//      known, so warp d runs the whole chain of component d with no
-//      synchronisation between warps. Lane l owns slots l, l+32, ... (K per
-//      lane, branch-free, next particle's slot metadata prefetched); the
-//      residual is reduced with warp shuffles (FAST) or folded by lane 0 in
-//      slot order (ORDERED, bit-exact with the reference); rate = residual /
-//      denom and the momentum-conserving neighbour correction follow from
-//      registers;
-//   3. write-back of the stencil velocities by all threads (disjoint
-//      stencils: no races).
-// Pairwise split: the same staging; warp d computes the per-slot
-// b/(m_i m_j - (m_i+m_j) b) of particle i and its lane 0 runs the palindromic
-// pair chain (damping.cpp:161-176) of component d (components never mix in
-// the 2x2 solve).
+// Per colour phase, one launch over the colour's non-empty cells, fuller cells
+// first (DevSystem::build_colour_lists). Colour b holds the cells whose
+// coordinates are congruent to b's residues mod 3; their 3^D stencils are
+// disjoint (neighbors.hpp:50-52), so every cell is an independent task:
+//
+// k_sweep_fast (FAST particle split, the bench path): one warp per cell,
+// chained to the previous phase by programmatic dependent launch.
+//   1. staging: the cell's slot block (pair factor G, per-slot mass factor
+//      G/m_j, stencil-local index), row offsets and fold constants by bulk
+//      copies (TMA) and the stencil rows' addresses -- all static, before
+//      griddepcontrol.wait; then the stencil velocities by per-lane cp.async;
+//   2. the chain (sweep_chain.cuh): the cell's particles in order (ascending
+//      id forward, descending on the reverse leg, damping.cpp:112-121), all D
+//      components per lane, one transposed shuffle tree per particle;
+//   3. write-back of the stencil rows by bulk stores (disjoint stencils: no
+//      races), plus, for a slab, the columns shared with its neighbours
+//      straight into their arrays (writeback_peers).
+//
+// k_sweep_phase (ORDERED particle split, pairwise split): one 128-thread CTA
+// per cell with the same staging; warp d runs the chain of component d (the
+// update is separable per component once diag and denom are known). ORDERED:
+// lanes form the residual terms, lane 0 folds them in slot order (bit-exact).
+// Pairwise: warp d computes the per-slot b/(m_i m_j - (m_i+m_j) b) and its
+// lane 0 runs the palindromic pair chain (damping.cpp:161-176) of component d.
 //
 // Division. B200 IEEE fp64 division costs ~425 cycles of dependent latency
 // (tools/fp64_latency.cu), so no division sits on the chain:
