@@ -262,6 +262,37 @@ def test_sweep_fast_within_tolerance(dim):
     assert rel_l2(d.get("v"), o.get("v")) <= TOL
 
 
+def irregular_bodies():
+    rng = np.random.RandomState(11)
+    yield "random2d", rng.uniform(0, 1, (600, 2)), 1e-4, 0.05          # ragged rows, sparse cells
+    yield "random3d", rng.uniform(0, 0.5, (700, 3)), 1e-6, 0.05        # 3D, K <= 4 register path
+    base = lattice_r0([12, 10, 9], 0.01)
+    yield "jitter3d", base + rng.uniform(-0.004, 0.004, base.shape), 1e-6, 0.013
+    yield "dense3d", rng.uniform(0, 0.25, (1000, 3)), 1e-6, 0.05       # > 128 slots per row: generic loop
+
+
+@pytest.mark.parametrize("case", list(irregular_bodies()), ids=lambda c: c[0])
+@pytest.mark.parametrize("mode", ["ordered", "fast"])
+def test_sweep_irregular_bodies(case, mode):
+    """Variable neighbour counts and cell occupancy, including rows longer than the register path."""
+    name, r0, V0, h = case
+    cons = (r0[:, 0] < np.quantile(r0[:, 0], 0.05)).astype(np.uint8)
+    o, d = pair(r0, V0, 1000.0, h, constrained=cons)
+    d.set_reduction(mode)
+    v = random_velocities(len(r0), r0.shape[1], 1.0, 21)
+    v[cons == 1] = 0.0
+    o.set("v", v)
+    d.set("v", v)
+    for _ in range(2):
+        o.damping_sweep("particle_split", 300.0, 1e-4)
+        d.damping_sweep("particle_split", 300.0, 1e-4)
+    if mode == "ordered":
+        assert np.array_equal(o.get("v"), d.get("v"))
+    else:
+        assert rel_l2(d.get("v"), o.get("v")) <= TOL
+    assert np.all(d.get("v")[cons == 1] == 0.0)
+
+
 def test_sweep_zero_eta_noop_and_explicit_rejected():
     r0 = lattice_r0([5, 5], 0.01)
     d = dev.DeviceSystem(r0, 1e-4, 1000.0, 0.013)
