@@ -113,7 +113,9 @@ tlsph_status tlsph_dev_create_grid(int dim, size_t n, const double* positions, d
 tlsph_status tlsph_dev_create_in_grid(int dim, size_t n, const double* r0, const double* V0, const double* rho0,
                                       const uint8_t* constrained, double h, const double* origin, const int* dims,
                                       tlsph_dev** out);
-/* Sweep tasks are the cells with x in [x0, x1) (default: the whole grid). */
+/* The slab's own cell columns [x0, x1) (default: the whole grid): they are its
+ * sweep tasks, and the TL-SPH passes and reductions advance only the particles
+ * of these columns (the halo columns' state arrives from their owners). */
 tlsph_status tlsph_dev_set_task_range(tlsph_dev* dev, int x0, int x1);
 /* One colour phase of strang_damping_sweep (damping.cpp:125-182): pass 0 is
  * the forward leg (colour `index` ascending), pass 1 the reverse leg; the
@@ -133,6 +135,14 @@ tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer);
 int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x);
 tlsph_status tlsph_dev_pack_column(tlsph_dev* dev, int x, double* device_dst);
 tlsph_status tlsph_dev_unpack_column(tlsph_dev* dev, int x, const double* device_src);
+/* The same for a named column field, component-major (width x count doubles):
+ * VELOCITY (width D; the sweep's and pass C's halo), STRESS (width D*D + 1:
+ * P B0 row-major and V0, the record pass B gathers, written by pass A). */
+typedef enum tlsph_dev_column_field { TLSPH_DEV_COLUMN_VELOCITY = 0, TLSPH_DEV_COLUMN_STRESS = 1 } tlsph_dev_column_field;
+int tlsph_dev_column_width(const tlsph_dev* dev, tlsph_dev_column_field field); /* -1 on error */
+tlsph_status tlsph_dev_pack_column_field(tlsph_dev* dev, tlsph_dev_column_field field, int x, double* device_dst);
+tlsph_status tlsph_dev_unpack_column_field(tlsph_dev* dev, tlsph_dev_column_field field, int x,
+                                           const double* device_src);
 
 void tlsph_dev_destroy(tlsph_dev* dev);
 
@@ -170,6 +180,17 @@ tlsph_status tlsph_dev_update_density(tlsph_dev* dev);                      /* i
 tlsph_status tlsph_dev_momentum_rhs(tlsph_dev* dev, const tlsph_dev_material* mat); /* :80-116 */
 tlsph_status tlsph_dev_verlet_step(tlsph_dev* dev, const tlsph_dev_material* mat, double dt); /* :118-152 */
 tlsph_status tlsph_dev_apply_constraints(tlsph_dev* dev);                   /* particle_system.hpp:51-58 */
+/* One pass of verlet_step (integrator.cpp:118-152) as the device loop fuses it:
+ * 0 = A (density from J^n, half-kick of F and r, constraints, P B0 record),
+ * 1 = B (momentum RHS + kick + constraints), 2 = C (dF/dt, density from
+ * J^(n+1/2), half-kick, constraints). Passes 0, 1, 2 in order equal
+ * tlsph_dev_verlet_step; an x-slab driver exchanges halo columns between them. */
+tlsph_status tlsph_dev_verlet_pass(tlsph_dev* dev, const tlsph_dev_material* mat, double dt, int pass);
+/* |v|max, |a|max (stable_dt's inputs, integrator.cpp:154-169) and, when
+ * want_ke, the kinetic energy (:171-178) over the owned particles into out[3];
+ * check_step >= 0 also runs check_finite (runner.cpp:233-247) for that step.
+ * A slab driver combines them across slabs (max, max, sum). */
+tlsph_status tlsph_dev_reduce_state(tlsph_dev* dev, int want_ke, int64_t check_step, double* out);
 /* stable_dt (integrator.cpp:154-169): writes 0.6*min(h/(c+|v|max), sqrt(h/|a|max)). */
 tlsph_status tlsph_dev_stable_dt(tlsph_dev* dev, const tlsph_dev_material* mat, double h, double* dt_acoustic);
 tlsph_status tlsph_dev_kinetic_energy(tlsph_dev* dev, double* out);        /* integrator.cpp:171-178 */

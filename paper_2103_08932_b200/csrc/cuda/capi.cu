@@ -160,6 +160,7 @@ tlsph_status tlsph_dev_set_task_range(tlsph_dev* dev, int x0, int x1) {
     s.task_x0 = x0;
     s.task_x1 = x1;
     s.build_colour_lists();
+    s.build_own_mask();
   });
 }
 
@@ -200,11 +201,26 @@ int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x) {
 }
 
 tlsph_status tlsph_dev_pack_column(tlsph_dev* dev, int x, double* device_dst) {
-  return guarded([&] { sys(dev).pack_column(x, device_dst); });
+  return guarded([&] { sys(dev).pack_column(TLSPH_DEV_COLUMN_VELOCITY, x, device_dst); });
 }
 
 tlsph_status tlsph_dev_unpack_column(tlsph_dev* dev, int x, const double* device_src) {
-  return guarded([&] { sys(dev).unpack_column(x, device_src); });
+  return guarded([&] { sys(dev).unpack_column(TLSPH_DEV_COLUMN_VELOCITY, x, device_src); });
+}
+
+int tlsph_dev_column_width(const tlsph_dev* dev, tlsph_dev_column_field field) {
+  int w = -1;
+  const tlsph_status st = guarded([&] { w = sys(dev).column_width(field); });
+  return st == TLSPH_OK ? w : -1;
+}
+
+tlsph_status tlsph_dev_pack_column_field(tlsph_dev* dev, tlsph_dev_column_field field, int x, double* device_dst) {
+  return guarded([&] { sys(dev).pack_column(field, x, device_dst); });
+}
+
+tlsph_status tlsph_dev_unpack_column_field(tlsph_dev* dev, tlsph_dev_column_field field, int x,
+                                           const double* device_src) {
+  return guarded([&] { sys(dev).unpack_column(field, x, device_src); });
 }
 
 tlsph_status tlsph_dev_set_contact_plane(tlsph_dev* dev, const double* point, const double* normal,
@@ -317,6 +333,20 @@ tlsph_status tlsph_dev_kinetic_energy(tlsph_dev* dev, double* out) {
 
 tlsph_status tlsph_dev_check_finite(tlsph_dev* dev, uint64_t step) {
   return guarded([&] { sys(dev).check_finite(step); });
+}
+
+tlsph_status tlsph_dev_verlet_pass(tlsph_dev* dev, const tlsph_dev_material* mat, double dt, int pass) {
+  return guarded([&] {
+    require_material(mat);
+    sys(dev).verlet_pass(tlsph_cuda::to_dmat(*mat), dt, pass);
+  });
+}
+
+tlsph_status tlsph_dev_reduce_state(tlsph_dev* dev, int want_ke, int64_t check_step, double* out) {
+  return guarded([&] {
+    if (!out) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "out must not be null");
+    sys(dev).reduce_owned(want_ke != 0, check_step, out);
+  });
 }
 
 tlsph_status tlsph_dev_damping_sweep(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt) {

@@ -117,6 +117,10 @@ struct DFields {
   double* rho0;
   double* rho;
   uint8_t* flag;
+  // x-slab ownership (slabs.py): 1 for particles of the slab's own cell columns, 0 for its halo
+  // columns; null when the system is not a slab (every particle owned). The TL-SPH passes and
+  // reductions skip halo particles, whose state arrives from the owning slab.
+  const uint8_t* own;
   int* perm;  // sorted -> reference index
   int* rank;  // reference -> sorted index
   // reference-configuration CSR in sorted row order
@@ -139,6 +143,9 @@ struct DFields {
   double cp_normal[3];
   double cp_k;
 };
+
+// x-slab ownership: halo particles of a slab are read, never advanced, by the TL-SPH passes
+__device__ __forceinline__ bool is_owned(const DFields& f, long long i) { return !f.own || f.own[i]; }
 
 constexpr int kWarp = 32;
 constexpr uint16_t kNoLocal = 0xFFFF;

@@ -41,6 +41,7 @@ __global__ void k_step_begin(DFields f, DScalars* sc, double* __restrict__ parti
   double vmax = 0.0, amax = 0.0, ke = 0.0;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < f.n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!is_owned(f, i)) continue;
     double sv = f.v[0][i] * f.v[0][i], sa = f.a[0][i] * f.a[0][i];
     bool fin = isfinite(f.v[0][i]) && isfinite(f.r[0][i]);
 #pragma unroll

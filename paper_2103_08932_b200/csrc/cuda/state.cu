@@ -570,6 +570,7 @@ DFields DevSystem::fields() const {
   f.qf = qf.p;
   f.pfsum = pf_sum.p;
   f.peer_idx = peer_idx.p;
+  f.own = own.p;
   for (int k = 0; k < 2; ++k) {
     f.peer_x[k] = peer_x[k];
     for (int d = 0; d < 3; ++d) f.peer_v[k][d] = peer_v[k][d];

@@ -350,6 +350,19 @@ __device__ __forceinline__ void wait_staging(const Tile<D>& t) {
 template <int D>
 __device__ __forceinline__ void writeback_rows(const DFields& f, const Tile<D>& t, int lane) {
   constexpr int kSegs = seg_count<D>();
+#ifdef TLSPH_WB_PLAIN
+  __syncwarp();
+#pragma unroll 1
+  for (int q = 0; q < kSegs; ++q) {
+    const long long rs = t.seg_start[q];
+    const int len = t.seg_len[q], tb = t.seg_base[q];
+    for (int e = lane; e < len; e += 32) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) f.v[d][rs + e] = t.sv[d][tb + e];
+    }
+  }
+  return;
+#endif
   fence_proxy_async_smem();  // the chain's shared-memory writes, visible to the bulk copies
   __syncwarp();
   if (lane < kSegs) {
@@ -824,18 +837,26 @@ void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_
 // ------------------------------------------------------------------ x-slab halo columns
 // Particles of cell column x in (z, y, cell order): the same sequence on every
 // rank that holds the column (cells keep ascending reference ids).
+// Component c of particle p of a column field lives at ptr[c][p * stride].
+struct ColumnField {
+  double* ptr[10];
+  int ncomp;
+  long long stride;
+};
+
 __global__ void k_column_copy(const long long* __restrict__ cell_start, const long long* __restrict__ col_off,
-                              int x, int dims0, int ncol_cells, DFields f, double* __restrict__ buf, long long count,
-                              int D, int pack) {
+                              int x, int dims0, int ncol_cells, ColumnField cf, double* __restrict__ buf,
+                              long long count, int pack) {
   const int q = blockIdx.x;  // (y, z) cell of the column
   if (q >= ncol_cells) return;
   const long long lin = static_cast<long long>(q) * dims0 + x;
   const long long p0 = cell_start[lin], p1 = cell_start[lin + 1];
   const long long o = col_off[q];
   for (long long e = threadIdx.x; e < p1 - p0; e += blockDim.x)
-    for (int d = 0; d < D; ++d) {
-      if (pack) buf[d * count + o + e] = f.v[d][p0 + e];
-      else f.v[d][p0 + e] = buf[d * count + o + e];
+    for (int c = 0; c < cf.ncomp; ++c) {
+      double* a = cf.ptr[c] + (p0 + e) * cf.stride;
+      if (pack) buf[c * count + o + e] = *a;
+      else *a = buf[c * count + o + e];
     }
 }
 
@@ -933,6 +954,24 @@ void DevSystem::build_colour_lists() {
   sync();
 }
 
+// Ownership of a slab's particles: those of the task columns [x0, x1). The
+// whole grid as task range (or no slab) clears the mask: every particle owned.
+void DevSystem::build_own_mask() {
+  const int x0 = task_x0, x1 = task_x1 < 0 ? dims[0] : std::min(task_x1, dims[0]);
+  if (x0 <= 0 && x1 >= dims[0]) {
+    own.release();
+    return;
+  }
+  std::vector<uint8_t> m(static_cast<size_t>(n), 0);
+  for (long long lin = 0; lin < ncells; ++lin) {
+    const int x = static_cast<int>(lin % dims[0]);
+    if (x < x0 || x >= x1) continue;
+    for (long long p = cell_start_h[lin]; p < cell_start_h[lin + 1]; ++p) m[static_cast<size_t>(p)] = 1;
+  }
+  own.alloc(m.size());
+  CK(cudaMemcpy(own.p, m.data(), m.size(), cudaMemcpyHostToDevice));
+}
+
 void DevSystem::enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index) {
   const int nb = D == 2 ? 9 : 27;
   if (pass < 0 || pass > 1 || index < 0 || index >= nb)
@@ -956,7 +995,24 @@ std::vector<long long> column_offsets(const DevSystem& s, int x) {
   return off;
 }
 
-void column_copy(DevSystem& s, int x, double* buf, bool pack) {
+ColumnField column_field(const DevSystem& s, int field) {
+  ColumnField cf{};
+  if (field == TLSPH_DEV_COLUMN_VELOCITY) {
+    cf.ncomp = s.D;
+    cf.stride = 1;
+    for (int d = 0; d < s.D; ++d) cf.ptr[d] = s.v[d].p;
+  } else if (field == TLSPH_DEV_COLUMN_STRESS) {
+    cf.ncomp = s.D * s.D + 1;  // P B0 row-major, V0 (the packed momentum-gather record)
+    cf.stride = s.D == 2 ? pbv_stride<2>() : pbv_stride<3>();
+    for (int c = 0; c < cf.ncomp; ++c) cf.ptr[c] = s.pbv.p + c;
+  } else {
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown column field " + std::to_string(field));
+  }
+  return cf;
+}
+
+void column_copy(DevSystem& s, int field, int x, double* buf, bool pack) {
+  const ColumnField cf = column_field(s, field);
   const std::vector<long long> off = column_offsets(s, x);
   const int nq = static_cast<int>(off.size()) - 1;
   const long long count = off.back();
@@ -964,16 +1020,19 @@ void column_copy(DevSystem& s, int x, double* buf, bool pack) {
   DBuf<long long> doff;
   doff.alloc(off.size());
   CK(cudaMemcpyAsync(doff.p, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice, s.stream));
-  k_column_copy<<<static_cast<unsigned>(nq), 64, 0, s.stream>>>(s.cell_start.p, doff.p, x, s.dims[0], nq, s.fields(),
-                                                                buf, count, s.D, pack ? 1 : 0);
+  k_column_copy<<<static_cast<unsigned>(nq), 64, 0, s.stream>>>(s.cell_start.p, doff.p, x, s.dims[0], nq, cf, buf,
+                                                                count, pack ? 1 : 0);
   CK_LAUNCH("k_column_copy");
   s.sync();  // the buffer is handed to another stream / library (NCCL, torch)
 }
 }  // namespace
 
 long long DevSystem::column_count(int x) const { return column_offsets(*this, x).back(); }
-void DevSystem::pack_column(int x, double* dev_dst) { column_copy(*this, x, dev_dst, true); }
-void DevSystem::unpack_column(int x, const double* dev_src) { column_copy(*this, x, const_cast<double*>(dev_src), false); }
+int DevSystem::column_width(int field) const { return column_field(*this, field).ncomp; }
+void DevSystem::pack_column(int field, int x, double* dev_dst) { column_copy(*this, field, x, dev_dst, true); }
+void DevSystem::unpack_column(int field, int x, const double* dev_src) {
+  column_copy(*this, field, x, const_cast<double*>(dev_src), false);
+}
 
 unsigned long long selftest_division(long long n, unsigned long long seed) {
   DBuf<unsigned long long> bad;

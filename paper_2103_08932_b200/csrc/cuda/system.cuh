@@ -72,6 +72,7 @@ class DevSystem {
   // phase's longest chains get the first SM slots; colour b's list starts at colour_start[b]
   // fused halo exchange with neighbouring slabs (tlsph_dev_link_peer)
   DBuf<int> peer_idx;
+  DBuf<uint8_t> own;  // x-slab ownership mask (set_task_range); empty: all owned
   double* peer_v[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
   int peer_x[2] = {-1, -1};
   DBuf<int> colour_cells;
@@ -151,6 +152,8 @@ class DevSystem {
   void update_density();
   void momentum_rhs(const DMaterial& mat);
   void verlet_step(const DMaterial& mat, double dt);
+  void verlet_pass(const DMaterial& mat, double dt, int pass);
+  void reduce_owned(bool want_ke, long long check_step, double out[3]);
   void apply_constraints();
   double stable_dt(const DMaterial& mat, double h_);
   double kinetic_energy();
@@ -162,11 +165,13 @@ class DevSystem {
   // one colour phase (pass 0 forward / 1 reverse, index-th colour of the pass)
   void enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index);
   void build_colour_lists();  // host sync: at construction and when the task range changes
+  void build_own_mask();      // own[] from the task range (x-slab ownership)
   void link_peer(int side, DevSystem& peer);  // sweep.cu
   // x-slab halo columns (sweep.cu)
   long long column_count(int x) const;
-  void pack_column(int x, double* dev_dst);
-  void unpack_column(int x, const double* dev_src);
+  int column_width(int field) const;  // doubles per particle of a column field
+  void pack_column(int field, int x, double* dev_dst);
+  void unpack_column(int field, int x, const double* dev_src);
   void particle_split_update(long long i, double eta, double dt_half);
   void pairwise_split_update(long long i, long long slot, double eta, double dt_half);
   void explicit_damping_accel(double eta, double* out_host);

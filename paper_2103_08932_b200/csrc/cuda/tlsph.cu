@@ -28,7 +28,7 @@ unsigned grid_for(long long n, int block) { return static_cast<unsigned>((n + bl
 template <int D>
 __global__ void k_correction_matrices(DFields f, DScalars* sc) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= f.n) return;
+  if (i >= f.n || !is_owned(f, i)) return;  // a halo particle's neighbourhood is cut by the slab
   M<D> mom;
 #pragma unroll
   for (int r = 0; r < D; ++r)
@@ -66,7 +66,7 @@ __global__ void k_deformation_rate(DFields f, DScalars* sc, double dt, int loop)
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long i = tid / G;
   const int l = static_cast<int>(tid % G);
-  const bool active = i < f.n;
+  const bool active = i < f.n && is_owned(f, i);
   double rate[D][D];
 #pragma unroll
   for (int r = 0; r < D; ++r)
@@ -132,7 +132,7 @@ __global__ void k_deformation_rate(DFields f, DScalars* sc, double dt, int loop)
 template <int D>
 __global__ void k_update_density(DFields f, DScalars* sc) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= f.n) return;
+  if (i >= f.n || !is_owned(f, i)) return;
   const double J = det(load_mat<D>(f.F, i));
   if (!(J > 0.0)) {
     record_error(sc, ERR_DENSITY_PRE, static_cast<unsigned long long>(f.perm[i]));
@@ -148,7 +148,7 @@ __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int 
   if (loop && sc->halt) return;
   const double half = 0.5 * (loop ? sc->dt : dt);
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= f.n) return;
+  if (i >= f.n || !is_owned(f, i)) return;  // a slab's halo records arrive from their owner
   M<D> F = load_mat<D>(f.F, i);
   if (PRE) {
     const double J0 = det(F);
@@ -201,7 +201,7 @@ __global__ void k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long i = tid / G;
   const int l = static_cast<int>(tid % G);
-  const bool active = i < f.n;
+  const bool active = i < f.n && is_owned(f, i);
   double acc[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) acc[d] = 0.0;
@@ -302,6 +302,7 @@ __global__ void k_reduce(DFields f, double* __restrict__ partials, DScalars* sc,
   double vmax = 0.0, amax = 0.0, ke = 0.0;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < f.n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!is_owned(f, i)) continue;
     double sv = f.v[0][i] * f.v[0][i], sa = f.a[0][i] * f.a[0][i];
     bool fin = isfinite(f.v[0][i]) && isfinite(f.r[0][i]);
 #pragma unroll
@@ -396,31 +397,30 @@ void DevSystem::momentum_rhs(const DMaterial& mat) {
   sync();
 }
 
-// Enqueues the three verlet passes on the handle's stream (no sync).
-void enqueue_verlet(DevSystem& s, const DMaterial& mat, double dt, int loop) {
+// Enqueues one verlet pass (0: A, 1: B, 2: C) on the handle's stream (no sync).
+void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop, int pass) {
   DFields f = s.fields();
   const long long n = s.n;
   const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED;
   cudaStream_t st = s.stream;
   if (s.D == 2) {
-    k_stress<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
-    if (ord) {
-      k_momentum<2, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-      k_deformation_rate<2, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    } else {
-      k_momentum<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-      k_deformation_rate<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    }
+    if (pass == 0) k_stress<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
+    else if (pass == 1 && ord) k_momentum<2, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1) k_momentum<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (ord) k_deformation_rate<2, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else k_deformation_rate<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
   } else {
-    k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
-    if (ord) {
-      k_momentum<3, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-      k_deformation_rate<3, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    } else {
-      k_momentum<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-      k_deformation_rate<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    }
+    if (pass == 0) k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
+    else if (pass == 1 && ord) k_momentum<3, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1) k_momentum<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (ord) k_deformation_rate<3, 1, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else k_deformation_rate<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
   }
+}
+
+// Enqueues the three verlet passes on the handle's stream (no sync).
+void enqueue_verlet(DevSystem& s, const DMaterial& mat, double dt, int loop) {
+  for (int pass = 0; pass < 3; ++pass) enqueue_verlet_pass(s, mat, dt, loop, pass);
   CK_LAUNCH("verlet passes");
 }
 
@@ -429,6 +429,16 @@ void DevSystem::verlet_step(const DMaterial& mat, double dt) {
   enqueue_verlet(*this, mat, dt, 0);
   raise_if_failed("verlet_step");
 }
+
+// One pass of verlet_step (x-slab driver: halo exchanges between the passes).
+void DevSystem::verlet_pass(const DMaterial& mat, double dt, int pass) {
+  if (pass < 0 || pass > 2) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "verlet pass must be 0 (A), 1 (B) or 2 (C)");
+  reset_errors();
+  enqueue_verlet_pass(*this, mat, dt, 0, pass);
+  CK_LAUNCH("verlet pass");
+  raise_if_failed("verlet_step");
+}
+
 
 void DevSystem::apply_constraints() {
   DFields f = fields();
@@ -486,6 +496,27 @@ void DevSystem::check_finite(uint64_t step) {
   CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
   if (hs.failed) {
     hs.err_step = static_cast<long long>(step);
+    CK(cudaMemcpy(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice));
+    raise_if_failed("check_finite");
+  }
+}
+
+// |v|max, |a|max and kinetic energy over the owned particles; a non-finite
+// owned particle fails with the check_finite message for `step` (check >= 0).
+void DevSystem::reduce_owned(bool want_ke, long long check_step, double out[3]) {
+  reset_errors();
+  const Reduced r = reduce_state(*this, want_ke);
+  out[0] = r.vmax;
+  out[1] = r.amax;
+  out[2] = r.ke;
+  if (check_step < 0) {
+    reset_errors();
+    return;
+  }
+  DScalars hs;
+  CK(cudaMemcpy(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost));
+  if (hs.failed) {
+    hs.err_step = check_step;
     CK(cudaMemcpy(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice));
     raise_if_failed("check_finite");
   }

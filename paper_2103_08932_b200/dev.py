@@ -35,6 +35,7 @@ FIELDS = {"r0": 0, "r": 1, "v": 2, "a": 3, "F": 4, "dFdt": 5, "B0": 6, "V0": 7, 
 _VEC = {"r0", "r", "v", "a", "body"}
 _MAT = {"F", "dFdt", "B0"}
 SCHEMES = {"explicit": 0, "particle_split": 1, "pairwise_split": 2}
+COLUMN_FIELDS = {"velocity": 0, "stress": 1}  # tlsph_dev_column_field
 
 
 class TlsphError(RuntimeError):
@@ -111,6 +112,11 @@ def lib():
     L.tlsph_dev_column_count.restype = C.c_int64
     L.tlsph_dev_pack_column.argtypes = [P, I, C.c_void_p]
     L.tlsph_dev_unpack_column.argtypes = [P, I, C.c_void_p]
+    L.tlsph_dev_column_width.argtypes = [P, I]
+    L.tlsph_dev_pack_column_field.argtypes = [P, I, I, C.c_void_p]
+    L.tlsph_dev_unpack_column_field.argtypes = [P, I, I, C.c_void_p]
+    L.tlsph_dev_verlet_pass.argtypes = [P, C.POINTER(Material), C.c_double, I]
+    L.tlsph_dev_reduce_state.argtypes = [P, I, C.c_int64, D]
     L.tlsph_dev_destroy.argtypes = [P]
     L.tlsph_dev_size.argtypes = [P]
     L.tlsph_dev_size.restype = S
@@ -360,12 +366,31 @@ class DeviceSystem:
             raise TlsphError(1, lib().tlsph_dev_last_error().decode())
         return c
 
-    def pack_column(self, x, device_ptr):
-        """Velocities of cell column x into the device buffer at device_ptr (D x count doubles)."""
-        _check(lib().tlsph_dev_pack_column(self._h, int(x), C.c_void_p(int(device_ptr))))
+    def column_width(self, field="velocity"):
+        """Doubles per particle of a column field ("velocity": D, "stress": D*D + 1)."""
+        w = int(lib().tlsph_dev_column_width(self._h, COLUMN_FIELDS[field]))
+        if w < 0:
+            raise TlsphError(1, lib().tlsph_dev_last_error().decode())
+        return w
 
-    def unpack_column(self, x, device_ptr):
-        _check(lib().tlsph_dev_unpack_column(self._h, int(x), C.c_void_p(int(device_ptr))))
+    def pack_column(self, x, device_ptr, field="velocity"):
+        """Field of cell column x into the device buffer at device_ptr (width x count doubles)."""
+        _check(lib().tlsph_dev_pack_column_field(self._h, COLUMN_FIELDS[field], int(x), C.c_void_p(int(device_ptr))))
+
+    def unpack_column(self, x, device_ptr, field="velocity"):
+        _check(lib().tlsph_dev_unpack_column_field(self._h, COLUMN_FIELDS[field], int(x),
+                                                   C.c_void_p(int(device_ptr))))
+
+    def verlet_pass(self, material, dt, pass_):
+        """One pass of verlet_step: 0 = A (stress record), 1 = B (momentum + kick), 2 = C (dF/dt)."""
+        _check(lib().tlsph_dev_verlet_pass(self._h, C.byref(material), float(dt), int(pass_)))
+
+    def reduce_state(self, want_ke=False, check_step=-1):
+        """(|v|max, |a|max, kinetic energy) over the owned particles; check_step >= 0 also runs
+        check_finite for that step."""
+        out = np.zeros(3)
+        _check(lib().tlsph_dev_reduce_state(self._h, 1 if want_ke else 0, int(check_step), _dp(out)))
+        return float(out[0]), float(out[1]), float(out[2])
 
     def particle_split_update(self, i, eta, dt_half):
         _check(lib().tlsph_dev_particle_split_update(self._h, i, eta, dt_half))

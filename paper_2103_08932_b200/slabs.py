@@ -20,11 +20,22 @@ The fused form (``link_peers`` / ``sweep_fused``): each slab's phase kernels sto
 columns straight into the neighbouring slab's arrays (NVLink peer access between GPUs), so the
 only inter-slab operation left is the per-phase ordering.
 
-The driver is independent of the engine and the transport: an engine runs a slab's colour
-phases and packs/unpacks halo columns (``DeviceSlabEngine`` over a ``DeviceSystem``);
-``SlabSweep`` exchanges the columns through ``torch.distributed`` (NCCL between GPUs, gloo
-on CPU) and ``sweep_in_process`` runs several slabs in one process with direct copies (the
-sequential statement of the same protocol).
+Full step (``run_loop``). A slab advances only its own particles through the TL-SPH passes
+(tlsph_dev_set_task_range also sets the ownership mask); its halo columns are refreshed from
+their owners twice per step -- the (P B0, V0) record after pass A, which pass B gathers, and the
+velocities after pass B's kick, which pass C and the sweep read -- and stable_dt's |v|max,
+|a|max are combined across slabs (max is exact, so dt is bitwise that of one GPU). The
+random-choice stream is replicated (RandomSource(seed) on every rank). With these, every
+owned particle follows bit for bit the undivided device loop (DevSystem::run,
+runner.cpp:341-391).
+
+The driver is independent of the engine and the transport: an engine runs a slab's passes
+and colour phases and packs/unpacks halo columns (``DeviceSlabEngine`` over a
+``DeviceSystem``); a group moves the columns -- ``LocalGroup`` between slabs held by this
+process with direct copies (the sequential statement of the protocol), ``DistGroup`` through
+``torch.distributed`` point-to-point operations (NCCL between GPUs, gloo on CPU) with
+all-reduces for the step scalars. ``sweep_in_process`` and ``SlabSweep`` are the sweep alone
+over those two groups.
 """
 from __future__ import annotations
 
@@ -155,8 +166,19 @@ def make_device_slab(grid, slab, r0, V0, rho0, h, constrained=None):
     return d
 
 
+def halo_transfers(ranges):
+    """Owner-to-holder transfers that refresh every halo column: at each boundary the left
+    slab's last own column (x1 - 1) goes right and the right slab's first (x1) goes left."""
+    out = []
+    for r in range(len(ranges) - 1):
+        x1 = ranges[r][1]
+        out.append(Transfer(x1 - 1, r, r + 1))
+        out.append(Transfer(x1, r + 1, r))
+    return out
+
+
 class DeviceSlabEngine:
-    """Phase runner + halo-column buffers of one DeviceSystem slab (CUDA torch tensors)."""
+    """Passes, phases and halo-column buffers of one DeviceSystem slab (CUDA torch tensors)."""
 
     def __init__(self, system, dim, device="cuda"):
         self.d = system
@@ -166,35 +188,109 @@ class DeviceSlabEngine:
     def phase(self, scheme, eta_tilde, dt, p, index):
         self.d.damping_phase(scheme, eta_tilde, dt, p, index)
 
-    def empty(self, x):
+    def verlet_pass(self, material, dt, p):
+        self.d.verlet_pass(material, dt, p)
+
+    def reduce(self, want_ke, check_step):
+        return self.d.reduce_state(want_ke, check_step)
+
+    def empty(self, x, field="velocity"):
         import torch
 
-        return torch.empty(self.dim * self.d.column_count(x), dtype=torch.float64, device=self.device)
+        w = self.d.column_width(field)
+        return torch.empty(w * self.d.column_count(x), dtype=torch.float64, device=self.device)
 
-    def pack(self, x):
-        buf = self.empty(x)
+    def pack(self, x, field="velocity"):
+        buf = self.empty(x, field)
         if buf.numel():
-            self.d.pack_column(x, buf.data_ptr())
+            self.d.pack_column(x, buf.data_ptr(), field)
         return buf
 
-    def unpack(self, x, buf):
+    def unpack(self, x, buf, field="velocity"):
         import torch
 
         if buf.numel():
             torch.cuda.synchronize(self.device)  # a received buffer is written on the communicator's stream
-            self.d.unpack_column(x, buf.data_ptr())
+            self.d.unpack_column(x, buf.data_ptr(), field)
+
+
+class LocalGroup:
+    """Slabs held by this process (one per GPU, or several on one): direct column copies."""
+
+    def __init__(self, engines, ranges):
+        self.engines = list(engines)
+        self.ranges = list(ranges)
+
+    def each(self, fn):
+        for e in self.engines:
+            fn(e)
+
+    def exchange(self, transfers, field="velocity"):
+        for t in transfers:
+            self.engines[t.dst].unpack(t.column, self.engines[t.src].pack(t.column, field), field)
+
+    def reduce(self, want_ke, check_step):
+        vals = [e.reduce(want_ke, check_step) for e in self.engines]
+        return max(v[0] for v in vals), max(v[1] for v in vals), sum(v[2] for v in vals)
+
+
+class DistGroup:
+    """This rank's slab; columns travel through torch.distributed point-to-point operations
+    (NCCL between GPUs, gloo on CPU), step scalars through all-reduces."""
+
+    def __init__(self, engine, ranges, rank):
+        self.e = engine
+        self.ranges = list(ranges)
+        self.rank = rank
+
+    def each(self, fn):
+        fn(self.e)
+
+    def exchange(self, transfers, field="velocity"):
+        import torch.distributed as dist
+
+        ops, unpack = [], []
+        for t in transfers:
+            if t.src == self.rank:
+                ops.append(dist.P2POp(dist.isend, self.e.pack(t.column, field), t.dst))
+            elif t.dst == self.rank:
+                buf = self.e.empty(t.column, field)
+                ops.append(dist.P2POp(dist.irecv, buf, t.src))
+                unpack.append((t.column, buf))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for col, buf in unpack:
+            self.e.unpack(col, buf, field)
+
+    def reduce(self, want_ke, check_step):
+        import torch
+        import torch.distributed as dist
+
+        vm, am, ke = self.e.reduce(want_ke, check_step)
+        mx = torch.tensor([vm, am], dtype=torch.float64, device=self.e.device)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        if want_ke:
+            s = torch.tensor([ke], dtype=torch.float64, device=self.e.device)
+            dist.all_reduce(s, op=dist.ReduceOp.SUM)
+            ke = float(s[0])
+        return float(mx[0]), float(mx[1]), ke
+
+
+def sweep(group, scheme, eta_tilde, dt, dim):
+    """strang_damping_sweep (damping.cpp:125-182) over the slabs of a group: each colour phase
+    on every slab, then that phase's column transfers."""
+    if eta_tilde == 0.0:
+        return
+    for p, index, rx in colour_schedule(dim):
+        group.each(lambda e: e.phase(scheme, eta_tilde, dt, p, index))
+        group.exchange(phase_transfers(group.ranges, rx), "velocity")
 
 
 def sweep_in_process(engines, ranges, scheme, eta_tilde, dt, dim):
     """One strang_damping_sweep over slab engines held by this process: every phase on every
     slab, then the phase's column transfers as direct copies (the protocol, sequentially)."""
-    if eta_tilde == 0.0:
-        return
-    for p, index, rx in colour_schedule(dim):
-        for e in engines:
-            e.phase(scheme, eta_tilde, dt, p, index)
-        for t in phase_transfers(ranges, rx):
-            engines[t.dst].unpack(t.column, engines[t.src].pack(t.column))
+    sweep(LocalGroup(engines, ranges), scheme, eta_tilde, dt, dim)
 
 
 def link_peers(systems):
@@ -220,28 +316,73 @@ class SlabSweep:
     point-to-point operations (NCCL between GPUs, gloo on CPU)."""
 
     def __init__(self, engine, ranges, rank, dim):
-        self.e = engine
-        self.ranges = list(ranges)
-        self.rank = rank
+        self.group = DistGroup(engine, ranges, rank)
         self.dim = dim
 
     def sweep(self, scheme, eta_tilde, dt):
-        import torch.distributed as dist
+        sweep(self.group, scheme, eta_tilde, dt, self.dim)
 
-        if eta_tilde == 0.0:
-            return
-        for p, index, rx in colour_schedule(self.dim):
-            self.e.phase(scheme, eta_tilde, dt, p, index)
-            ops, unpack = [], []
-            for t in phase_transfers(self.ranges, rx):
-                if t.src == self.rank:
-                    ops.append(dist.P2POp(dist.isend, self.e.pack(t.column), t.dst))
-                elif t.dst == self.rank:
-                    buf = self.e.empty(t.column)
-                    ops.append(dist.P2POp(dist.irecv, buf, t.src))
-                    unpack.append((t.column, buf))
-            if ops:
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
-            for col, buf in unpack:
-                self.e.unpack(col, buf)
+
+@dataclass
+class LoopSpec:
+    """The inputs of DevSystem::run (tlsph_dev_loop_params) a slab loop uses: fixed step count."""
+    material: object  # dev.Material (rho0, c)
+    h: float
+    eta: float
+    alpha: float
+    steps: int
+    seed: int = 0
+    scheme: str = "particle_split"
+    fixed_dt: float = 0.0
+    elastic: bool = True
+
+
+def step_dt(spec, vmax, amax, dim):
+    """dt of one step as k_step_begin forms it: the fixed dt, else stable_dt (integrator.cpp:
+    154-169) capped by the implicit viscous bound (damping.cpp:12-27, runner.cpp:343-351)."""
+    if spec.fixed_dt > 0.0:
+        return spec.fixed_dt
+    h = spec.h
+    bound = h / (spec.material.c + vmax)
+    if amax > 0.0:
+        b2 = math.sqrt(h / amax)
+        bound = b2 if b2 < bound else bound
+    dt = 0.6 * bound
+    if spec.eta > 0.0 and spec.scheme in ("particle_split", "explicit"):
+        nu = spec.eta / (spec.alpha * spec.material.rho0)
+        vb = (0.5 if spec.scheme == "explicit" else 50.0) * h * h / (nu * dim)
+        dt = vb if vb < dt else dt
+    return dt
+
+
+def run_loop(group, spec, dim):
+    """runner.cpp:341-391 over the slabs of a group, step for step as DevSystem::run executes
+    it: step_begin (finite check of the previous step, dt from the combined maxima), verlet
+    passes A, B, C with the halo refreshes between them, the random-choice sweep. The slabs
+    must be prepared (runner.cpp:306-312) after their task ranges are set."""
+    from . import dev
+
+    if spec.scheme not in ("particle_split", "pairwise_split"):
+        raise ValueError("slab loops sweep the split schemes only")
+    damping = spec.eta > 0.0
+    if damping and not (0.0 < spec.alpha <= 1.0):
+        raise ValueError(f"random-choice probability must lie in (0, 1], got {spec.alpha}")
+    # RandomSource(seed), one draw per step (damping.hpp:41-50, runner.cpp:358-360): replicated
+    flags = dev.random_uniforms(spec.seed, spec.steps) < spec.alpha if damping else np.zeros(spec.steps, bool)
+    eta_tilde = spec.eta / spec.alpha if damping else 0.0
+    halo = halo_transfers(group.ranges)
+    t, dt = 0.0, 0.0
+    for k in range(spec.steps):
+        vmax, amax, _ = group.reduce(False, k if k > 0 else -1)
+        dt = step_dt(spec, vmax, amax, dim)
+        if spec.elastic:
+            group.each(lambda e: e.verlet_pass(spec.material, dt, 0))
+            group.exchange(halo, "stress")
+            group.each(lambda e: e.verlet_pass(spec.material, dt, 1))
+            group.exchange(halo, "velocity")
+            group.each(lambda e: e.verlet_pass(spec.material, dt, 2))
+        if flags[k]:
+            sweep(group, spec.scheme, eta_tilde, dt, dim)
+        t = t + dt
+    group.reduce(False, spec.steps)  # check_finite of the last step
+    return {"steps": spec.steps, "damped": int(flags.sum()), "t": t, "last_dt": dt}

@@ -1,14 +1,20 @@
-"""x-slab decomposition of the damping sweep (paper_2103_08932_b200/slabs.py).
+"""x-slab decomposition of the damping sweep and the full step (SURVEY.md §8(e),
+paper_2103_08932_b200/slabs.py).
 
 CPU: the partition and exchange protocol, run with the oracle as the per-slab engine, both
 in one process and as a world-size-2/3 gloo job; the decomposed sweep must equal the
 undivided oracle sweep bit for bit (same-colour stencils are disjoint, neighbors.hpp:50-52).
-GPU: the same protocol over DeviceSystem slabs (tlsph_dev_create_in_grid + per-phase
-sweeps + column pack/unpack) against the undivided device sweep, bit for bit.
+The full-step loop (halo refreshes between the TL-SPH passes, combined step scalars) runs
+over a column-coupled toy engine under gloo and must equal the undivided toy run.
+GPU: the same protocols over DeviceSystem slabs (tlsph_dev_create_in_grid + per-phase
+sweeps + column pack/unpack, verlet passes on owned particles) against the undivided device
+sweep and the undivided device loop (tlsph_dev_run), bit for bit.
 """
 from __future__ import annotations
 
+import math
 import os
+import types
 import socket
 
 import numpy as np
@@ -87,13 +93,13 @@ class OracleSlab:
             out.extend(g["cell_particles"][g["cell_start"][c]:g["cell_start"][c + 1]])
         return self.lmap[np.array(out, dtype=np.int64)]
 
-    def empty(self, x):
+    def empty(self, x, field="velocity"):
         return torch.empty(self.dim * len(self._column(x)), dtype=torch.float64)
 
-    def pack(self, x):
+    def pack(self, x, field="velocity"):
         return torch.from_numpy(np.ascontiguousarray(self.o.get("v")[self._column(x)].T).ravel().copy())
 
-    def unpack(self, x, buf):
+    def unpack(self, x, buf, field="velocity"):
         v = self.o.get("v")
         v[self._column(x)] = buf.numpy().reshape(self.dim, -1).T
         self.o.set("v", v)
@@ -287,3 +293,189 @@ def test_device_phases_compose_to_sweep():
     for p, index, _ in slabs.colour_schedule(3):
         b.damping_phase("particle_split", 160.0, 1e-4, p, index)
     assert np.array_equal(a.get("v"), b.get("v"))
+
+
+# ---------------------------------------------------------------- full-step loop, toy engine (CPU)
+class ToySlab:
+    """Column-coupled stand-in for a slab with the dependency pattern of the real step: pass A
+    writes a per-particle record from own state (v, and w as F from dF/dt), pass B reads the
+    records of the x-neighbour columns and kicks v, pass C writes w from the velocities of the
+    x-neighbour columns (it changes no velocity, like the real pass C); a sweep task writes its
+    column and both x-neighbours. Undivided = one slab owning every column."""
+
+    NCOL, M = 13, 3
+
+    def __init__(self, x0, x1):
+        self.x0, self.x1 = x0, x1
+        self.lo, self.hi = max(0, x0 - 1), min(self.NCOL, x1 + 1)
+        c = np.arange(self.NCOL)[:, None] + np.arange(self.M)[None, :] / self.M
+        self.v = np.sin(1.7 * c)[self.lo:self.hi].copy()
+        self.rec = np.zeros_like(self.v)
+        self.a = np.zeros_like(self.v)
+        self.w = np.zeros_like(self.v)
+        self.device = "cpu"
+
+    def _own(self):
+        return range(self.x0 - self.lo, self.x1 - self.lo)
+
+    def _get(self, c, arr):
+        k = c - self.lo
+        return arr[k] if 0 <= c < self.NCOL else 0.0
+
+    def verlet_pass(self, mat, dt, p):
+        new_v = self.v.copy()
+        for k in self._own():
+            c = k + self.lo
+            if p == 0:
+                self.rec[k] = np.cos(self.v[k]) + 0.25 * c + self.w[k]
+            elif p == 1:
+                self.a[k] = self._get(c - 1, self.rec) + self._get(c + 1, self.rec) - 2.0 * self.rec[k]
+                new_v[k] = self.v[k] + dt * self.a[k]
+            else:
+                self.w[k] = self.w[k] + 0.3 * (self._get(c - 1, self.v) - self._get(c + 1, self.v))
+        self.v = new_v
+
+    def phase(self, scheme, eta, dt, p, index):
+        b = index if p == 0 else 26 - index
+        for t in range(self.x0, self.x1):
+            if t % 3 != b % 3:
+                continue
+            cols = [c for c in (t - 1, t, t + 1) if 0 <= c < self.NCOL]
+            s = sum(self.v[c - self.lo].sum() for c in cols)
+            for c in cols:
+                self.v[c - self.lo] = 0.9 * self.v[c - self.lo] + 0.1 * np.tanh(s + c) * eta * dt
+
+    def reduce(self, want_ke, check_step):
+        own = list(self._own())
+        return (float(np.abs(self.v[own]).max()), float(np.abs(self.a[own]).max()),
+                float(0.5 * (self.v[own] ** 2).sum()) if want_ke else 0.0)
+
+    def _arr(self, field):
+        return self.v if field == "velocity" else self.rec
+
+    def empty(self, x, field="velocity"):
+        return torch.empty(self.M, dtype=torch.float64)
+
+    def pack(self, x, field="velocity"):
+        return torch.from_numpy(self._arr(field)[x - self.lo].copy())
+
+    def unpack(self, x, buf, field="velocity"):
+        self._arr(field)[x - self.lo] = buf.numpy()
+
+    def owned(self):
+        return np.arange(self.x0, self.x1), self.v[list(self._own())]
+
+
+TOY_SPEC = dict(material=types.SimpleNamespace(c=3.0, rho0=1.0), h=0.05, eta=0.4, alpha=0.5, steps=9, seed=4)
+
+
+def _toy_reference():
+    whole = ToySlab(0, ToySlab.NCOL)
+    out = slabs.run_loop(slabs.LocalGroup([whole], [(0, ToySlab.NCOL)]), slabs.LoopSpec(**TOY_SPEC), 3)
+    return whole.v, out
+
+
+def test_toy_loop_in_process_equals_undivided():
+    ref, out_ref = _toy_reference()
+    ranges = slabs.plan(np.ones(ToySlab.NCOL), 3)
+    engines = [ToySlab(a, b) for a, b in ranges]
+    out = slabs.run_loop(slabs.LocalGroup(engines, ranges), slabs.LoopSpec(**TOY_SPEC), 3)
+    assert out == out_ref and 0 < out["damped"] < out["steps"]
+    got = np.concatenate([e.owned()[1] for e in engines])
+    assert np.array_equal(got, ref)
+    # without the halo refreshes the slabs drift from the undivided run
+    saved = slabs.halo_transfers
+    try:
+        slabs.halo_transfers = lambda ranges: []
+        engines = [ToySlab(a, b) for a, b in ranges]
+        slabs.run_loop(slabs.LocalGroup(engines, ranges), slabs.LoopSpec(**TOY_SPEC), 3)
+        assert not np.array_equal(np.concatenate([e.owned()[1] for e in engines]), ref)
+    finally:
+        slabs.halo_transfers = saved
+
+
+def test_step_dt_matches_device_formula():
+    mat = types.SimpleNamespace(c=40.0, rho0=1000.0)
+    spec = slabs.LoopSpec(material=mat, h=0.013, eta=100.0, alpha=0.2, steps=1)
+    dt = slabs.step_dt(spec, 0.5, 2.0e3, 3)
+    acoustic = 0.6 * min(0.013 / (40.0 + 0.5), math.sqrt(0.013 / 2.0e3))
+    visc = 50.0 * 0.013 * 0.013 / ((100.0 / (0.2 * 1000.0)) * 3)
+    assert dt == min(acoustic, visc)
+    assert slabs.step_dt(slabs.LoopSpec(material=mat, h=0.013, eta=0.0, alpha=1.0, steps=1), 0.5, 0.0, 3) == \
+        0.6 * (0.013 / 40.5)
+    assert slabs.step_dt(slabs.LoopSpec(material=mat, h=0.013, eta=1.0, alpha=1.0, steps=1, fixed_dt=1e-5),
+                         9.0, 9.0, 3) == 1e-5
+
+
+def _gloo_toy_rank(rank, world, port, result_dir):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ranges = slabs.plan(np.ones(ToySlab.NCOL), world)
+        eng = ToySlab(*ranges[rank])
+        out = slabs.run_loop(slabs.DistGroup(eng, ranges, rank), slabs.LoopSpec(**TOY_SPEC), 3)
+        ids, vv = eng.owned()
+        np.save(os.path.join(result_dir, f"rank{rank}.npy"), np.concatenate([ids[:, None], vv], axis=1))
+        np.save(os.path.join(result_dir, f"out{rank}.npy"), np.array([out["t"], out["damped"], out["last_dt"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_toy_loop_equals_undivided(tmp_path, world):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_gloo_toy_rank, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    ref, out_ref = _toy_reference()
+    got = np.full_like(ref, np.nan)
+    for r in range(world):
+        a = np.load(tmp_path / f"rank{r}.npy")
+        got[a[:, 0].astype(np.int64)] = a[:, 1:]
+        o = np.load(tmp_path / f"out{r}.npy")
+        assert o[0] == out_ref["t"] and o[1] == out_ref["damped"] and o[2] == out_ref["last_dt"]
+    assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------- GPU: full step over device slabs
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,world,mode", [(2, 2, "ordered"), (2, 3, "fast"), (3, 2, "ordered"),
+                                            (3, 3, "fast")])
+def test_slab_loop_equals_undivided_device_loop(dim, world, mode):
+    """TL-SPH passes on owned particles + halo refreshes + decomposed random-choice sweeps
+    reproduce tlsph_dev_run on the undivided body bit for bit (elastic, gravity, clamped root)."""
+    from paper_2103_08932_b200 import dev, scenarios as S
+
+    mat = S.material()
+    r0, cons, v = body(dim, [40, 9] if dim == 2 else [24, 6, 5])
+    v = 0.05 * v
+    g = np.zeros_like(r0)
+    g[:, 1] = -9.81
+    eta = 0.2 * RHO * mat.c * H
+    steps, alpha, seed = 14, 0.5, 3
+    whole = dev.DeviceSystem(r0, DP ** dim, RHO, H, cons)
+    whole.set_reduction(mode)
+    whole.set("v", v)
+    whole.set("body", g)
+    whole.prepare(mat)
+    ref = whole.run(mat, eta=eta, alpha=alpha, steps=steps, seed=seed)
+    grid, parts = slabs.decompose(r0, H, world)
+    engines = []
+    for s in parts:
+        d = slabs.make_device_slab(grid, s, r0, DP ** dim, RHO, H, cons)
+        d.set_reduction(mode)
+        d.set("v", v[s.ids])
+        d.set("body", g[s.ids])
+        d.prepare(mat)
+        engines.append(slabs.DeviceSlabEngine(d, dim))
+    out = slabs.run_loop(slabs.LocalGroup(engines, [(s.x0, s.x1) for s in parts]),
+                         slabs.LoopSpec(mat, H, eta, alpha, steps, seed=seed), dim)
+    assert out["damped"] == ref["damped"] > 0 and out["t"] == ref["t"] and out["last_dt"] == ref["last_dt"]
+    cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
+    for name in ("v", "r", "F", "dFdt", "rho", "a"):
+        want = whole.get(name)
+        for s, e in zip(parts, engines):
+            own = (cols[s.ids] >= s.x0) & (cols[s.ids] < s.x1)
+            assert np.array_equal(e.d.get(name)[own], want[s.ids[own]]), name
