@@ -401,6 +401,19 @@ __device__ __forceinline__ M<D> second_pk(const M<D>& F, double J, const DMateri
 template <int D>
 __host__ __device__ constexpr int pbv_stride() { return D == 3 ? 10 : 6; }
 
+// Layout of DFields::pbv: component c of particle p. Chunk-major: the 16-byte chunk
+// (components 2k, 2k+1) of every particle is contiguous, so the momentum pass's gather of a
+// chunk for the 32 neighbours a warp holds touches few 128-byte lines (neighbour indices come
+// in runs); an 80-byte record per particle made every chunk load touch every record's line.
+template <int D>
+__host__ __device__ __forceinline__ long long pbv_at(long long n, long long p, int c) {
+#ifdef TLSPH_PBV_AOS
+  return p * pbv_stride<D>() + c;
+#else
+  return 2 * ((c >> 1) * n + p) + (c & 1);
+#endif
+}
+
 template <int D>
 __device__ __forceinline__ M<D> load_mat(double* const* arr, long long i) {
   M<D> m;

@@ -183,8 +183,8 @@ __global__ void k_gather_init(DFields f, const double* __restrict__ r0aos, const
   }
   const double vol = V0h[i], dens = rho0h[i];
 #pragma unroll
-  for (int k = 0; k < pbv_stride<D>(); ++k) f.pbv[s * pbv_stride<D>() + k] = 0.0;
-  f.pbv[s * pbv_stride<D>() + D * D] = vol;
+  for (int k = 0; k < pbv_stride<D>(); ++k) f.pbv[pbv_at<D>(f.n, s, k)] = 0.0;
+  f.pbv[pbv_at<D>(f.n, s, D * D)] = vol;
   f.V0[s] = vol;
   f.m[s] = dens * vol;  // particle_system.hpp:40
   f.rho0[s] = dens;

@@ -1003,8 +1003,10 @@ ColumnField column_field(const DevSystem& s, int field) {
     for (int d = 0; d < s.D; ++d) cf.ptr[d] = s.v[d].p;
   } else if (field == TLSPH_DEV_COLUMN_STRESS) {
     cf.ncomp = s.D * s.D + 1;  // P B0 row-major, V0 (the packed momentum-gather record)
-    cf.stride = s.D == 2 ? pbv_stride<2>() : pbv_stride<3>();
-    for (int c = 0; c < cf.ncomp; ++c) cf.ptr[c] = s.pbv.p + c;
+    // component c of particle p at pbv_at(n, p, c) = ptr[c] + p * stride
+    const auto at = [&](long long p, int c) { return s.D == 2 ? pbv_at<2>(s.n, p, c) : pbv_at<3>(s.n, p, c); };
+    cf.stride = at(1, 0) - at(0, 0);
+    for (int c = 0; c < cf.ncomp; ++c) cf.ptr[c] = s.pbv.p + at(0, c);
   } else {
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown column field " + std::to_string(field));
   }

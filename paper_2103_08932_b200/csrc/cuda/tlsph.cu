@@ -76,6 +76,13 @@ __global__ void k_correction_matrices(DFields f, DScalars* sc) {
 #ifndef TLSPH_TL_LBC
 #define TLSPH_TL_LBC 8
 #endif
+#ifndef TLSPH_TL_GB3
+#define TLSPH_TL_GB3 8
+#endif
+#ifndef TLSPH_TL_GC3
+#define TLSPH_TL_GC3 8
+#endif
+constexpr int kGB3 = TLSPH_TL_GB3, kGC3 = TLSPH_TL_GC3;  // lanes per particle in 3D, passes B and C
 #if TLSPH_TL_LBB > 0
 #define TL_BOUNDS_B __launch_bounds__(128, TLSPH_TL_LBB)
 #else
@@ -241,13 +248,19 @@ __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int 
     const M<D> S = second_pk<D>(F, J, mat);
     PB = matmul(matmul(F, S), load_mat<D>(f.B0, i));
   }
-  // packed record for the momentum gather: P B0 row-major, then V0 (common.cuh)
-  double* rec = f.pbv + i * pbv_stride<D>();
+  // packed record for the momentum gather: P B0 row-major, then V0, 16-byte chunks (common.cuh)
+  constexpr int W = pbv_stride<D>();
+  double rec[W];
 #pragma unroll
   for (int r = 0; r < D; ++r)
 #pragma unroll
     for (int q = 0; q < D; ++q) rec[r * D + q] = PB.c[r][q];
   rec[D * D] = f.V0[i];
+#pragma unroll
+  for (int c = D * D + 1; c < W; ++c) rec[c] = 0.0;
+#pragma unroll
+  for (int k = 0; k < W / 2; ++k)
+    *reinterpret_cast<double2*>(f.pbv + pbv_at<D>(f.n, i, 2 * k)) = make_double2(rec[2 * k], rec[2 * k + 1]);
 }
 
 // ------------------------------------------------------------------ momentum RHS (integrator.cpp:105-115)
@@ -267,10 +280,9 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
     constexpr int W = pbv_stride<D>();
     double pbi[W];
     {
-      const double2* ri = reinterpret_cast<const double2*>(f.pbv + i * W);
 #pragma unroll
       for (int k = 0; k < W / 2; ++k) {
-        const double2 x = ri[k];
+        const double2 x = *reinterpret_cast<const double2*>(f.pbv + pbv_at<D>(f.n, i, 2 * k));
         pbi[2 * k] = x.x;
         pbi[2 * k + 1] = x.y;
       }
@@ -293,10 +305,9 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
         if (u > 0 && s + u * G >= hi) break;
         // P B0 and V0 of j in W/2 16-byte loads from one packed record
         double pbj[W];
-        const double2* rj = reinterpret_cast<const double2*>(f.pbv + static_cast<long long>(j[u]) * W);
 #pragma unroll
         for (int k = 0; k < W / 2; ++k) {
-          const double2 x = __ldg(rj + k);
+          const double2 x = __ldg(reinterpret_cast<const double2*>(f.pbv + pbv_at<D>(f.n, j[u], 2 * k)));
           pbj[2 * k] = x.x;
           pbj[2 * k + 1] = x.y;
         }
@@ -440,7 +451,7 @@ void DevSystem::deformation_rate() {
     else k_deformation_rate<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   } else {
     if (ord) k_deformation_rate_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
-    else k_deformation_rate<3, 8, false><<<grid_for(n * 8, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    else k_deformation_rate<3, kGC3, false><<<grid_for(n * kGC3, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   }
   CK_LAUNCH("k_deformation_rate");
   sync();
@@ -468,7 +479,7 @@ void DevSystem::momentum_rhs(const DMaterial& mat) {
     else k_momentum<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   } else {
     if (ord) k_momentum_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
-    else k_momentum<3, 8, false><<<grid_for(n * 8, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    else k_momentum<3, kGB3, false><<<grid_for(n * kGB3, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   }
   CK_LAUNCH("k_momentum");
   sync();
@@ -489,9 +500,9 @@ void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop
   } else {
     if (pass == 0) k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
     else if (pass == 1 && ord) k_momentum_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    else if (pass == 1) k_momentum<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1) k_momentum<3, kGB3, true><<<grid_for(n * kGB3, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
     else if (ord) k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    else k_deformation_rate<3, 8, true><<<grid_for(n * 8, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else k_deformation_rate<3, kGC3, true><<<grid_for(n * kGC3, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
   }
 }
 
