@@ -154,6 +154,19 @@ tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const do
 tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host);
 tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode);
 
+/* Where the FAST particle-split sweep keeps a cell's slot block (pair factors,
+ * stencil indices) while its chain runs: staged in shared memory (four cells
+ * per SM; the latency-bound form for colours of up to ~600 cells) or streamed
+ * from L2 (a tile of stencil velocities only, 12-16 cells per SM; the
+ * throughput form for large bodies). AUTO picks by the colour's cell count.
+ * Results are identical in every mode. */
+typedef enum tlsph_dev_sweep_tiling {
+  TLSPH_SWEEP_TILING_AUTO = 0,
+  TLSPH_SWEEP_TILING_STAGED = 1,
+  TLSPH_SWEEP_TILING_STREAMED = 2
+} tlsph_dev_sweep_tiling;
+tlsph_status tlsph_dev_set_sweep_tiling(tlsph_dev* dev, tlsph_dev_sweep_tiling mode);
+
 /* Penalty contact plane of ExternalAccel<D> (forces.hpp:13-39): a_i +=
  * stiffness * max(0, -(r_i - point).normal) / m_i * normal, evaluated at the
  * current position inside the momentum RHS. stiffness <= 0 removes it. */

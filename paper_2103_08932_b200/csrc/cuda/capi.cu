@@ -263,6 +263,14 @@ tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode) {
   });
 }
 
+tlsph_status tlsph_dev_set_sweep_tiling(tlsph_dev* dev, tlsph_dev_sweep_tiling mode) {
+  return guarded([&] {
+    if (mode != TLSPH_SWEEP_TILING_AUTO && mode != TLSPH_SWEEP_TILING_STAGED && mode != TLSPH_SWEEP_TILING_STREAMED)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown sweep tiling");
+    sys(dev).sweep_tiling = mode;
+  });
+}
+
 tlsph_status tlsph_dev_grid_info(const tlsph_dev* dev, int* dims, double* origin, double* cell_size,
                                  int64_t* n_cells) {
   return guarded([&] {

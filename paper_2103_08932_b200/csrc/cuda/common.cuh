@@ -101,6 +101,10 @@ struct DFields {
   double* m;
   double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
   double* qf;     // per slot: pair_factor * RN(1/m_j), 0 for clamped j (FAST sweep)
+  // uniform masses (every m equal): RN(1/m), and per slot the stencil index with bit 15 set for
+  // a clamped j (the streamed FAST sweep forms qf = pf * minv_uniform from them); null otherwise
+  const uint16_t* nlocf;
+  double minv_uniform;
   // x-slab peers (slabs.py): per particle of a column shared with a neighbouring slab, the
   // particle's index in that slab's arrays (-1: not shared; >= 0: right peer; <= -2: left
   // peer at -2 - index); the peers' velocity arrays (device memory reachable from here)

@@ -375,6 +375,18 @@ __global__ void k_qf(const double* __restrict__ pf, const int* __restrict__ nbr,
   qf[s] = y > 0.0 ? pf[s] * y : 0.0;
 }
 
+__global__ void k_mass_differs(const double* __restrict__ m, long long n, int* __restrict__ differs) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && m[i] != m[0]) atomicOr(differs, 1);
+}
+
+__global__ void k_nlocf(const uint16_t* __restrict__ nloc, const int* __restrict__ nbr,
+                        const uint8_t* __restrict__ flag, uint16_t* __restrict__ nlocf, long long nslots) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nslots) return;
+  nlocf[s] = static_cast<uint16_t>(nloc[s] | (flag[nbr[s]] ? 0x8000u : 0u));
+}
+
 __global__ void k_pf_sums(DFields f) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= f.n) return;
@@ -577,6 +589,8 @@ DFields DevSystem::fields() const {
   }
   f.pfsq = pf_sq.p;
   f.nloc = nloc.p;
+  f.nlocf = uniform_mass ? nlocf.p : nullptr;
+  f.minv_uniform = minv_uniform;
   f.cell_start = cell_start.p;
   f.cell = cutoff;
   f.has_body = has_body ? 1 : 0;
@@ -778,6 +792,27 @@ void DevSystem::refresh_minvf() {
     qf.alloc(static_cast<size_t>(nslots));
     k_qf<<<grid_for(nslots, 256), 256, 0, stream>>>(pf.p, nbr.p, minvf.p, qf.p, nslots);
     CK_LAUNCH("k_qf");
+  }
+  // uniform masses: the streamed FAST sweep needs no per-slot or per-stencil mass data
+  uniform_mass = false;
+  if (n > 0 && nslots > 0 && nloc.p && stencil_ok) {
+    DBuf<int> differs_d;
+    differs_d.alloc(1);
+    CK(cudaMemsetAsync(differs_d.p, 0, sizeof(int), stream));
+    k_mass_differs<<<grid_for(n, 256), 256, 0, stream>>>(m.p, n, differs_d.p);
+    CK_LAUNCH("k_mass_differs");
+    int differs = 1;
+    double m0 = 0.0;
+    CK(cudaMemcpyAsync(&differs, differs_d.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(&m0, m.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (!differs && m0 > 0.0) {
+      uniform_mass = true;
+      minv_uniform = 1.0 / m0;  // k_minvf's RN(1/m)
+      nlocf.alloc(static_cast<size_t>(nslots));
+      k_nlocf<<<grid_for(nslots, 256), 256, 0, stream>>>(nloc.p, nbr.p, flag.p, nlocf.p, nslots);
+      CK_LAUNCH("k_nlocf");
+    }
   }
   fold_valid = false;  // constrained particles are marked in the fold constants
 }

@@ -47,6 +47,7 @@
 //   FAST:    x * y (<= 1 ulp), within the 1e-10 north_star class.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "stencil_tile.cuh"
 #include "sweep_chain.cuh"
@@ -67,7 +68,7 @@ struct Phase {
   int SC;          // max slots per cell, multiple of 8
   int MC;          // max particles per cell, even
   int MR;          // per-warp scratch (max slots per particle): pairwise k, ORDERED residual terms
-  int fast;        // FAST particle-split tile: no masses, per-slot mass factors instead
+  int fast;        // FAST particle-split tile: 1 no masses, per-slot mass factors instead; 2 (streamed) stencil 1/m
   double eta;
   double dt;       // used when dt_from_scalars == 0
   int dt_from_scalars;
@@ -101,7 +102,7 @@ constexpr int kHeader = 16 + 16 * 9;  // barrier + spare word + segment table
 template <int D>
 __host__ __device__ inline size_t tile_bytes(int S, int SC, int MC, int MR, int fast) {
   size_t b = kHeader;
-  b += sizeof(double) * (static_cast<size_t>(fast ? D : D + 2) * S);
+  b += sizeof(double) * (static_cast<size_t>(fast == 1 ? D : fast == 2 ? D + 1 : D + 2) * S);
   b += sizeof(long long) * static_cast<size_t>(mco(MC));
   b += sizeof(double) * static_cast<size_t>(3 * mco(MC));
   b += sizeof(double) * static_cast<size_t>(SC + 2) * (fast ? 2 : 1);
@@ -124,10 +125,14 @@ __device__ inline Tile<D> carve(unsigned char* base, const Phase& ph) {
 #pragma unroll
   for (int k = 0; k < D; ++k) t.sv[k] = d + static_cast<size_t>(k) * ph.S;
   double* after_v = d + static_cast<size_t>(D) * ph.S;
-  if (ph.fast) {
+  if (ph.fast == 1) {
     t.sm = nullptr;
     t.smf = nullptr;
     t.soff = reinterpret_cast<long long*>(after_v);
+  } else if (ph.fast == 2) {  // streamed FAST: stencil 1/m instead of per-slot mass factors
+    t.sm = nullptr;
+    t.smf = after_v;
+    t.soff = reinterpret_cast<long long*>(t.smf + ph.S);
   } else {
     t.sm = after_v;
     t.smf = t.sm + ph.S;
@@ -137,8 +142,8 @@ __device__ inline Tile<D> carve(unsigned char* base, const Phase& ph) {
   t.sden = t.sdiag + mc;
   t.sy = t.sden + mc;
   t.spf = t.sy + mc;
-  t.sqf = ph.fast ? t.spf + ph.SC + 2 : nullptr;
-  t.skf = (ph.fast ? t.sqf : t.spf) + ph.SC + 2;
+  t.sqf = ph.fast == 1 ? t.spf + ph.SC + 2 : nullptr;
+  t.skf = (ph.fast == 1 ? t.sqf : t.spf) + ph.SC + 2;
   t.snl = reinterpret_cast<uint16_t*>(t.skf + static_cast<size_t>(D) * ph.MR);
   return t;
 }
@@ -236,9 +241,10 @@ struct CellSpan {
 // the flattened row table, the cell's slot block, row offsets and fold
 // constants by bulk copies on the mbarrier. MASS: also stage m (ORDERED
 // divisions, pairwise).
-template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false>
+template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true>
 __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
-                                              long long sstart, long long send, int lane) {
+                                              long long sstart, long long send, int lane,
+                                              const uint16_t* nl_src = nullptr) {
   constexpr int kSegs = seg_count<D>();
   const int slen = static_cast<int>(send - sstart);
   const int par = static_cast<int>(sstart & 1);
@@ -257,10 +263,10 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   }
   uint32_t mybytes = 0;
   if (lane == 0) mybytes = static_cast<uint32_t>((cs.o1() - cs.o0()) * 8);
-  else if (lane == 1) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
-  else if (lane == 2) mybytes = static_cast<uint32_t>((cs.n1() - cs.n0()) * 2);
+  else if (SLOTS && lane == 1) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
+  else if (SLOTS && lane == 2) mybytes = static_cast<uint32_t>((cs.n1() - cs.n0()) * 2);
   else if (FOLD && lane == 3) mybytes = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8 * 3);
-  else if (QF && lane == 4) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
+  else if (SLOTS && QF && lane == 4) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
   uint32_t total = mybytes;
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
@@ -273,17 +279,22 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   stamp(blockIdx.x, 9);
   if (lane == 0) {
     tma_load_1d(t.soff, f.offs + cs.o0(), mybytes, t.bar);
-  } else if (lane == 1) {
+  } else if (SLOTS && lane == 1) {
     tma_load_1d(t.spf, f.pf + cs.f0(), mybytes, t.bar);
-  } else if (lane == 2) {
+  } else if (SLOTS && lane == 2) {
     tma_load_1d(t.snl, f.nloc + cs.n0(), mybytes, t.bar);
   } else if (FOLD && lane == 3) {
     const uint32_t nb = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8);
     tma_load_1d(t.sdiag, f.fdiag + cs.q0(), nb, t.bar);
     tma_load_1d(t.sden, f.fden + cs.q0(), nb, t.bar);
     tma_load_1d(t.sy, f.fy + cs.q0(), nb, t.bar);
-  } else if (QF && lane == 4) {
+  } else if (SLOTS && QF && lane == 4) {
     tma_load_1d(t.sqf, f.qf + cs.f0(), mybytes, t.bar);
+  }
+  if (!SLOTS) {  // streamed slot block: bring it into L2 ahead of the chain's register loads
+    if (lane == 1) tma_prefetch_l2(f.pf + cs.f0(), static_cast<uint32_t>((cs.f1() - cs.f0()) * 8));
+    else if (lane == 2)
+      tma_prefetch_l2((nl_src ? nl_src : f.nloc) + cs.n0(), static_cast<uint32_t>((cs.n1() - cs.n0()) * 2));
   }
   stamp(blockIdx.x, 3);
   const RowPairs rp = row_pairs(sstart, lane < kSegs ? slen : 0, sbase, lane);
@@ -652,7 +663,13 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 // The whole chain of a cell in one warp (sweep_chain.cuh): every slot's
 // metadata is read once for all D components and the D residuals share one
 // shuffle tree.
-template <int D, int K>
+// STREAM: the slot block is not staged; the chain reads pair factors, mass
+// factors and stencil indices from global memory (L2), a particle ahead. The
+// tile shrinks to the stencil velocities and per-particle constants, so many
+// more cells share an SM -- the form for colours with more cells than one
+// wave of staged tiles holds (large bodies).
+// UNI (with STREAM, uniform masses): no stencil 1/m staged (fast_chain_stream).
+template <int D, int K, bool STREAM, bool UNI>
 __global__ void __launch_bounds__(kWarp)
 k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   if (ph.dt_from_scalars && sc->halt) return;
@@ -672,7 +689,8 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   locate_row<D>(f, c, lane, sstart, send);
   if (cs.p0 == cs.p1) return;
   stamp(blockIdx.x, 2);
-  issue_staging<D, true, false, true, true>(f, t, cs, sstart, send, lane);
+  issue_staging<D, true, false, true, !STREAM || UNI, !STREAM>(f, t, cs, sstart, send, lane,
+                                                                UNI ? f.nlocf : f.nloc);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
@@ -680,9 +698,17 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   ChainTile<D> ct;
 #pragma unroll
   for (int d = 0; d < D; ++d) ct.sv[d] = t.sv[d];
-  ct.pf = t.spf + (cs.s0 - cs.f0());
-  ct.qf = t.sqf + (cs.s0 - cs.f0());
-  ct.nl = t.snl + (cs.s0 - cs.n0());
+  ct.smf = t.smf;
+  if (STREAM) {
+    ct.pf = f.pf + cs.s0;
+    ct.qf = nullptr;  // formed from 1/m (fast_chain_stream)
+    ct.nl = (UNI ? f.nlocf : f.nloc) + cs.s0;
+    ct.minv = f.minv_uniform;
+  } else {
+    ct.pf = t.spf + (cs.s0 - cs.f0());
+    ct.qf = t.sqf + (cs.s0 - cs.f0());
+    ct.nl = t.snl + (cs.s0 - cs.n0());
+  }
   ct.offs = t.soff + (cs.p0 - cs.o0());
   ct.s0 = cs.s0;
   ct.diag = t.sdiag + (cs.p0 - cs.q0());
@@ -691,7 +717,8 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   ct.np = static_cast<int>(cs.p1 - cs.p0);
   ct.forward = ph.forward;
   ct.kb = kb;
-  fast_chain<D, K>(ct, lane);
+  if (STREAM) fast_chain_stream<D, K, UNI>(ct, lane);
+  else fast_chain<D, K>(ct, lane);
   __syncwarp();
   stamp(blockIdx.x, 6);
 
@@ -703,12 +730,57 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 #endif
 }
 
-template <int D, int K>
-void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
-  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
+// Staged or streamed slot block (tlsph_dev_set_sweep_tiling); AUTO: streamed
+// when the colour's cells exceed one wave of staged tiles
+// (TLSPH_SWEEP_STREAM=0/1 overrides AUTO, for A/B runs).
+inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_bytes) {
+  if (s.sweep_tiling != TLSPH_SWEEP_TILING_AUTO) return s.sweep_tiling == TLSPH_SWEEP_TILING_STREAMED;
+  static const int force = [] {
+    const char* e = std::getenv("TLSPH_SWEEP_STREAM");
+    return e && *e ? std::atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long per_sm = std::max<long long>(1, static_cast<long long>((228 * 1024) / (staged_bytes + 1024)));
+  return ph.ncol > per_sm * sms;
+}
+
+inline bool uniform_disabled() {  // TLSPH_SWEEP_UNIFORM=0: the stencil-1/m form even for uniform masses (A/B)
+  static const bool off = [] {
+    const char* e = std::getenv("TLSPH_SWEEP_UNIFORM");
+    return e && *e == '0';
+  }();
+  return off;
+}
+
+template <int D, int K, bool STREAM, bool UNI = false>
+void launch_fast_impl(const DevSystem& s, const DFields& f, Phase ph) {
+  if (STREAM) {
+    ph.SC = 0;  // no slot block in the tile
+    ph.fast = UNI ? 1 : 2;  // stencil velocities only, or with the stencil's 1/m
+  }
+  size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
+  {
+    // Spread a colour that fits in one wave over every SM: the CTA scheduler fills
+    // an SM up to its resident limit, so a small tile would pack the cells onto
+    // fewer SMs (more chains per scheduler, idle SMs). Pad the tile so at most
+    // ceil(cells / SMs) are resident per SM.
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long per_sm = (ph.ncol + sms - 1) / sms;
+    constexpr size_t kSmemSM = 228 * 1024, kReserve = 1024;
+    if (per_sm >= 1 && per_sm < 32) {
+      const size_t cap = (kSmemSM / static_cast<size_t>(per_sm) - kReserve) & ~static_cast<size_t>(127);
+      if (cap > smem && static_cast<size_t>(per_sm) * (smem + kReserve) <= kSmemSM) smem = std::min<size_t>(cap, 200 * 1024);
+    }
+  }
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    CK(cudaFuncSetAttribute(k_sweep_fast<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(cudaFuncSetAttribute(k_sweep_fast<D, K, STREAM, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
     configured = smem;
   }
   // programmatic dependent launch: the phase's CTAs may start (and stage their
@@ -724,7 +796,14 @@ void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_sweep_fast<D, K>, f, ph, s.scal.p));
+  CK(cudaLaunchKernelEx(&cfg, k_sweep_fast<D, K, STREAM, UNI>, f, ph, s.scal.p));
+}
+
+template <int D, int K>
+void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
+  if (!stream_slots(s, ph, tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast))) launch_fast_impl<D, K, false>(s, f, ph);
+  else if (f.nlocf && !uniform_disabled()) launch_fast_impl<D, K, true, true>(s, f, ph);
+  else launch_fast_impl<D, K, true, false>(s, f, ph);
 }
 
 template <int D, int SCHEME, bool ORDERED, int K>

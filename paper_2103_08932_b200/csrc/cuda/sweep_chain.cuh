@@ -29,6 +29,8 @@ struct ChainTile {
   const double* pf;       // the cell's pair factors, cell-relative slot index
   const double* qf;       // pair_factor / m_j per slot (0: clamped j, never written)
   const uint16_t* nl;     // the cell's stencil-local neighbour indices
+  const double* smf;      // fast_chain_stream: staged stencil signed RN(1/m) (negative: clamped)
+  double minv;            // fast_chain_stream<UNI>: the uniform RN(1/m); nl carries bit 15 = clamped j
   const long long* offs;  // offs[p] - s0 = cell-relative first slot of particle p
   long long s0;
   const double* diag;     // per-particle fold constants (NaN: constrained particle)
@@ -187,6 +189,145 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     pk1 = pk2;
     lo1 = lo2;
     cnt1 = cnt2;
+  }
+}
+
+// The same chain with the slot block streamed from global memory (L2) instead
+// of shared memory (k_sweep_fast<STREAM>): neighbour indices and pair factors
+// are loaded two particles ahead, and the per-slot mass factor is formed as
+// pair_factor * RN(1/m_j) from the staged stencil -- exactly the stored qf
+// (state.cu k_qf), so the arithmetic is that of fast_chain. UNI (uniform
+// masses): no stencil 1/m either; the factor is pair_factor * RN(1/m) unless
+// bit 15 of the slot's stencil index marks a clamped j.
+template <int D, int K, bool UNI>
+__device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lane) {
+  const int np = t.np;
+  auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
+  auto row = [&](int p, int& lo, int& cnt) {
+    lo = static_cast<int>(t.offs[p] - t.s0);
+    cnt = static_cast<int>(t.offs[p + 1] - t.s0) - lo;
+  };
+  // raw loads; UNI: j keeps bit 15 (clamped j) until mass_factors / coefficients strip it
+  auto load_raw = [&](int lo, int cnt, int li, int (&j)[K], double (&pf)[K]) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const int s = lane + u * 32;
+      const bool v = s < cnt;
+      j[u] = v ? static_cast<int>(t.nl[lo + s]) : li;  // invalid lanes read i itself with b = 0
+      pf[u] = v ? t.pf[lo + s] : 0.0;
+    }
+  };
+  auto mass_factors = [&](const int (&j)[K], const double (&pf)[K], double (&q)[K]) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      if (UNI) {
+        q[u] = (j[u] & 0x8000) ? 0.0 : pf[u] * t.minv;
+      } else {
+        const double my = t.smf[j[u]];
+        q[u] = my > 0.0 ? pf[u] * my : 0.0;  // clamped j: never written (damping.cpp:84-86)
+      }
+    }
+  };
+
+  int jq[K];
+  double bq[K], bmq[K], c1[K], cq[K];
+  unsigned upm;
+  bool skip;
+  double diag, y;
+  auto coefficients = [&](const int (&j)[K], const double (&pf)[K], const double (&q)[K], int cnt) {
+    skip = diag != diag || cnt == 0;
+    upm = 0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      jq[u] = UNI ? (j[u] & 0x7fff) : j[u];
+      bq[u] = t.kb * pf[u];
+      bmq[u] = t.kb * q[u];
+      c1[u] = 1.0 + bmq[u];
+      cq[u] = -bmq[u] * (diag + bq[u]);
+      upm |= q[u] != 0.0 ? (1u << u) : 0u;
+    }
+    if (skip) upm = 0;
+  };
+
+  // particle 0: coefficients; particle 1: raw loads in flight; particle 2: row extents
+  int pk = pidx(0);
+  const int pk1i = np > 1 ? pidx(1) : pk;
+  int pk1 = pk1i, pk2 = np > 2 ? pidx(2) : pk1i;
+  int jn[K], lo1, cnt1, lo2, cnt2;
+  double pfn[K];
+  row(pk1, lo1, cnt1);
+  row(pk2, lo2, cnt2);
+  load_raw(lo1, cnt1, t.lbase + pk1, jn, pfn);
+  {
+    int lo, cnt, j0[K];
+    double pf0[K], q0[K];
+    row(pk, lo, cnt);
+    load_raw(lo, cnt, t.lbase + pk, j0, pf0);
+    diag = t.diag[pk];
+    y = t.y[pk];
+    mass_factors(j0, pf0, q0);
+    coefficients(j0, pf0, q0, cnt);
+  }
+
+  for (int kk = 0; kk < np; ++kk) {
+    const int li = t.lbase + pk;
+    // particle kk+2: raw loads (two iterations of latency cover)
+    int jn2[K];
+    double pfn2[K];
+    load_raw(lo2, cnt2, t.lbase + pk2, jn2, pfn2);
+    const int pk3 = kk + 3 < np ? pidx(kk + 3) : pk2;
+    int lo3, cnt3;
+    row(pk3, lo3, cnt3);
+
+    // the chain: gathers
+    double vi[D], vq[K][D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) vi[d] = t.sv[d][li];
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int d = 0; d < D; ++d) vq[u][d] = t.sv[d][jq[u]];
+    const double diag1 = t.diag[pk1], y1 = t.y[pk1];
+
+    double P[D], Y[K][D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      P[d] = bq[0] * (vq[0][d] - vi[d]);
+#pragma unroll
+      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], vq[u][d] - vi[d], P[d]);
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(c1[u], vq[u][d], -bmq[u] * vi[d]);
+    warp_sum_vec<D>(P, lane);
+    double qfn[K];
+    mass_factors(jn, pfn, qfn);  // particle kk+1 (loaded an iteration ago)
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double rate = P[d] * y;
+#pragma unroll
+      for (int u = 0; u < K; ++u)
+        if (upm & (1u << u)) t.sv[d][jq[u]] = __fma_rn(cq[u], rate, Y[u][d]);
+      // i is not its own neighbour, so this store cannot race the scatter above
+      if (lane == 0 && !skip) t.sv[d][li] = __fma_rn(diag, rate, vi[d]);
+    }
+    __syncwarp();
+
+    diag = diag1;
+    y = y1;
+    coefficients(jn, pfn, qfn, cnt1);
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      jn[u] = jn2[u];
+      pfn[u] = pfn2[u];
+    }
+    pk = pk1;
+    pk1 = pk2;
+    pk2 = pk3;
+    cnt1 = cnt2;
+    lo2 = lo3;
+    cnt2 = cnt3;
   }
 }
 

@@ -51,6 +51,7 @@ class DevSystem {
   double cutoff = 0.0;
   cudaStream_t stream = nullptr;
   tlsph_dev_reduction reduction = TLSPH_REDUCTION_FAST;
+  tlsph_dev_sweep_tiling sweep_tiling = TLSPH_SWEEP_TILING_AUTO;
 
   // grid
   int dims[3] = {1, 1, 1};
@@ -110,6 +111,9 @@ class DevSystem {
   DBuf<double> qf;  // pf * RN(1/m_j), 0 for clamped j: the FAST sweep's per-slot mass factor
   DBuf<double> pf_sum, pf_sq;  // per-particle sums of pf and pf^2 (static)
   DBuf<uint16_t> nloc;
+  DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)
+  bool uniform_mass = false;  // every particle has the same mass
+  double minv_uniform = 0.0;  // RN(1/m) then
 
   // scratch
   DBuf<DScalars> scal;

@@ -126,6 +126,7 @@ def lib():
     L.tlsph_dev_set_field.argtypes = [P, I, D]
     L.tlsph_dev_get_field.argtypes = [P, I, D]
     L.tlsph_dev_set_reduction.argtypes = [P, I]
+    L.tlsph_dev_set_sweep_tiling.argtypes = [P, I]
     L.tlsph_dev_grid_info.argtypes = [P, C.POINTER(I), D, D, C.POINTER(C.c_int64)]
     L.tlsph_dev_grid_cells.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.tlsph_dev_get_neighborhood.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D, D, D, D]
@@ -238,6 +239,10 @@ class DeviceSystem:
 
     def set_reduction(self, mode):
         _check(lib().tlsph_dev_set_reduction(self._h, {"fast": 0, "ordered": 1}[mode]))
+
+    def set_sweep_tiling(self, mode):
+        """FAST sweep slot-block placement: "auto", "staged" (shared memory) or "streamed" (L2)."""
+        _check(lib().tlsph_dev_set_sweep_tiling(self._h, {"auto": 0, "staged": 1, "streamed": 2}[mode]))
 
     # ---- fields
     def _shape(self, name):
