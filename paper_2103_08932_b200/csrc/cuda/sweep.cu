@@ -68,7 +68,8 @@ struct Phase {
   int SC;          // max slots per cell, multiple of 8
   int MC;          // max particles per cell, even
   int MR;          // per-warp scratch (max slots per particle): pairwise k, ORDERED residual terms
-  int fast;        // FAST particle-split tile: 1 no masses, per-slot mass factors instead; 2 (streamed) stencil 1/m
+  int fast;        // FAST particle-split tile: 1 no masses, per-slot mass factors instead; 2 (streamed) stencil 1/m;
+                   // 3 uniform masses, neither (slot clamp bit)
   double eta;
   double dt;       // used when dt_from_scalars == 0
   int dt_from_scalars;
@@ -102,10 +103,10 @@ constexpr int kHeader = 16 + 16 * 9;  // barrier + spare word + segment table
 template <int D>
 __host__ __device__ inline size_t tile_bytes(int S, int SC, int MC, int MR, int fast) {
   size_t b = kHeader;
-  b += sizeof(double) * (static_cast<size_t>(fast == 1 ? D : fast == 2 ? D + 1 : D + 2) * S);
+  b += sizeof(double) * (static_cast<size_t>(fast == 1 || fast == 3 ? D : fast == 2 ? D + 1 : D + 2) * S);
   b += sizeof(long long) * static_cast<size_t>(mco(MC));
   b += sizeof(double) * static_cast<size_t>(3 * mco(MC));
-  b += sizeof(double) * static_cast<size_t>(SC + 2) * (fast ? 2 : 1);
+  b += sizeof(double) * static_cast<size_t>(SC + 2) * (fast == 1 ? 2 : 1);
   b += sizeof(double) * static_cast<size_t>(D * MR);
   b += sizeof(uint16_t) * static_cast<size_t>(SC + 16);
   return (b + 15) & ~static_cast<size_t>(15);
@@ -125,7 +126,7 @@ __device__ inline Tile<D> carve(unsigned char* base, const Phase& ph) {
 #pragma unroll
   for (int k = 0; k < D; ++k) t.sv[k] = d + static_cast<size_t>(k) * ph.S;
   double* after_v = d + static_cast<size_t>(D) * ph.S;
-  if (ph.fast == 1) {
+  if (ph.fast == 1 || ph.fast == 3) {  // 3: staged, uniform masses (no per-slot mass factors)
     t.sm = nullptr;
     t.smf = nullptr;
     t.soff = reinterpret_cast<long long*>(after_v);
@@ -241,7 +242,7 @@ struct CellSpan {
 // the flattened row table, the cell's slot block, row offsets and fold
 // constants by bulk copies on the mbarrier. MASS: also stage m (ORDERED
 // divisions, pairwise).
-template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true>
+template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true, bool UNI = false>
 __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
                                               long long sstart, long long send, int lane,
                                               const uint16_t* nl_src = nullptr) {
@@ -266,7 +267,7 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   else if (SLOTS && lane == 1) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
   else if (SLOTS && lane == 2) mybytes = static_cast<uint32_t>((cs.n1() - cs.n0()) * 2);
   else if (FOLD && lane == 3) mybytes = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8 * 3);
-  else if (SLOTS && QF && lane == 4) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
+  else if (SLOTS && QF && !UNI && lane == 4) mybytes = static_cast<uint32_t>((cs.f1() - cs.f0()) * 8);
   uint32_t total = mybytes;
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
@@ -282,13 +283,13 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   } else if (SLOTS && lane == 1) {
     tma_load_1d(t.spf, f.pf + cs.f0(), mybytes, t.bar);
   } else if (SLOTS && lane == 2) {
-    tma_load_1d(t.snl, f.nloc + cs.n0(), mybytes, t.bar);
+    tma_load_1d(t.snl, (nl_src ? nl_src : f.nloc) + cs.n0(), mybytes, t.bar);
   } else if (FOLD && lane == 3) {
     const uint32_t nb = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8);
     tma_load_1d(t.sdiag, f.fdiag + cs.q0(), nb, t.bar);
     tma_load_1d(t.sden, f.fden + cs.q0(), nb, t.bar);
     tma_load_1d(t.sy, f.fy + cs.q0(), nb, t.bar);
-  } else if (SLOTS && QF && lane == 4) {
+  } else if (SLOTS && QF && !UNI && lane == 4) {
     tma_load_1d(t.sqf, f.qf + cs.f0(), mybytes, t.bar);
   }
   if (!SLOTS) {  // streamed slot block: bring it into L2 ahead of the chain's register loads
@@ -689,8 +690,8 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   locate_row<D>(f, c, lane, sstart, send);
   if (cs.p0 == cs.p1) return;
   stamp(blockIdx.x, 2);
-  issue_staging<D, true, false, true, !STREAM || UNI, !STREAM>(f, t, cs, sstart, send, lane,
-                                                                UNI ? f.nlocf : f.nloc);
+  issue_staging<D, true, false, true, !STREAM || UNI, !STREAM, UNI>(f, t, cs, sstart, send, lane,
+                                                                     UNI ? f.nlocf : f.nloc);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
@@ -706,8 +707,9 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
     ct.minv = f.minv_uniform;
   } else {
     ct.pf = t.spf + (cs.s0 - cs.f0());
-    ct.qf = t.sqf + (cs.s0 - cs.f0());
+    ct.qf = UNI ? nullptr : t.sqf + (cs.s0 - cs.f0());
     ct.nl = t.snl + (cs.s0 - cs.n0());
+    ct.minv = f.minv_uniform;
   }
   ct.offs = t.soff + (cs.p0 - cs.o0());
   ct.s0 = cs.s0;
@@ -718,7 +720,7 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   ct.forward = ph.forward;
   ct.kb = kb;
   if (STREAM) fast_chain_stream<D, K, UNI>(ct, lane);
-  else fast_chain<D, K>(ct, lane);
+  else fast_chain<D, K, true, true, UNI>(ct, lane);
   __syncwarp();
   stamp(blockIdx.x, 6);
 
@@ -760,6 +762,8 @@ void launch_fast_impl(const DevSystem& s, const DFields& f, Phase ph) {
   if (STREAM) {
     ph.SC = 0;  // no slot block in the tile
     ph.fast = UNI ? 1 : 2;  // stencil velocities only, or with the stencil's 1/m
+  } else if (UNI) {
+    ph.fast = 3;  // slot block without per-slot mass factors
   }
   size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
   {
@@ -772,9 +776,14 @@ void launch_fast_impl(const DevSystem& s, const DFields& f, Phase ph) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long per_sm = (ph.ncol + sms - 1) / sms;
     constexpr size_t kSmemSM = 228 * 1024, kReserve = 1024;
-    if (per_sm >= 1 && per_sm < 32) {
-      const size_t cap = (kSmemSM / static_cast<size_t>(per_sm) - kReserve) & ~static_cast<size_t>(127);
-      if (cap > smem && static_cast<size_t>(per_sm) * (smem + kReserve) <= kSmemSM) smem = std::min<size_t>(cap, 200 * 1024);
+    static const int pad_mode = [] {  // TLSPH_SWEEP_PAD=0: no padding; =2: room for two phases (A/B runs)
+      const char* e = std::getenv("TLSPH_SWEEP_PAD");
+      return e && *e ? std::atoi(e) : 1;
+    }();
+    if (pad_mode && per_sm >= 1 && per_sm * pad_mode < 32) {
+      const long long ps = per_sm * pad_mode;
+      const size_t cap = (kSmemSM / static_cast<size_t>(ps) - kReserve) & ~static_cast<size_t>(127);
+      if (cap > smem && static_cast<size_t>(ps) * (smem + kReserve) <= kSmemSM) smem = std::min<size_t>(cap, 200 * 1024);
     }
   }
   static size_t configured = 0;
@@ -801,8 +810,11 @@ void launch_fast_impl(const DevSystem& s, const DFields& f, Phase ph) {
 
 template <int D, int K>
 void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
-  if (!stream_slots(s, ph, tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast))) launch_fast_impl<D, K, false>(s, f, ph);
-  else if (f.nlocf && !uniform_disabled()) launch_fast_impl<D, K, true, true>(s, f, ph);
+  const bool uni = f.nlocf && !uniform_disabled();
+  if (!stream_slots(s, ph, tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, uni ? 3 : ph.fast))) {
+    if (uni) launch_fast_impl<D, K, false, true>(s, f, ph);
+    else launch_fast_impl<D, K, false, false>(s, f, ph);
+  } else if (f.nlocf && !uniform_disabled()) launch_fast_impl<D, K, true, true>(s, f, ph);
   else launch_fast_impl<D, K, true, false>(s, f, ph);
 }
 

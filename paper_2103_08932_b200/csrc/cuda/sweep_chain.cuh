@@ -71,7 +71,9 @@ __device__ __forceinline__ void warp_sum_vec(double (&x)[D], int lane) {
   for (int d = 0; d < D; ++d) x[d] = __shfl_sync(kAll, c, D == 3 ? 8 * d : 16 * d);
 }
 
-template <int D, int K, bool SHUF = true, bool SCATTER = true>
+// UNI (uniform masses): no per-slot mass factors; qf = pair_factor * RN(1/m)
+// unless bit 15 of the stencil index marks a clamped j (exactly the stored qf).
+template <int D, int K, bool SHUF = true, bool SCATTER = true, bool UNI = false>
 __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
   const int np = t.np;
   auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
@@ -101,8 +103,9 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     for (int u = 0; u < K; ++u) {
       const int s = lane + u * 32;
       const bool v = s < cnt;
-      const int j = v ? t.nl[lo + s] : t.lbase + pk;  // invalid lanes read i itself with b = 0
-      const double q = v ? t.qf[lo + s] : 0.0;
+      const int jr = v ? t.nl[lo + s] : t.lbase + pk;  // invalid lanes read i itself with b = 0
+      const int j = UNI ? (jr & 0x7fff) : jr;
+      const double q = UNI ? ((v && !(jr & 0x8000)) ? t.pf[lo + s] * t.minv : 0.0) : (v ? t.qf[lo + s] : 0.0);
       const bool up = q != 0.0;                      // clamped j: never written (damping.cpp:84-86)
       jq[u] = j;
       bq[u] = v ? t.kb * t.pf[lo + s] : 0.0;
@@ -126,7 +129,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       const bool v = s < cnt1;
       jn[u] = v ? t.nl[lo1 + s] : li1;
       pfn[u] = v ? t.pf[lo1 + s] : 0.0;
-      qfn[u] = v ? t.qf[lo1 + s] : 0.0;
+      if (!UNI) qfn[u] = v ? t.qf[lo1 + s] : 0.0;
     }
     // row extents two particles ahead
     const int pk2 = kk + 2 < np ? pidx(kk + 2) : pk1;
@@ -170,6 +173,13 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     __syncwarp();
 
     // (D) next particle's coefficients
+    if (UNI) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        qfn[u] = (jn[u] & 0x8000) ? 0.0 : pfn[u] * t.minv;  // invalid lanes: pfn = 0
+        jn[u] &= 0x7fff;
+      }
+    }
     diag = diag1;
     y = y1;
     skip = diag != diag || cnt1 == 0;
