@@ -325,6 +325,46 @@ def particle_steps(args, ws, rank):
     return out
 
 
+def sweep_at_scale(args, ws, rank):
+    """The damping sweep on a large body: BASELINE cfg5's weak-scaling share of one GPU (250 x 250 x 250
+    lattice, 15.6 M particles, 1.24 G slots, dp 0.004, 5-layer clamp), where the colours hold ~10^4
+    cells and the streamed FAST kernel (slot block from L2) runs; DPU/s against the HBM roofline on the
+    same algorithmic byte model as the headline, with the DRAM bytes per launch of the committed ncu
+    capture (profiles/traffic_scale.json)."""
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg5_weak()
+    d = S.build_device(cfg, prepare=False)
+    d.set_reduction("fast")
+    offsets = d.row_offsets()
+    s_free, n_free = free_slots(offsets, cfg["constrained"])
+    b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_free)
+    eta_t, dt = cfg["eta"] / cfg["alpha"], 1e-5
+    d.damping_sweep("particle_split", eta_t, dt, count=2)
+    sweeps = max(3, min(args.scale_sweeps, 50))
+    elapsed = d.damping_sweep("particle_split", eta_t, dt, count=sweeps)
+    t_max = barrier_and_max(elapsed, ws)
+    t_sweep = t_max / sweeps
+    peak, peak_src = load_peaks()
+    achieved = b_sweep / t_sweep / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_scale.json")) as fh:
+            traffic = json.load(fh)
+    except Exception:
+        pass
+    del d
+    return {"metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
+            "value": 2 * s_free * sweeps * ws / t_max, "unit": "DPU/s", "sweeps": sweeps,
+            "ms_per_sweep": t_sweep * 1e3,
+            "config": {"workload": "cfg5 weak-scaling share of one GPU: 250^3 lattice dp 0.004, 5-layer clamp",
+                       "particles": len(cfg["r0"]), "slots": int(offsets[-1]), "reduction": "fast",
+                       "sweep_tiling": "auto (streamed: colours of ~9,700 cells)"},
+            "roofline": {"bound": "hbm", "kernel": "k_sweep_fast<streamed> (one colour phase)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "bytes_per_launch": b_sweep / 54, "avg_launch_s": t_sweep / 54,
+                         "traffic": traffic, "peak_source": peak_src}}
+
+
 def cfg3_oracle_steps(threads, steps):
     """Reference CPU path (oracle port, OpenMP) over the first `steps` cfg3 loop steps."""
     from oracle import oracle as O
@@ -401,6 +441,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sampling")
     ap.add_argument("--ps-steps", type=int, default=300, help="loop steps of the particle-steps/s leg (cfg3)")
     ap.add_argument("--no-ps", action="store_true", help="skip the particle-steps/s leg")
+    ap.add_argument("--scale-sweeps", type=int, default=10, help="sweeps of the large-body (cfg5-weak) leg")
+    ap.add_argument("--no-scale", action="store_true", help="skip the large-body sweep leg")
     ap.add_argument("--parity-sweeps", type=int, default=500, help="cfg2 sweeps of the GPU-vs-oracle check (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
@@ -420,6 +462,8 @@ def main():
         out = run_cfg2(args, ws, rank)
         if not args.no_ps:
             out["particle_steps"] = particle_steps(args, ws, rank)
+        if not args.no_scale:
+            out["sweep_at_scale"] = sweep_at_scale(args, ws, rank)
     if rank == 0 and out is not None:
         print(json.dumps(out))
     if ws > 1:
