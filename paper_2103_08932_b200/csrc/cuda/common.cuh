@@ -101,6 +101,7 @@ struct DFields {
   double* m;
   double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
   double* qf;     // per slot: pair_factor * RN(1/m_j), 0 for clamped j (FAST sweep)
+  double* pkf;    // per slot, per (eta, dt): the pairwise factor b / (m_i m_j - (m_i + m_j) b) (sweep.cu)
   // uniform masses (every m equal): RN(1/m), and per slot the stencil index with bit 15 set for
   // a clamped j (the streamed FAST sweep forms qf = pf * minv_uniform from them); null otherwise
   const uint16_t* nlocf;

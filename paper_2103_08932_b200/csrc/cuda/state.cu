@@ -580,6 +580,7 @@ DFields DevSystem::fields() const {
   f.dwdr0 = dwdr0.p;
   f.pf = pf.p;
   f.qf = qf.p;
+  f.pkf = pkf.p;
   f.pfsum = pf_sum.p;
   f.peer_idx = peer_idx.p;
   f.own = own.p;
@@ -815,6 +816,7 @@ void DevSystem::refresh_minvf() {
     }
   }
   fold_valid = false;  // constrained particles are marked in the fold constants
+  pkf_valid = false;   // pairwise factors use the masses
 }
 
 void DevSystem::compute_sweep_stats() {

@@ -30,12 +30,17 @@
 //      races), plus, for a slab, the columns shared with its neighbours
 //      straight into their arrays (writeback_peers).
 //
-// k_sweep_phase (ORDERED particle split, pairwise split): one 128-thread CTA
-// per cell with the same staging; warp d runs the chain of component d (the
-// update is separable per component once diag and denom are known). ORDERED:
-// lanes form the residual terms, lane 0 folds them in slot order (bit-exact).
-// Pairwise: warp d computes the per-slot b/(m_i m_j - (m_i+m_j) b) and its
-// lane 0 runs the palindromic pair chain (damping.cpp:161-176) of component d.
+// k_sweep_phase (ORDERED particle split): one 128-thread CTA per cell with the
+// same staging; warp d runs the chain of component d (the update is separable
+// per component once diag and denom are known): lanes form the residual terms,
+// lane 0 folds them in slot order (bit-exact).
+//
+// k_sweep_pairwise (pairwise split, damping.cpp:91-106, palindrome :171-176):
+// one warp per cell, PDL-chained like k_sweep_fast, with per-slot factors
+// b/(m_i m_j - (m_i+m_j) b) formed once per (eta, dt) by k_pair_factors.
+// ORDERED: lanes 0..D-1 run the D components' pair chains in lockstep
+// (bit-exact). FAST: each leg of a particle's palindrome is a warp scan of
+// affine maps of v_i, so all pairs of a row are solved at once.
 //
 // Division. B200 IEEE fp64 division costs ~425 cycles of dependent latency
 // (tools/fp64_latency.cu), so no division sits on the chain:
@@ -213,6 +218,26 @@ __global__ void k_sweep_folds(DFields f, double eta, double dt_fixed, int dt_fro
   f.fy[i] = 1.0 / den;
 }
 
+// ------------------------------------------------------------------ per-sweep pairwise factors
+// damping.cpp:91-106: b = eta G dt_pair, k = b / (m_i m_j - (m_i + m_j) b), dt_pair = dt/4 (the
+// palindrome's half steps, :171-176). Velocity-independent, so formed once per (eta, dt) for every
+// slot (IEEE division, the reference's operation order) and staged with the slot block.
+__global__ void k_pair_factors(DFields f, double eta, double dt_fixed, int dt_from_scalars,
+                               const DScalars* __restrict__ sc) {
+  if (dt_from_scalars && sc->halt) return;
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  const double dt_pair = 0.5 * (0.5 * (dt_from_scalars ? sc->dt : dt_fixed));
+  const double mi = f.m[i];
+  const long long hi = f.offs[i + 1];
+  for (long long s = f.offs[i]; s < hi; ++s) {
+    const double b = eta * f.pf[s] * dt_pair;
+    const double mj = f.m[f.nbr[s]];
+    const double denom = mi * mj - (mi + mj) * b;
+    f.pkf[s] = b / denom;
+  }
+}
+
 // ------------------------------------------------------------------ staging (step 1)
 template <int D>
 __device__ __forceinline__ long long phase_cell(const Phase& ph, const DFields& f, long long k, int c[3]) {
@@ -245,7 +270,7 @@ struct CellSpan {
 template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true, bool UNI = false>
 __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
                                               long long sstart, long long send, int lane,
-                                              const uint16_t* nl_src = nullptr) {
+                                              const uint16_t* nl_src = nullptr, const double* pf_src = nullptr) {
   constexpr int kSegs = seg_count<D>();
   const int slen = static_cast<int>(send - sstart);
   const int par = static_cast<int>(sstart & 1);
@@ -281,7 +306,7 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   if (lane == 0) {
     tma_load_1d(t.soff, f.offs + cs.o0(), mybytes, t.bar);
   } else if (SLOTS && lane == 1) {
-    tma_load_1d(t.spf, f.pf + cs.f0(), mybytes, t.bar);
+    tma_load_1d(t.spf, (pf_src ? pf_src : f.pf) + cs.f0(), mybytes, t.bar);
   } else if (SLOTS && lane == 2) {
     tma_load_1d(t.snl, (nl_src ? nl_src : f.nloc) + cs.n0(), mybytes, t.bar);
   } else if (FOLD && lane == 3) {
@@ -472,7 +497,8 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   // ---- 2. the chain: warp d owns velocity component d
   if (warp < D) {
     double* const vd = t.sv[0] + static_cast<size_t>(warp) * ph.S;
-    if (SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT) {
+    static_assert(SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT, "pairwise split: k_sweep_pairwise");
+    {
       constexpr int KK = K > 0 ? K : 1;
       // metadata of the next particle in chain order; none of it depends on the chain
       int pk_n = ph.forward ? 0 : np - 1;
@@ -592,58 +618,6 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
         if (lane == 0) vd[li] = vnew;
         __syncwarp();
       }
-    } else {
-      // pairwise split (damping.cpp:91-106, palindrome :171-176): lane 0 of warp d runs component d
-      double* const kf_scr = t.skf + static_cast<size_t>(warp) * ph.MR;
-      for (int kk = 0; kk < np; ++kk) {
-        const int pk = ph.forward ? kk : np - 1 - kk;
-        const int li = lbase + pk;
-        if (t.smf[li] < 0.0) continue;
-        const int lo = static_cast<int>(offc[pk] - s0), cnt = static_cast<int>(offc[pk + 1] - s0) - lo;
-        const double mi = t.sm[li];
-        for (int s = lane; s < cnt; s += kWarp) {
-          const double b = eta * pfc[lo + s] * dt_op;
-          const double mj = t.sm[nlc[lo + s]];
-          const double denom = mi * mj - (mi + mj) * b;
-          kf_scr[s] = b / denom;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          // The chain carries only v_i. A row's j are distinct, so the operands of
-          // kPairBatch consecutive pairs are loaded before any of them is solved;
-          // the loads of a batch follow the previous batch's stores, and the reverse
-          // leg starts after the forward leg's last store.
-          constexpr int kPairBatch = 8;
-          double vi = vd[li];
-          for (int pass = 0; pass < 2; ++pass) {
-            for (int u0 = 0; u0 < cnt; u0 += kPairBatch) {
-              int jb[kPairBatch];
-              double kfb[kPairBatch], mjb[kPairBatch], vjb[kPairBatch];
-              bool upb[kPairBatch];
-#pragma unroll
-              for (int q = 0; q < kPairBatch; ++q) {
-                const int u = u0 + q < cnt ? u0 + q : cnt - 1;
-                const int s = pass == 0 ? u : cnt - 1 - u;
-                const int j = nlc[lo + s];
-                jb[q] = j;
-                kfb[q] = kf_scr[s];
-                mjb[q] = t.sm[j];
-                vjb[q] = vd[j];
-                upb[q] = t.smf[j] > 0.0;
-              }
-#pragma unroll
-              for (int q = 0; q < kPairBatch; ++q) {
-                if (u0 + q >= cnt) break;
-                const double scaled = kfb[q] * (vi - vjb[q]);
-                vi = vi + mjb[q] * scaled;
-                if (upb[q]) vd[jb[q]] = vjb[q] - mi * scaled;
-              }
-            }
-          }
-          vd[li] = vi;
-        }
-        __syncwarp();
-      }
     }
   }
   __syncthreads();
@@ -730,6 +704,228 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 #ifdef TLSPH_SWEEP_TIMING
   if (lane == 0 && blockIdx.x < (1 << 16)) g_sweep_stamp[blockIdx.x][8] = static_cast<unsigned long long>(cs.p1 - cs.p0);
 #endif
+}
+
+// ------------------------------------------------------------------ pairwise split, one warp per cell
+// damping.cpp:91-106 (pairwise_split_update) in the palindromic order of :171-176: per particle
+// i, its slots ascending then descending, each a 2x2 implicit solve at dt/4 that changes v_i and
+// v_j. The chain of a particle is carried by v_i alone (a row's j are distinct).
+//   ORDERED: lanes 0..D-1 run the D components' chains in lockstep, pair after pair, in the
+//            reference's operation order (bit-exact); operands of kPairBatch pairs are loaded
+//            ahead of their solves.
+//   FAST:    the chain is an affine recurrence in v_i: v_i <- (1 + c_s) v_i - c_s v_j,s with
+//            c_s = m_j k_s, so each leg is a warp scan of affine maps (lane l owns slots
+//            l K .. l K + K - 1; shuffle-up scan forward, shuffle-down scan on the reverse leg)
+//            that yields v_i before every pair at once; the v_j updates
+//            v_j -= m_i k_s (v_i,before - v_j) then run in parallel. Reassociated (FAST class).
+// Per-slot factors k_s come precomputed (k_pair_factors) in the staged slot block.
+template <int D>
+__device__ __forceinline__ void affine_compose(double& A, double (&B)[D], double A2, const double (&B2)[D]) {
+  // (A, B) <- (A, B) o (A2, B2): x -> A (A2 x + B2) + B
+#pragma unroll
+  for (int d = 0; d < D; ++d) B[d] = __fma_rn(A, B2[d], B[d]);
+  A = A * A2;
+}
+
+template <int D, int K, bool ORDERED>
+__global__ void __launch_bounds__(kWarp)
+k_sweep_pairwise(DFields f, Phase ph, const DScalars* __restrict__ sc) {
+  if (ph.dt_from_scalars && sc->halt) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  grid_launch_dependents();
+  int c[3];
+  const long long lin = phase_cell<D>(ph, f, blockIdx.x, c);
+  Tile<D> t = carve<D>(smem, ph);
+  const CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
+  long long sstart, send;
+  locate_row<D>(f, c, lane, sstart, send);
+  if (cs.p0 == cs.p1) return;
+  issue_staging<D, false, true, true>(f, t, cs, sstart, send, lane, nullptr, f.pkf);
+  wait_staging(t);
+  __syncwarp();
+  const int lbase = reinterpret_cast<const int*>(t.bar + 1)[0];
+  const long long* offc = t.soff + (cs.p0 - cs.o0());
+  const double* kfc = t.spf + (cs.s0 - cs.f0());  // staged pairwise factors
+  const uint16_t* nlc = t.snl + (cs.s0 - cs.n0());
+  const int np = static_cast<int>(cs.p1 - cs.p0);
+
+  for (int kk = 0; kk < np; ++kk) {
+    const int pk = ph.forward ? kk : np - 1 - kk;
+    const int li = lbase + pk;
+    if (t.smf[li] < 0.0) continue;  // constrained i (damping.cpp:151)
+    const int lo = static_cast<int>(offc[pk] - cs.s0), cnt = static_cast<int>(offc[pk + 1] - cs.s0) - lo;
+    if (cnt == 0) continue;
+    const double mi = t.sm[li];
+    if (ORDERED || K == 0 || cnt > K * kWarp) {
+      if (lane < D) {
+        double* const vd = t.sv[0] + static_cast<size_t>(lane) * ph.S;  // component arrays are contiguous
+        constexpr int kPairBatch = 8;
+        double vi = vd[li];
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int u0 = 0; u0 < cnt; u0 += kPairBatch) {
+            int jb[kPairBatch];
+            double kfb[kPairBatch], mjb[kPairBatch], vjb[kPairBatch];
+            bool upb[kPairBatch];
+#pragma unroll
+            for (int q = 0; q < kPairBatch; ++q) {
+              const int u = u0 + q < cnt ? u0 + q : cnt - 1;
+              const int s = pass == 0 ? u : cnt - 1 - u;
+              const int j = nlc[lo + s];
+              jb[q] = j;
+              kfb[q] = kfc[lo + s];
+              mjb[q] = t.sm[j];
+              vjb[q] = vd[j];
+              upb[q] = t.smf[j] > 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < kPairBatch; ++q) {
+              if (u0 + q < cnt) {
+                const double scaled = kfb[q] * (vi - vjb[q]);
+                vi = vi + mjb[q] * scaled;
+                if (upb[q]) vd[jb[q]] = vjb[q] - mi * scaled;  // clamped j: discarded (damping.cpp:105)
+              }
+            }
+          }
+        }
+        vd[li] = vi;
+      }
+    } else {
+      constexpr int KK = K > 0 ? K : 1;
+      int jq[KK];
+      bool up[KK];
+      double kq[KK], al[KK], vj[KK][D], vi0[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) vi0[d] = t.sv[d][li];
+#pragma unroll
+      for (int u = 0; u < KK; ++u) {
+        const int s = lane * KK + u;
+        const bool v = s < cnt;
+        const int j = v ? nlc[lo + s] : li;
+        jq[u] = j;
+        kq[u] = v ? kfc[lo + s] : 0.0;
+        up[u] = v && t.smf[j] > 0.0;
+        al[u] = v ? t.sm[j] * kq[u] : 0.0;  // c_s = m_j k_s (identity map for padding slots)
+#pragma unroll
+        for (int d = 0; d < D; ++d) vj[u][d] = t.sv[d][j];
+      }
+      double vfin[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) vfin[d] = vi0[d];
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        // this lane's slots as one affine map, in leg order
+        double A = 1.0, B[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) B[d] = 0.0;
+#pragma unroll
+        for (int q = 0; q < KK; ++q) {
+          const int u = pass == 0 ? q : KK - 1 - q;
+          double Bu[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) Bu[d] = -al[u] * vj[u][d];
+          // later map o earlier: x -> (1 + c) (A x + B) - c v_j
+          double Al = 1.0 + al[u];
+          double Bl[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) Bl[d] = Bu[d];
+          affine_compose<D>(Al, Bl, A, B);
+          A = Al;
+#pragma unroll
+          for (int d = 0; d < D; ++d) B[d] = Bl[d];
+        }
+        // inclusive scan over the lanes in leg order (forward: lower lanes first; reverse: higher)
+#pragma unroll
+        for (int o = 1; o < kWarp; o <<= 1) {
+          double A2 = pass == 0 ? __shfl_up_sync(kFull, A, o) : __shfl_down_sync(kFull, A, o);
+          double B2[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) B2[d] = pass == 0 ? __shfl_up_sync(kFull, B[d], o) : __shfl_down_sync(kFull, B[d], o);
+          const bool has = pass == 0 ? lane >= o : lane + o < kWarp;
+          if (has) affine_compose<D>(A, B, A2, B2);
+        }
+        // exclusive prefix applied to the leg's start value: v_i before this lane's first slot
+        double vstart[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) vstart[d] = pass == 0 ? vi0[d] : vfin[d];
+        double Ae = pass == 0 ? __shfl_up_sync(kFull, A, 1) : __shfl_down_sync(kFull, A, 1);
+        double x[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const double Be = pass == 0 ? __shfl_up_sync(kFull, B[d], 1) : __shfl_down_sync(kFull, B[d], 1);
+          const bool first = pass == 0 ? lane == 0 : lane == kWarp - 1;
+          x[d] = first ? vstart[d] : __fma_rn(Ae, vstart[d], Be);
+        }
+        // the leg's end value: the whole composition (last lane in leg order)
+        const int endl = pass == 0 ? kWarp - 1 : 0;
+        const double At = __shfl_sync(kFull, A, endl);
+        double vend[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) vend[d] = __fma_rn(At, vstart[d], __shfl_sync(kFull, B[d], endl));
+        // the pairs of this lane: v_j updates from v_i before each pair
+#pragma unroll
+        for (int q = 0; q < KK; ++q) {
+          const int u = pass == 0 ? q : KK - 1 - q;
+          const double mk = mi * kq[u];
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double w = x[d] - vj[u][d];
+            x[d] = __fma_rn(al[u], w, x[d]);  // v_i + m_j k (v_i - v_j)
+            if (up[u]) vj[u][d] = vj[u][d] - mk * w;
+          }
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) vfin[d] = vend[d];
+      }
+#pragma unroll
+      for (int u = 0; u < KK; ++u)
+        if (up[u]) {
+#pragma unroll
+          for (int d = 0; d < D; ++d) t.sv[d][jq[u]] = vj[u][d];
+        }
+      if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) t.sv[d][li] = vfin[d];
+      }
+    }
+    __syncwarp();
+  }
+  writeback_peers<D>(f, t, c, lane, kWarp);
+  writeback_rows<D>(f, t, lane);
+}
+
+template <int D, int K, bool ORDERED>
+void launch_pairwise(const DevSystem& s, const DFields& f, Phase ph) {
+  ph.fast = 0;  // masses and 1/m staged; the slot block carries the pairwise factors
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, 0, 0);
+  ph.MR = 0;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    CK(cudaFuncSetAttribute(k_sweep_pairwise<D, K, ORDERED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(ph.ncol));
+  cfg.blockDim = dim3(kWarp);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_sweep_pairwise<D, K, ORDERED>, f, ph, s.scal.p));
+}
+
+template <int D>
+void launch_pairwise_any(const DevSystem& s, const DFields& f, const Phase& ph) {
+  const int K = (s.max_row + kWarp - 1) / kWarp;
+  if (s.reduction == TLSPH_REDUCTION_ORDERED || K > 4) launch_pairwise<D, 0, true>(s, f, ph);
+  else if (K <= 1) launch_pairwise<D, 1, false>(s, f, ph);
+  else if (K == 2) launch_pairwise<D, 2, false>(s, f, ph);
+  else if (K == 3) launch_pairwise<D, 3, false>(s, f, ph);
+  else launch_pairwise<D, 4, false>(s, f, ph);
 }
 
 // Staged or streamed slot block (tlsph_dev_set_sweep_tiling); AUTO: streamed
@@ -878,6 +1074,17 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "damping sweep: a cell's stencil and slot block (" + std::to_string(per_cell) +
                        " bytes) exceed the shared-memory tile");
+  if (scheme == TLSPH_SCHEME_PAIRWISE_SPLIT &&
+      (from_scal || !s.pkf_valid || s.pkf_eta != eta || s.pkf_dt != dt)) {
+    s.pkf.alloc(static_cast<size_t>(std::max<long long>(s.nslots, 1)));
+    DFields fk = s.fields();
+    k_pair_factors<<<static_cast<unsigned>((s.n + 127) / 128), 128, 0, s.stream>>>(fk, eta, dt, from_scal ? 1 : 0,
+                                                                                   s.scal.p);
+    CK_LAUNCH("k_pair_factors");
+    s.pkf_valid = !from_scal;
+    s.pkf_eta = eta;
+    s.pkf_dt = dt;
+  }
   if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
     // per-sweep fold constants; reused while (eta, dt) are unchanged
     const int mode = static_cast<int>(s.reduction);
@@ -913,7 +1120,7 @@ void enqueue_phase(DevSystem& s, int scheme, Phase ph, int pass, int index) {
     if (s.reduction == TLSPH_REDUCTION_ORDERED) launch_particle_split<D, true>(s, f, ph);
     else launch_particle_split<D, false>(s, f, ph);
   } else {
-    launch_phase<D, TLSPH_SCHEME_PAIRWISE_SPLIT, false, 0>(s, f, ph);
+    launch_pairwise_any<D>(s, f, ph);
   }
 }
 

@@ -88,6 +88,9 @@ class DevSystem {
   // per-sweep particle-split constants and the (eta, dt) they were formed for
   DBuf<double> fold_diag, fold_den, fold_y;
   bool fold_valid = false;
+  DBuf<double> pkf;  // pairwise factors per slot (k_pair_factors), valid for (pkf_eta, pkf_dt)
+  bool pkf_valid = false;
+  double pkf_eta = 0.0, pkf_dt = 0.0;
   double fold_eta = 0.0, fold_dt = 0.0;
   int fold_mode = -1;  // reduction mode the fold constants were formed in
   DBuf<uint8_t> flag;

@@ -250,15 +250,16 @@ def test_sweep_ordered_bit_exact(scheme, dim):
 
 
 @pytest.mark.parametrize("dim", [2, 3])
-def test_sweep_fast_within_tolerance(dim):
+@pytest.mark.parametrize("scheme", ["particle_split", "pairwise_split"])
+def test_sweep_fast_within_tolerance(dim, scheme):
     r0 = lattice_r0([31, 29] if dim == 2 else [13, 12, 11], 0.01)
     o, d = pair(r0, 0.01 ** dim, 1000.0, 0.013)
     v = random_velocities(len(r0), dim, 1.0, 9)
     o.set("v", v)
     d.set("v", v)
     for _ in range(5):
-        o.damping_sweep("particle_split", 2000.0, 2e-4)
-        d.damping_sweep("particle_split", 2000.0, 2e-4)
+        o.damping_sweep(scheme, 2000.0, 2e-4)
+        d.damping_sweep(scheme, 2000.0, 2e-4)
     assert rel_l2(d.get("v"), o.get("v")) <= TOL
 
 
@@ -273,7 +274,8 @@ def irregular_bodies():
 
 @pytest.mark.parametrize("case", list(irregular_bodies()), ids=lambda c: c[0])
 @pytest.mark.parametrize("mode", ["ordered", "fast"])
-def test_sweep_irregular_bodies(case, mode):
+@pytest.mark.parametrize("scheme", ["particle_split", "pairwise_split"])
+def test_sweep_irregular_bodies(case, mode, scheme):
     """Variable neighbour counts and cell occupancy, including rows longer than the register path."""
     name, r0, V0, h = case
     cons = (r0[:, 0] < np.quantile(r0[:, 0], 0.05)).astype(np.uint8)
@@ -284,8 +286,8 @@ def test_sweep_irregular_bodies(case, mode):
     o.set("v", v)
     d.set("v", v)
     for _ in range(2):
-        o.damping_sweep("particle_split", 300.0, 1e-4)
-        d.damping_sweep("particle_split", 300.0, 1e-4)
+        o.damping_sweep(scheme, 300.0, 1e-4)
+        d.damping_sweep(scheme, 300.0, 1e-4)
     if mode == "ordered":
         assert np.array_equal(o.get("v"), d.get("v"))
     else:
