@@ -134,6 +134,12 @@ struct DFields {
   double* r0_len;
   double* e0[3];
   double* dwdr0;
+  // the same slots with each row re-ordered by ascending (cell-sorted) neighbour index: the FAST
+  // neighbour passes B and C gather from neighbours grouped by cell (fewer cache lines per warp
+  // load than the reference's ascending-reference-id order, which the ORDERED kernels keep)
+  const int* snbr;
+  const double* sdw;
+  const double* se0[3];
   double* pf;
   uint16_t* nloc;  // index of j inside the staged 3^D stencil of i's cell
   // cell grid

@@ -387,6 +387,28 @@ __global__ void k_nlocf(const uint16_t* __restrict__ nloc, const int* __restrict
   nlocf[s] = static_cast<uint16_t>(nloc[s] | (flag[nbr[s]] ? 0x8000u : 0u));
 }
 
+// Rows re-ordered by ascending neighbour index (distinct within a row): one warp per row, each
+// slot's destination is its rank in the row.
+template <int D>
+__global__ void k_sorted_rows(DFields f, int* __restrict__ snbr, double* __restrict__ sdw,
+                              double* __restrict__ se0x, double* __restrict__ se0y, double* __restrict__ se0z) {
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (i >= f.n) return;
+  const long long lo = f.offs[i], hi = f.offs[i + 1];
+  for (long long s = lo + lane; s < hi; s += 32) {
+    const int key = f.nbr[s];
+    long long rank = 0;
+    for (long long t = lo; t < hi; ++t) rank += f.nbr[t] < key ? 1 : 0;
+    const long long dst = lo + rank;
+    snbr[dst] = key;
+    sdw[dst] = f.dwdr0[s];
+    se0x[dst] = f.e0[0][s];
+    se0y[dst] = f.e0[1][s];
+    if (D == 3) se0z[dst] = f.e0[2][s];
+  }
+}
+
 __global__ void k_pf_sums(DFields f) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= f.n) return;
@@ -578,6 +600,9 @@ DFields DevSystem::fields() const {
   f.nbr = nbr.p;
   f.r0_len = r0_len.p;
   f.dwdr0 = dwdr0.p;
+  f.snbr = snbr.p;
+  f.sdw = sdw.p;
+  for (int d = 0; d < 3; ++d) f.se0[d] = se0[d].p;
   f.pf = pf.p;
   f.qf = qf.p;
   f.pkf = pkf.p;
@@ -821,6 +846,17 @@ void DevSystem::refresh_minvf() {
 
 void DevSystem::compute_sweep_stats() {
   refresh_minvf();
+  if (nslots > 0) {
+    const size_t S = static_cast<size_t>(nslots);
+    snbr.alloc(S);
+    sdw.alloc(S);
+    for (int d = 0; d < D; ++d) se0[d].alloc(S);
+    const DFields f = fields();
+    const unsigned grid = static_cast<unsigned>((n * 32 + 255) / 256);
+    if (D == 2) k_sorted_rows<2><<<grid, 256, 0, stream>>>(f, snbr.p, sdw.p, se0[0].p, se0[1].p, nullptr);
+    else k_sorted_rows<3><<<grid, 256, 0, stream>>>(f, snbr.p, sdw.p, se0[0].p, se0[1].p, se0[2].p);
+    CK_LAUNCH("k_sorted_rows");
+  }
   pf_sum.alloc(static_cast<size_t>(n));
   pf_sq.alloc(static_cast<size_t>(n));
   k_pf_sums<<<grid_for(n, 256), 256, 0, stream>>>(fields());

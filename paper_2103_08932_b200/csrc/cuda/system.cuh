@@ -113,6 +113,8 @@ class DevSystem {
   DBuf<double> r0_len, e0[3], dwdr0, pf;
   DBuf<double> qf;  // pf * RN(1/m_j), 0 for clamped j: the FAST sweep's per-slot mass factor
   DBuf<double> pf_sum, pf_sq;  // per-particle sums of pf and pf^2 (static)
+  DBuf<int> snbr;              // rows in neighbour-index order (k_sorted_rows): FAST passes B, C
+  DBuf<double> sdw, se0[3];
   DBuf<uint16_t> nloc;
   DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)
   bool uniform_mass = false;  // every particle has the same mass

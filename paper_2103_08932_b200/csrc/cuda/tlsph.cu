@@ -96,6 +96,25 @@ constexpr int kGB3 = TLSPH_TL_GB3, kGC3 = TLSPH_TL_GC3;  // lanes per particle i
 // The ORDERED kernels (G = 1: one thread per particle, slot-order sums) are separate entry
 // points with one slot per iteration and no register bound; both changes cost them ~20 %.
 
+// Slot arrays of the neighbour passes: the FAST kernels (G > 1) read the rows in neighbour-index
+// order (DFields::snbr, set up by k_sorted_rows), the ORDERED ones in the reference's order.
+#ifndef TLSPH_TL_SORTED
+#define TLSPH_TL_SORTED 1
+#endif
+template <int D, int G>
+struct SlotView {
+  const int* nbr;
+  const double* dw;
+  const double* e0[D];
+  __device__ explicit SlotView(const DFields& f) {
+    const bool s = TLSPH_TL_SORTED && G > 1 && f.snbr;
+    nbr = s ? f.snbr : f.nbr;
+    dw = s ? f.sdw : f.dwdr0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) e0[d] = s ? f.se0[d] : f.e0[d];
+  }
+};
+
 template <int D, int G, int U, bool POST>
 __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars* sc, double dt, int loop) {
   if (loop && sc->halt) return;
@@ -104,6 +123,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
   const long long i = tid / G;
   const int l = static_cast<int>(tid % G);
   const bool active = i < f.n && is_owned(f, i);
+  const SlotView<D, G> sv(f);
   double rate[D][D];
 #pragma unroll
   for (int r = 0; r < D; ++r)
@@ -123,10 +143,10 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
       for (int u = 0; u < U; ++u) {
         const bool ok = s + u * G < hi;
         const long long su = ok ? s + u * G : s;
-        j[u] = f.nbr[su];
-        dw[u] = f.dwdr0[su];
+        j[u] = sv.nbr[su];
+        dw[u] = sv.dw[su];
 #pragma unroll
-        for (int d = 0; d < D; ++d) e[u][d] = f.e0[d][su];
+        for (int d = 0; d < D; ++d) e[u][d] = sv.e0[d][su];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -273,6 +293,7 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
   const long long i = tid / G;
   const int l = static_cast<int>(tid % G);
   const bool active = i < f.n && is_owned(f, i);
+  const SlotView<D, G> sv(f);
   double acc[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) acc[d] = 0.0;
@@ -295,10 +316,10 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long su = s + u * G < hi ? s + u * G : s;
-        j[u] = f.nbr[su];
-        dw[u] = f.dwdr0[su];
+        j[u] = sv.nbr[su];
+        dw[u] = sv.dw[su];
 #pragma unroll
-        for (int d = 0; d < D; ++d) e[u][d] = f.e0[d][su];
+        for (int d = 0; d < D; ++d) e[u][d] = sv.e0[d][su];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
