@@ -458,6 +458,9 @@ def tiling_bodies():
     yield "lattice2d_uniform", base2, 0.01 ** 2, 1000.0, 0.013
     jit = base3 + rng.uniform(-0.004, 0.004, base3.shape)
     yield "jitter3d_masses", jit, rng.uniform(0.5e-6, 1.5e-6, len(jit)), 1000.0, 0.013
+    # sparse clouds: ragged rows, empty and single-particle cells, isolated particles
+    yield "random2d", rng.uniform(0, 1, (600, 2)), 1e-4, 1000.0, 0.05
+    yield "random3d", rng.uniform(0, 0.5, (700, 3)), 1e-6, 1000.0, 0.05
 
 
 @pytest.mark.parametrize("case", list(tiling_bodies()), ids=lambda c: c[0])
