@@ -132,6 +132,16 @@ tlsph_status tlsph_dev_damping_phase(tlsph_dev* dev, tlsph_dev_scheme scheme, do
  * NVLink when the slabs live on different GPUs), so no pack/unpack is needed;
  * the caller only orders the phases of all slabs (a barrier per phase). */
 tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer);
+/* `count` sweeps over peer-linked slabs held by this process (slabs[r]'s
+ * right neighbour is slabs[r+1]), enqueued at once with no host
+ * synchronisation between phases: each slab's phases run on its own stream
+ * (its GPU), and before phase q+1 a slab's stream waits on the phase-q events
+ * of its two neighbours -- the per-phase barrier of the fused exchange, kept on
+ * the devices. Returns after the last phase; tlsph_dev_last_elapsed(slabs[0])
+ * then holds the device time of the whole call. Results equal the sweeps of
+ * the undivided body bit for bit (ORDERED and FAST). */
+tlsph_status tlsph_dev_sweep_linked(tlsph_dev* const* slabs, int nslabs, tlsph_dev_scheme scheme, double eta_tilde,
+                                    double dt, int count);
 int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x);
 tlsph_status tlsph_dev_pack_column(tlsph_dev* dev, int x, double* device_dst);
 tlsph_status tlsph_dev_unpack_column(tlsph_dev* dev, int x, const double* device_src);

@@ -176,6 +176,23 @@ tlsph_status tlsph_dev_damping_phase(tlsph_dev* dev, tlsph_dev_scheme scheme, do
   });
 }
 
+tlsph_status tlsph_dev_sweep_linked(tlsph_dev* const* slabs, int nslabs, tlsph_dev_scheme scheme, double eta_tilde,
+                                    double dt, int count) {
+  return guarded([&] {
+    if (!slabs || nslabs < 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "no slabs");
+    if (count < 0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "negative sweep count");
+    if (scheme != TLSPH_SCHEME_PARTICLE_SPLIT && scheme != TLSPH_SCHEME_PAIRWISE_SPLIT)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "only the split schemes are swept");
+    std::vector<DevSystem*> sl;
+    for (int r = 0; r < nslabs; ++r) {
+      if (!slabs[r]) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null slab");
+      sl.push_back(&sys(slabs[r]));
+    }
+    if (eta_tilde == 0.0 || count == 0) return;  // damping.cpp:132
+    sweep_linked(sl, scheme, eta_tilde, dt, count);
+  });
+}
+
 tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer) {
   return guarded([&] {
     if (!peer) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer must not be null");

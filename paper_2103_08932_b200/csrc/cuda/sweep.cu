@@ -1279,6 +1279,68 @@ void DevSystem::enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixe
   CK_LAUNCH("k_sweep_phase");
 }
 
+// Sweeps over peer-linked slabs with the per-phase ordering on the devices (tlsph_dev_sweep_linked).
+// Phase q of slab r may start once phase q-1 of slabs r-1 and r+1 has finished: they store into
+// r's shared columns (fused exchange) and read the columns r stores into theirs. Events are
+// recorded and waited in host program order, so every wait refers to the intended phase.
+void sweep_linked(const std::vector<DevSystem*>& sl, int scheme, double eta_tilde, double dt, int count) {
+  if (sl.empty()) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "no slabs");
+  const int D0 = sl[0]->D;
+  for (DevSystem* s : sl)
+    if (!s || s->D != D0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "slabs must share the dimension");
+  const int nphase = 2 * (D0 == 2 ? 9 : 27);
+  for (DevSystem* s : sl) {
+    CK(cudaSetDevice(s->device));
+    while (static_cast<int>(s->phase_events.size()) < nphase) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->phase_events.push_back(e);
+    }
+  }
+  DevSystem& s0 = *sl[0];
+  CK(cudaSetDevice(s0.device));
+  cudaEvent_t t0, t1;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventRecord(t0, s0.stream));
+  for (size_t r = 1; r < sl.size(); ++r) {  // every slab starts after t0
+    CK(cudaSetDevice(sl[r]->device));
+    CK(cudaStreamWaitEvent(sl[r]->stream, t0, 0));
+  }
+  const int nr = static_cast<int>(sl.size());
+  for (int c = 0; c < count; ++c) {
+    for (int q = 0; q < nphase; ++q) {
+      const int pass = q < nphase / 2 ? 0 : 1, index = q % (nphase / 2);
+      for (int r = 0; r < nr; ++r) {
+        DevSystem& s = *sl[r];
+        CK(cudaSetDevice(s.device));
+        const bool first = c == 0 && q == 0;
+        if (!first) {
+          const int qp = q > 0 ? q - 1 : nphase - 1;  // the previous phase (of the previous sweep)
+          if (r > 0) CK(cudaStreamWaitEvent(s.stream, sl[r - 1]->phase_events[qp], 0));
+          if (r + 1 < nr) CK(cudaStreamWaitEvent(s.stream, sl[r + 1]->phase_events[qp], 0));
+        }
+        s.enqueue_sweep_phase(scheme, eta_tilde, dt, pass, index);
+        CK(cudaEventRecord(s.phase_events[q], s.stream));
+      }
+    }
+  }
+  CK(cudaSetDevice(s0.device));
+  for (int r = 1; r < nr; ++r) CK(cudaStreamWaitEvent(s0.stream, sl[r]->phase_events[nphase - 1], 0));
+  CK(cudaEventRecord(t1, s0.stream));
+  CK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, t0, t1));
+  s0.last_elapsed = ms * 1e-3;
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  for (DevSystem* s : sl) {
+    CK(cudaSetDevice(s->device));
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  CK(cudaSetDevice(s0.device));
+}
+
 namespace {
 // cell count of a column and the exclusive prefix of its cells' particle counts
 std::vector<long long> column_offsets(const DevSystem& s, int x) {

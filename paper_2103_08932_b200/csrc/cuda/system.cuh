@@ -173,6 +173,7 @@ class DevSystem {
   void enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars);
   // one colour phase (pass 0 forward / 1 reverse, index-th colour of the pass)
   void enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index);
+  std::vector<cudaEvent_t> phase_events;  // tlsph_dev_sweep_linked: one per colour phase (this device)
   void build_colour_lists();  // host sync: at construction and when the task range changes
   void build_own_mask();      // own[] from the task range (x-slab ownership)
   void link_peer(int side, DevSystem& peer);  // sweep.cu
@@ -197,6 +198,7 @@ unsigned long long selftest_division(long long n, unsigned long long seed);  // 
 
 // kernels shared across translation units
 void launch_reduce_state(const DevSystem& s, bool with_finite, bool with_ke, bool dt_mode);
+void sweep_linked(const std::vector<DevSystem*>& slabs, int scheme, double eta_tilde, double dt, int count);
 
 }  // namespace tlsph_cuda
 

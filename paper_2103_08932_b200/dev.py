@@ -126,6 +126,7 @@ def lib():
     L.tlsph_dev_set_field.argtypes = [P, I, D]
     L.tlsph_dev_get_field.argtypes = [P, I, D]
     L.tlsph_dev_set_reduction.argtypes = [P, I]
+    L.tlsph_dev_sweep_linked.argtypes = [C.POINTER(P), I, I, C.c_double, C.c_double, I]
     L.tlsph_dev_set_sweep_tiling.argtypes = [P, I]
     L.tlsph_dev_grid_info.argtypes = [P, C.POINTER(I), D, D, C.POINTER(C.c_int64)]
     L.tlsph_dev_grid_cells.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
@@ -155,6 +156,14 @@ def lib():
 
 def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def sweep_linked(systems, scheme, eta_tilde, dt, count=1):
+    """tlsph_dev_sweep_linked: `count` sweeps over peer-linked slabs (left to right) with the
+    per-phase ordering kept on the devices; returns the device time of the call (seconds)."""
+    arr = (C.c_void_p * len(systems))(*[d._h.value for d in systems])
+    _check(lib().tlsph_dev_sweep_linked(arr, len(systems), SCHEMES[scheme], float(eta_tilde), float(dt), int(count)))
+    return float(lib().tlsph_dev_last_elapsed(systems[0]._h))
 
 
 def _check(status):

@@ -311,6 +311,18 @@ def sweep_fused(systems, scheme, eta_tilde, dt, dim):
             d.damping_phase(scheme, eta_tilde, dt, p, index)
 
 
+def sweep_linked(systems, scheme, eta_tilde, dt, count=1):
+    """The fused sweep with the phase barrier on the devices: all phases of all slabs enqueued at
+    once, each slab's stream waiting on its neighbours' previous-phase events
+    (tlsph_dev_sweep_linked); no host synchronisation until the last phase. Returns the device
+    time in seconds."""
+    from paper_2103_08932_b200 import dev
+
+    if eta_tilde == 0.0:
+        return 0.0
+    return dev.sweep_linked(systems, scheme, eta_tilde, dt, count)
+
+
 class SlabSweep:
     """One rank's share of the decomposed sweep; halo columns travel through torch.distributed
     point-to-point operations (NCCL between GPUs, gloo on CPU)."""

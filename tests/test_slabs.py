@@ -280,6 +280,33 @@ def test_fused_peer_slabs_equal_undivided_device(dim, world, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("dim,world,mode,scheme", [(2, 3, "ordered", "particle_split"), (3, 2, "fast", "particle_split"),
+                                                   (3, 4, "ordered", "particle_split"), (3, 3, "fast", "particle_split"),
+                                                   (3, 3, "ordered", "pairwise_split"), (3, 2, "fast", "pairwise_split")])
+def test_linked_slabs_equal_undivided_device(dim, world, mode, scheme):
+    """Fused exchange with the per-phase barrier on the devices (stream event dependencies between
+    neighbouring slabs, no host synchronisation): bitwise the undivided sweep."""
+    from paper_2103_08932_b200 import dev
+
+    r0, cons, v = body(dim, [40, 9] if dim == 2 else [30, 6, 5])
+    whole = dev.DeviceSystem(r0, DP ** dim, RHO, H, cons)
+    whole.set_reduction(mode)
+    whole.set("v", v)
+    grid, parts = slabs.decompose(r0, H, world)
+    systems = [slabs.make_device_slab(grid, s, r0, DP ** dim, RHO, H, cons) for s in parts]
+    for s, d in zip(parts, systems):
+        d.set_reduction(mode)
+        d.set("v", v[s.ids])
+    slabs.link_peers(systems)
+    whole.damping_sweep(scheme, 160.0, 1e-4, count=3)
+    el = slabs.sweep_linked(systems, scheme, 160.0, 1e-4, count=3)
+    assert el > 0.0
+    ref = whole.get("v")
+    for s, d in zip(parts, systems):
+        assert np.array_equal(d.get("v"), ref[s.ids])
+
+
+@pytest.mark.gpu
 def test_device_phases_compose_to_sweep():
     from paper_2103_08932_b200 import dev
 
