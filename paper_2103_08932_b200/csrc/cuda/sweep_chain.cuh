@@ -73,6 +73,39 @@ __device__ __forceinline__ void warp_sum_vec(double (&x)[D], int lane) {
 
 // UNI (uniform masses): no per-slot mass factors; qf = pair_factor * RN(1/m)
 // unless bit 15 of the stencil index marks a clamped j (exactly the stored qf).
+// The same sum through the fp64 tensor-core MMA (mma.sync m8n8k4, B = ones): one MMA per
+// component sums each group of four lanes (lane 4r+k supplies A[r][k]; every lane of group r
+// receives the group sum), then a three-level xor butterfly adds the eight group sums. Dependent
+// latency ~185 cycles against ~233 for the shuffle tree (tools/dmma_probe.cu); the summation order
+// differs (FAST class).
+#ifndef TLSPH_SWEEP_MMA_SUM
+#define TLSPH_SWEEP_MMA_SUM 1
+#endif
+template <int D>
+__device__ __forceinline__ void warp_sum_vec_mma(double (&x)[D]) {
+  constexpr unsigned kAll = 0xffffffffu;
+  double r[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double unused;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+                 : "=d"(r[d]), "=d"(unused)
+                 : "d"(x[d]), "d"(1.0), "d"(0.0), "d"(0.0));
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+    for (int d = 0; d < D; ++d) r[d] += __shfl_xor_sync(kAll, r[d], o);
+#pragma unroll
+  for (int d = 0; d < D; ++d) x[d] = r[d];
+}
+
+template <int D>
+__device__ __forceinline__ void chain_sum(double (&x)[D], int lane) {
+  if (TLSPH_SWEEP_MMA_SUM) warp_sum_vec_mma<D>(x);
+  else warp_sum_vec<D>(x, lane);
+}
+
 template <int D, int K, bool SHUF = true, bool SCATTER = true, bool UNI = false>
 __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
   const int np = t.np;
@@ -158,7 +191,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     for (int u = 0; u < K; ++u)
 #pragma unroll
       for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(c1[u], vq[u][d], -bmq[u] * vi[d]);
-    if (SHUF) warp_sum_vec<D>(P, lane);
+    if (SHUF) chain_sum<D>(P, lane);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const double rate = P[d] * y;
@@ -310,7 +343,7 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     for (int u = 0; u < K; ++u)
 #pragma unroll
       for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(c1[u], vq[u][d], -bmq[u] * vi[d]);
-    warp_sum_vec<D>(P, lane);
+    chain_sum<D>(P, lane);
     double qfn[K];
     mass_factors(jn, pfn, qfn);  // particle kk+1 (loaded an iteration ago)
 #pragma unroll
