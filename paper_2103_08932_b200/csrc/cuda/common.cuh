@@ -182,6 +182,29 @@ __device__ __forceinline__ double group_sum(double x) {
   return x;
 }
 
+// Sum over groups of G consecutive lanes (G = 4 or 8) with the fp64 tensor-core MMA: mma.sync
+// m8n8k4 with B = ones gives every lane the sum of its four-lane group (lane 4r+k supplies
+// A[r][k]); one xor level completes G = 8. Whole warp, converged. FAST summation order.
+#ifndef TLSPH_GROUP_MMA
+#define TLSPH_GROUP_MMA 1
+#endif
+template <int G>
+__device__ __forceinline__ double group_sum_mma(double x) {
+  static_assert(G == 4 || G == 8, "G");
+  double r, unused;
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+               : "=d"(r), "=d"(unused)
+               : "d"(x), "d"(1.0), "d"(0.0), "d"(0.0));
+  if (G == 8) r += __shfl_xor_sync(0xffffffffu, r, 4);
+  return r;
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum_fast(double x) {
+  if constexpr (TLSPH_GROUP_MMA && (G == 4 || G == 8)) return group_sum_mma<G>(x);
+  else return group_sum<G>(x);
+}
+
 // ---------------------------------------------------------------- cell grid
 // CellGrid::coords_of_position (neighbors.cpp:14-22) and linear_index
 // (neighbors.hpp:32-36, x fastest).

@@ -171,7 +171,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
-      for (int q = 0; q < D; ++q) rate[r][q] = group_sum<G>(rate[r][q]);
+      for (int q = 0; q < D; ++q) rate[r][q] = group_sum_fast<G>(rate[r][q]);
   }
   if (!active || l != 0) return;
   M<D> R;
@@ -345,7 +345,7 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
   }
   if (G > 1) {
 #pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] = group_sum<G>(acc[d]);
+    for (int d = 0; d < D; ++d) acc[d] = group_sum_fast<G>(acc[d]);
   }
   if (!active || l != 0) return;
   const double mi = f.m[i];
