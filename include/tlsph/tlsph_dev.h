@@ -140,6 +140,24 @@ tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer);
  * the devices. Returns after the last phase; tlsph_dev_last_elapsed(slabs[0])
  * then holds the device time of the whole call. Results equal the sweeps of
  * the undivided body bit for bit (ORDERED and FAST). */
+/* Cross-process linking (one process per GPU, e.g. under torchrun). A slab
+ * exports its velocity arrays and colour-phase events as CUDA IPC handles in an
+ * opaque blob of tlsph_dev_ipc_size() bytes; the host hands the blobs and the
+ * cell tables (tlsph_dev_grid_cells' cell_start, ncells + 1 entries) to the
+ * neighbours, which open and link them (the fused exchange of
+ * tlsph_dev_link_peer, across processes). tlsph_dev_sweep_phase_ipc then
+ * enqueues colour phase q (0 .. 2*3^D - 1: forward leg, then the reverse leg)
+ * asynchronously: the slab's stream first waits on the linked neighbours'
+ * events of phase wait_q (-1: none), runs the phase and records its own phase-q
+ * event. The caller must only request a wait on a phase its neighbours have
+ * already enqueued (a host-side counter per slab suffices; see slabs.py).
+ * tlsph_dev_synchronize waits for the slab's stream. */
+size_t tlsph_dev_ipc_size(void);
+tlsph_status tlsph_dev_ipc_export(tlsph_dev* dev, void* blob);
+tlsph_status tlsph_dev_link_peer_ipc(tlsph_dev* dev, int side, const void* peer_blob, const int64_t* peer_cell_start);
+tlsph_status tlsph_dev_sweep_phase_ipc(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt, int q,
+                                       int wait_q);
+tlsph_status tlsph_dev_synchronize(tlsph_dev* dev);
 tlsph_status tlsph_dev_sweep_linked(tlsph_dev* const* slabs, int nslabs, tlsph_dev_scheme scheme, double eta_tilde,
                                     double dt, int count);
 int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x);

@@ -2,6 +2,7 @@
 // Exception-free: every entry point maps DevError / std::exception to a
 // tlsph_status and a thread-local message, as the reference C API does
 // (proj/src/capi.cpp:12,26-42).
+#include <cstring>
 #include <memory>
 #include <random>
 #include <string>
@@ -10,6 +11,7 @@
 
 using tlsph_cuda::DevError;
 using tlsph_cuda::DevSystem;
+using tlsph_cuda::IpcExport;
 
 namespace {
 
@@ -190,6 +192,44 @@ tlsph_status tlsph_dev_sweep_linked(tlsph_dev* const* slabs, int nslabs, tlsph_d
     }
     if (eta_tilde == 0.0 || count == 0) return;  // damping.cpp:132
     sweep_linked(sl, scheme, eta_tilde, dt, count);
+  });
+}
+
+size_t tlsph_dev_ipc_size(void) { return sizeof(IpcExport); }
+
+tlsph_status tlsph_dev_ipc_export(tlsph_dev* dev, void* blob) {
+  return guarded([&] {
+    if (!blob) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null blob");
+    IpcExport e;
+    sys(dev).ipc_export(&e);
+    std::memcpy(blob, &e, sizeof(e));
+  });
+}
+
+tlsph_status tlsph_dev_link_peer_ipc(tlsph_dev* dev, int side, const void* peer_blob, const int64_t* peer_cell_start) {
+  return guarded([&] {
+    if (!peer_blob || !peer_cell_start) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null peer export");
+    IpcExport e;
+    std::memcpy(&e, peer_blob, sizeof(e));
+    static_assert(sizeof(int64_t) == sizeof(long long), "cell table");
+    sys(dev).link_peer_ipc(side, e, reinterpret_cast<const long long*>(peer_cell_start));
+  });
+}
+
+tlsph_status tlsph_dev_sweep_phase_ipc(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt, int q,
+                                       int wait_q) {
+  return guarded([&] {
+    if (scheme != TLSPH_SCHEME_PARTICLE_SPLIT && scheme != TLSPH_SCHEME_PAIRWISE_SPLIT)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "only the split schemes are swept");
+    sys(dev).sweep_phase_ipc(scheme, eta_tilde, dt, q, wait_q);
+  });
+}
+
+tlsph_status tlsph_dev_synchronize(tlsph_dev* dev) {
+  return guarded([&] {
+    DevSystem& s = sys(dev);
+    CK(cudaSetDevice(s.device));
+    s.sync();
   });
 }
 

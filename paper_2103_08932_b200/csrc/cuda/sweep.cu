@@ -53,6 +53,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "stencil_tile.cuh"
 #include "sweep_chain.cuh"
@@ -1194,9 +1195,18 @@ void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, boo
 // 1: right): both hold the columns' particles, binned in the same global cells
 // with the same in-cell order, so the k-th particle of a cell maps to the k-th.
 void DevSystem::link_peer(int side, DevSystem& peer) {
-  if (side != 0 && side != 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer side must be 0 (left) or 1 (right)");
-  if (!grid_given || !peer.grid_given || peer.D != D || peer.ncells != ncells)
+  if (!peer.grid_given || peer.D != D || peer.ncells != ncells)
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peers must be slabs of the same global grid");
+  double* pv[3] = {nullptr, nullptr, nullptr};
+  for (int d = 0; d < D; ++d) pv[d] = peer.v[d].p;
+  link_peer_arrays(side, peer.cell_start_h.data(), pv);
+}
+
+// The peer given by its cell table (host, ncells + 1 entries) and velocity arrays (device
+// pointers reachable from this slab's GPU: the peer's own, or opened from its IPC export).
+void DevSystem::link_peer_arrays(int side, const long long* peer_cell_start, double* const* peer_vel) {
+  if (side != 0 && side != 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer side must be 0 (left) or 1 (right)");
+  if (!grid_given) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peers must be slabs of the same global grid");
   const int x0 = task_x0, x1 = task_x1 < 0 ? dims[0] : task_x1;
   // shared columns: left x0-1 (peer owns) and x0 (we own); right x1-1 (we own) and x1 (peer owns)
   const int ca = side == 0 ? x0 - 1 : x1 - 1, cb = ca + 1;
@@ -1208,7 +1218,7 @@ void DevSystem::link_peer(int side, DevSystem& peer) {
     for (int q = 0; q < nq; ++q) {
       const long long lin = static_cast<long long>(q) * dims[0] + x;
       const long long a0 = cell_start_h[lin], a1 = cell_start_h[lin + 1];
-      const long long b0 = peer.cell_start_h[lin], b1 = peer.cell_start_h[lin + 1];
+      const long long b0 = peer_cell_start[lin], b1 = peer_cell_start[lin + 1];
       if (a1 - a0 != b1 - b0) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer slabs disagree on a shared cell");
       for (long long k = 0; k < a1 - a0; ++k) {
         const long long j = b0 + k;
@@ -1217,8 +1227,79 @@ void DevSystem::link_peer(int side, DevSystem& peer) {
     }
   peer_idx.alloc(idx.size());
   CK(cudaMemcpy(peer_idx.p, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice));
-  for (int d = 0; d < 3; ++d) peer_v[side][d] = d < D ? peer.v[d].p : nullptr;
+  for (int d = 0; d < 3; ++d) peer_v[side][d] = d < D ? peer_vel[d] : nullptr;
   peer_x[side] = side == 0 ? x0 : x1 - 1;
+}
+
+// ---- cross-process linking (one process per GPU)
+void DevSystem::ensure_phase_events(bool interprocess) {
+  const int nphase = 2 * (D == 2 ? 9 : 27);
+  if (interprocess && !phase_events_ipc) {
+    for (cudaEvent_t e : phase_events) cudaEventDestroy(e);
+    phase_events.clear();
+  }
+  CK(cudaSetDevice(device));
+  while (static_cast<int>(phase_events.size()) < nphase) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (interprocess ? cudaEventInterprocess : 0)));
+    phase_events.push_back(e);
+  }
+  if (interprocess) phase_events_ipc = true;
+}
+
+void DevSystem::ipc_export(IpcExport* out) {
+  ensure_phase_events(true);
+  std::memset(out, 0, sizeof(IpcExport));
+  out->magic = IpcExport::kMagic;
+  out->dim = D;
+  out->device = device;
+  out->nphase = static_cast<int>(phase_events.size());
+  for (int d = 0; d < D; ++d) CK(cudaIpcGetMemHandle(&out->vel[d], v[d].p));
+  for (int q = 0; q < out->nphase; ++q) CK(cudaIpcGetEventHandle(&out->ev[q], phase_events[q]));
+}
+
+void DevSystem::link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start) {
+  if (peer.magic != IpcExport::kMagic || peer.dim != D)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "not an IPC export of a slab of this dimension");
+  if (side != 0 && side != 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer side must be 0 (left) or 1 (right)");
+  CK(cudaSetDevice(device));
+  IpcPeer& ip = ipc_peer[side];
+  ip.close();
+  double* pv[3] = {nullptr, nullptr, nullptr};
+  for (int d = 0; d < D; ++d) {
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, peer.vel[d], cudaIpcMemLazyEnablePeerAccess));
+    ip.mem.push_back(p);
+    pv[d] = static_cast<double*>(p);
+  }
+  for (int q = 0; q < peer.nphase; ++q) {
+    cudaEvent_t e;
+    CK(cudaIpcOpenEventHandle(&e, peer.ev[q]));
+    ip.ev.push_back(e);
+  }
+  link_peer_arrays(side, peer_cell_start, pv);
+}
+
+void IpcPeer::close() {
+  for (void* p : mem) cudaIpcCloseMemHandle(p);
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  mem.clear();
+  ev.clear();
+}
+
+// Phase q of the decomposed sweep of this slab, asynchronous: the stream first waits on the
+// linked neighbours' events of phase `wait_q` (-1: none), then runs the phase and records
+// its own event q. The caller orders the calls so a neighbour recorded wait_q before.
+void DevSystem::sweep_phase_ipc(int scheme, double eta_tilde, double dt, int q, int wait_q) {
+  ensure_phase_events(true);
+  const int nphase = static_cast<int>(phase_events.size());
+  if (q < 0 || q >= nphase || wait_q >= nphase) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "phase out of range");
+  CK(cudaSetDevice(device));
+  if (wait_q >= 0)
+    for (int side = 0; side < 2; ++side)
+      if (!ipc_peer[side].ev.empty()) CK(cudaStreamWaitEvent(stream, ipc_peer[side].ev[wait_q], 0));
+  if (eta_tilde != 0.0) enqueue_sweep_phase(scheme, eta_tilde, dt, q < nphase / 2 ? 0 : 1, q % (nphase / 2));
+  CK(cudaEventRecord(phase_events[q], stream));
 }
 
 void DevSystem::build_colour_lists() {

@@ -42,6 +42,22 @@ struct DBuf {
 
 struct SweepPlan;  // damping.cu
 
+// A slab's export for cross-process linking: its velocity arrays and colour-phase events as
+// CUDA IPC handles (tlsph_dev_ipc_export); plain bytes, exchanged by the host.
+struct IpcExport {
+  static constexpr unsigned kMagic = 0x74736c31u;  // "tsl1"
+  unsigned magic;
+  int dim, device, nphase;
+  cudaIpcMemHandle_t vel[3];
+  cudaIpcEventHandle_t ev[54];
+};
+// A neighbour opened from its export (mapped velocity arrays, its phase events)
+struct IpcPeer {
+  std::vector<void*> mem;
+  std::vector<cudaEvent_t> ev;
+  void close();
+};
+
 class DevSystem {
  public:
   int D = 3;
@@ -177,6 +193,14 @@ class DevSystem {
   void build_colour_lists();  // host sync: at construction and when the task range changes
   void build_own_mask();      // own[] from the task range (x-slab ownership)
   void link_peer(int side, DevSystem& peer);  // sweep.cu
+  void link_peer_arrays(int side, const long long* peer_cell_start, double* const* peer_vel);
+  // cross-process linking (tlsph_dev_ipc_*), sweep.cu
+  void ensure_phase_events(bool interprocess);
+  void ipc_export(IpcExport* out);
+  void link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start);
+  void sweep_phase_ipc(int scheme, double eta_tilde, double dt, int q, int wait_q);
+  IpcPeer ipc_peer[2];
+  bool phase_events_ipc = false;
   // x-slab halo columns (sweep.cu)
   long long column_count(int x) const;
   int column_width(int field) const;  // doubles per particle of a column field

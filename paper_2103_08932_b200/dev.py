@@ -128,6 +128,12 @@ def lib():
     L.tlsph_dev_set_reduction.argtypes = [P, I]
     L.tlsph_dev_sweep_linked.argtypes = [C.POINTER(P), I, I, C.c_double, C.c_double, I]
     L.tlsph_dev_set_sweep_tiling.argtypes = [P, I]
+    L.tlsph_dev_ipc_size.argtypes = []
+    L.tlsph_dev_ipc_size.restype = S
+    L.tlsph_dev_ipc_export.argtypes = [P, C.c_void_p]
+    L.tlsph_dev_link_peer_ipc.argtypes = [P, I, C.c_char_p, C.POINTER(C.c_int64)]
+    L.tlsph_dev_sweep_phase_ipc.argtypes = [P, I, C.c_double, C.c_double, I, I]
+    L.tlsph_dev_synchronize.argtypes = [P]
     L.tlsph_dev_grid_info.argtypes = [P, C.POINTER(I), D, D, C.POINTER(C.c_int64)]
     L.tlsph_dev_grid_cells.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.tlsph_dev_get_neighborhood.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D, D, D, D]
@@ -369,6 +375,26 @@ class DeviceSystem:
     def damping_phase(self, scheme, eta_tilde, dt, pass_, index):
         _check(lib().tlsph_dev_damping_phase(self._h, SCHEMES[scheme], float(eta_tilde), float(dt), int(pass_),
                                              int(index)))
+
+    # ---- cross-process linking (one process per GPU; slabs.IpcSlabSweep)
+    def ipc_export(self):
+        """This slab's velocity arrays and phase events as CUDA IPC handles (opaque bytes)."""
+        buf = C.create_string_buffer(int(lib().tlsph_dev_ipc_size()))
+        _check(lib().tlsph_dev_ipc_export(self._h, C.cast(buf, C.c_void_p)))
+        return buf.raw
+
+    def link_peer_ipc(self, side, blob, peer_cell_start):
+        """Fused exchange with a slab of another process: its export and its cell table."""
+        cs = np.ascontiguousarray(peer_cell_start, dtype=np.int64)
+        _check(lib().tlsph_dev_link_peer_ipc(self._h, int(side), bytes(blob), cs.ctypes.data_as(C.POINTER(C.c_int64))))
+
+    def sweep_phase_ipc(self, scheme, eta_tilde, dt, q, wait_q):
+        """Enqueue colour phase q after the linked neighbours' phase wait_q (-1: no wait); asynchronous."""
+        _check(lib().tlsph_dev_sweep_phase_ipc(self._h, SCHEMES[scheme], float(eta_tilde), float(dt), int(q),
+                                               int(wait_q)))
+
+    def synchronize(self):
+        _check(lib().tlsph_dev_synchronize(self._h))
 
     def link_peer(self, side, peer):
         """Fused exchange: this slab's phases also store the shared columns into `peer` (0 left, 1 right)."""

@@ -40,6 +40,7 @@ over those two groups.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -321,6 +322,101 @@ def sweep_linked(systems, scheme, eta_tilde, dt, count=1):
     if eta_tilde == 0.0:
         return 0.0
     return dev.sweep_linked(systems, scheme, eta_tilde, dt, count)
+
+
+class PhaseCounters:
+    """Per-slab counts of enqueued colour phases, shared by the processes of one job through a file
+    in /dev/shm (each process writes only its own slot). Before a process enqueues phase g with a
+    wait on its neighbours' phase g-1 events, their counters must show g: cudaStreamWaitEvent binds
+    to the event's most recent record at call time."""
+
+    def __init__(self, path, world, create):
+        import numpy as np
+
+        mode = "w+" if create else "r+"
+        self.path = path
+        self.c = np.memmap(path, dtype=np.int64, mode=mode, shape=(world,))
+        if create:
+            self.c[:] = 0
+            self.c.flush()
+
+    def set(self, rank, value):
+        self.c[rank] = value
+
+    def wait(self, ranks, value, timeout=60.0):
+        import time
+
+        t0 = time.perf_counter()
+        while any(int(self.c[r]) < value for r in ranks):
+            if time.perf_counter() - t0 > timeout:
+                raise TimeoutError(f"slab phase handshake: neighbours {ranks} did not reach phase {value}")
+
+    def close(self, unlink):
+        del self.c
+        if unlink:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+
+
+class IpcSlabSweep:
+    """One process's slab of a decomposed sweep, fused with its neighbours across processes
+    (one process per GPU, e.g. under torchrun): the neighbours' velocity arrays are mapped through
+    CUDA IPC, so each phase kernel stores the shared columns straight into them (over NVLink between
+    GPUs), and the per-phase barrier is a stream wait on the neighbours' IPC phase events -- no host
+    synchronisation between phases, only a host-side counter handshake that keeps every wait bound
+    to the intended phase. `group`: torch.distributed process group for the one-time exchange of
+    exports and cell tables (default group if None)."""
+
+    def __init__(self, system, rank, world, group=None):
+        import uuid
+
+        import torch.distributed as dist
+
+        self.d, self.rank, self.world = system, rank, world
+        blob = system.ipc_export()
+        cell_start = system.grid()["cell_start"]
+        items = [None] * world
+        dist.all_gather_object(items, (blob, cell_start), group=group)
+        token = [uuid.uuid4().hex if rank == 0 else None]
+        dist.broadcast_object_list(token, src=0, group=group)
+        path = os.path.join("/dev/shm", f"tlsph_slab_{token[0]}")
+        if rank == 0:
+            self.counters = PhaseCounters(path, world, create=True)
+        dist.barrier(group=group)
+        if rank != 0:
+            self.counters = PhaseCounters(path, world, create=False)
+        dist.barrier(group=group)
+        self.neighbours = [r for r in (rank - 1, rank + 1) if 0 <= r < world]
+        if rank > 0:
+            system.link_peer_ipc(0, *items[rank - 1])
+        if rank + 1 < world:
+            system.link_peer_ipc(1, *items[rank + 1])
+        dist.barrier(group=group)  # every slab linked before any phase runs
+        self.enqueued = 0
+        self.nphase = 2 * 3 ** system.dim
+        self._group = group
+
+    def sweep(self, scheme, eta_tilde, dt, count=1):
+        """`count` sweeps, enqueued phase by phase; returns after this slab's last phase ran."""
+        if eta_tilde == 0.0:
+            return
+        for _ in range(count):
+            for q in range(self.nphase):
+                g = self.enqueued
+                if g > 0:
+                    self.counters.wait(self.neighbours, g)
+                self.d.sweep_phase_ipc(scheme, eta_tilde, dt, q, (q - 1) % self.nphase if g > 0 else -1)
+                self.enqueued = g + 1
+                self.counters.set(self.rank, self.enqueued)
+        self.d.synchronize()
+
+    def close(self):
+        import torch.distributed as dist
+
+        dist.barrier(group=self._group)
+        self.counters.close(unlink=self.rank == 0)
 
 
 class SlabSweep:

@@ -506,3 +506,92 @@ def test_slab_loop_equals_undivided_device_loop(dim, world, mode):
         for s, e in zip(parts, engines):
             own = (cols[s.ids] >= s.x0) & (cols[s.ids] < s.x1)
             assert np.array_equal(e.d.get(name)[own], want[s.ids[own]]), name
+
+
+# ---------------------------------------------------------------- cross-process phase handshake
+def _counter_rank(rank, world, port, result_dir):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        path = os.path.join(result_dir, "counters")
+        if rank == 0:
+            c = slabs.PhaseCounters(path, world, create=True)
+        dist.barrier()
+        if rank != 0:
+            c = slabs.PhaseCounters(path, world, create=False)
+        dist.barrier()
+        nb = [r for r in (rank - 1, rank + 1) if 0 <= r < world]
+        seen = []
+        for g in range(200):  # the IpcSlabSweep discipline: wait for the neighbours' phase g-1
+            if g > 0:
+                c.wait(nb, g, timeout=30.0)
+                seen.append(min(int(c.c[r]) for r in nb))
+            c.set(rank, g + 1)
+        np.save(os.path.join(result_dir, f"seen{rank}.npy"), np.array(seen))
+        dist.barrier()
+        c.close(unlink=rank == 0)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_phase_counter_handshake(tmp_path, world):
+    """Host side of the cross-process fused sweep: no rank ever runs more than one phase ahead of
+    a neighbour, and the lockstep never deadlocks."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_counter_rank, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        seen = np.load(os.path.join(tmp_path, f"seen{r}.npy"))
+        assert np.all(seen >= np.arange(1, 200)) and np.all(seen <= np.arange(1, 200) + 1)
+
+
+def _ipc_rank(rank, world, port, dim, scheme, mode, result_dir):
+    import torch.distributed as dist
+
+    from paper_2103_08932_b200 import dev
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev.select_device(0)  # one GPU: every process's slab on device 0 (IPC within the device)
+        r0, cons, v = body(dim, [30, 6, 5] if dim == 3 else [40, 9])
+        grid, parts = slabs.decompose(r0, H, world)
+        d = slabs.make_device_slab(grid, parts[rank], r0, DP ** dim, RHO, H, cons)
+        d.set_reduction(mode)
+        d.set("v", v[parts[rank].ids])
+        sweep = slabs.IpcSlabSweep(d, rank, world)
+        sweep.sweep(scheme, 160.0, 1e-4, count=2)
+        sweep.sweep(scheme, 160.0, 1e-4, count=1)
+        np.save(os.path.join(result_dir, f"v{rank}.npy"), d.get("v"))
+        np.save(os.path.join(result_dir, f"ids{rank}.npy"), parts[rank].ids)
+        sweep.close()
+        del d
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,world,mode,scheme", [(3, 2, "fast", "particle_split"), (3, 3, "ordered", "particle_split"),
+                                                   (2, 3, "fast", "particle_split"), (3, 2, "fast", "pairwise_split")])
+def test_ipc_slabs_equal_undivided_device(tmp_path, dim, world, mode, scheme):
+    """One process per slab (all on GPU 0 here), fused exchange through CUDA IPC mappings and IPC
+    phase events, host-side counter handshake: bitwise the undivided sweep."""
+    import torch.multiprocessing as mp
+
+    from paper_2103_08932_b200 import dev
+
+    mp.spawn(_ipc_rank, args=(world, _free_port(), dim, scheme, mode, str(tmp_path)), nprocs=world, join=True)
+    r0, cons, v = body(dim, [30, 6, 5] if dim == 3 else [40, 9])
+    whole = dev.DeviceSystem(r0, DP ** dim, RHO, H, cons)
+    whole.set_reduction(mode)
+    whole.set("v", v)
+    whole.damping_sweep(scheme, 160.0, 1e-4, count=3)
+    ref = whole.get("v")
+    for r in range(world):
+        ids = np.load(os.path.join(tmp_path, f"ids{r}.npy"))
+        assert np.array_equal(np.load(os.path.join(tmp_path, f"v{r}.npy")), ref[ids])
