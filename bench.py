@@ -135,7 +135,7 @@ def barrier_and_max(value, ws):
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -365,6 +365,65 @@ def sweep_at_scale(args, ws, rank):
                          "traffic": traffic, "peak_source": peak_src}}
 
 
+def sweep_sharded(args, ws, rank):
+    """N > 1: BASELINE cfg5's weak-scaling run. A body of ws x `--scale-layers` x-layers of 250 x 250
+    (dp 0.004; 15.6 M particles per GPU at the default 250) is x-slab decomposed, one slab per rank,
+    with the fused exchange across processes (slabs.IpcSlabSweep: CUDA IPC mappings of the
+    neighbours' velocity arrays, phase kernels storing shared columns into them over NVLink, the
+    per-phase barrier as stream waits on the neighbours' IPC phase events). Device time per rank
+    (events on the slab's stream), max over ranks; DPU over the whole body. Compare with
+    `sweep_at_scale` of the N = 1 line for the weak-scaling efficiency of the decomposed sweep."""
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2103_08932_b200 import scenarios as S
+    from paper_2103_08932_b200 import slabs
+
+    layers, dp = args.scale_layers, 0.004
+    r0, _ = S.box_lattice([0.0, 0.0, 0.0], [layers * ws * dp, 1.0, 1.0], dp)
+    h = 1.3 * dp
+    cons = (r0[:, 0] < 5 * dp).astype(np.uint8)
+    grid, parts = slabs.decompose(r0, h, ws)
+    part = parts[rank]
+    d = slabs.make_device_slab(grid, part, r0, dp ** 3, S.RHO0, h, cons)
+    cols = slabs.cell_columns(r0[part.ids], grid[0], grid[2], grid[1][0])
+    own = (cols >= part.x0) & (cols < part.x1)
+    cons_local = cons[part.ids]
+    del r0, cons
+    d.set_reduction("fast")
+    off = d.row_offsets()
+    rows = off[1:] - off[:-1]
+    s_free_local = int(rows[own & (cons_local == 0)].sum())
+    gloo = dist.new_group(backend="gloo")
+    sweep = slabs.IpcSlabSweep(d, rank, ws, group=gloo)
+    eta_t, dt = S.eta_for(h), 1e-5
+    sweep.sweep("particle_split", eta_t, dt, count=2)
+    sweeps = max(3, min(args.scale_sweeps, 50))
+    dist.barrier(group=gloo)
+    d.timer_start()
+    sweep.sweep("particle_split", eta_t, dt, count=sweeps)
+    t = d.timer_stop()
+    t_max = barrier_and_max(t, ws)
+    tot = [None] * ws
+    dist.all_gather_object(tot, (s_free_local, int(own.sum())), group=gloo)
+    s_free = sum(x[0] for x in tot)
+    n_owned = sum(x[1] for x in tot)
+    sweep.close()
+    del d
+    peak, peak_src = load_peaks()
+    b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_owned)  # whole body; per GPU divide by ws
+    return {"metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
+            "value": 2 * s_free * sweeps / t_max, "unit": "DPU/s", "sweeps": sweeps, "ms_per_sweep": t_max / sweeps * 1e3,
+            "scaling": "weak",
+            "config": {"workload": f"cfg5 weak scaling: {layers * ws} x 250 x 250 lattice (dp 0.004), "
+                                   f"{ws} x-slabs, one per GPU", "particles": n_owned, "slots_free": s_free,
+                       "exchange": "fused: CUDA IPC peer stores of shared columns + IPC phase events (no host sync)"},
+            "roofline": {"bound": "hbm", "achieved_per_gpu": b_sweep / ws / (t_max / sweeps) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": b_sweep / ws / (t_max / sweeps) / 1e9 / peak,
+                         "peak_source": peak_src},
+            "timing": "CUDA events on each slab's stream between a barrier and the last phase, max over ranks"}
+
+
 def cfg3_oracle_steps(threads, steps):
     """Reference CPU path (oracle port, OpenMP) over the first `steps` cfg3 loop steps."""
     from oracle import oracle as O
@@ -443,15 +502,22 @@ def main():
     ap.add_argument("--no-ps", action="store_true", help="skip the particle-steps/s leg")
     ap.add_argument("--scale-sweeps", type=int, default=10, help="sweeps of the large-body (cfg5-weak) leg")
     ap.add_argument("--no-scale", action="store_true", help="skip the large-body sweep leg")
+    ap.add_argument("--scale-layers", type=int, default=250,
+                    help="x-layers of 250 x 250 per GPU of the N > 1 sharded leg (cfg5 weak scaling)")
     ap.add_argument("--parity-sweeps", type=int, default=500, help="cfg2 sweeps of the GPU-vs-oracle check (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     ws, rank, local = dist_env()
+    # TLSPH_BENCH_ONE_DEVICE=1: every rank on GPU 0 over gloo (protocol tests of the N > 1 path on a
+    # one-GPU box; small --scale-layers)
+    one_device = os.environ.get("TLSPH_BENCH_ONE_DEVICE") == "1"
+    if one_device:
+        local = 0
     if ws > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if one_device else "nccl")
     if args.impl == "reference":
         out = run_reference(args, ws, rank)
         if out is not None and not args.no_ps:
@@ -463,7 +529,12 @@ def main():
         if not args.no_ps:
             out["particle_steps"] = particle_steps(args, ws, rank)
         if not args.no_scale:
-            out["sweep_at_scale"] = sweep_at_scale(args, ws, rank)
+            if ws == 1:
+                out["sweep_at_scale"] = sweep_at_scale(args, ws, rank)
+            else:
+                sh = sweep_sharded(args, ws, rank)
+                if out is not None:
+                    out["sweep_sharded"] = sh
     if rank == 0 and out is not None:
         print(json.dumps(out))
     if ws > 1:

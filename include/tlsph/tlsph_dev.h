@@ -158,6 +158,11 @@ tlsph_status tlsph_dev_link_peer_ipc(tlsph_dev* dev, int side, const void* peer_
 tlsph_status tlsph_dev_sweep_phase_ipc(tlsph_dev* dev, tlsph_dev_scheme scheme, double eta_tilde, double dt, int q,
                                        int wait_q);
 tlsph_status tlsph_dev_synchronize(tlsph_dev* dev);
+/* Device time of a span of work on the slab's stream: tlsph_dev_timer_start
+ * records a start event, tlsph_dev_timer_stop records the end, waits for it and
+ * returns the elapsed seconds (negative on error). */
+tlsph_status tlsph_dev_timer_start(tlsph_dev* dev);
+double tlsph_dev_timer_stop(tlsph_dev* dev);
 tlsph_status tlsph_dev_sweep_linked(tlsph_dev* const* slabs, int nslabs, tlsph_dev_scheme scheme, double eta_tilde,
                                     double dt, int count);
 int64_t tlsph_dev_column_count(const tlsph_dev* dev, int x);

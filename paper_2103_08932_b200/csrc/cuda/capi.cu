@@ -233,6 +233,31 @@ tlsph_status tlsph_dev_synchronize(tlsph_dev* dev) {
   });
 }
 
+tlsph_status tlsph_dev_timer_start(tlsph_dev* dev) {
+  return guarded([&] {
+    DevSystem& s = sys(dev);
+    CK(cudaSetDevice(s.device));
+    for (cudaEvent_t& e : s.timer_ev)
+      if (!e) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(s.timer_ev[0], s.stream));
+  });
+}
+
+double tlsph_dev_timer_stop(tlsph_dev* dev) {
+  double out = -1.0;
+  const tlsph_status st = guarded([&] {
+    DevSystem& s = sys(dev);
+    if (!s.timer_ev[0]) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "timer not started");
+    CK(cudaSetDevice(s.device));
+    CK(cudaEventRecord(s.timer_ev[1], s.stream));
+    CK(cudaEventSynchronize(s.timer_ev[1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s.timer_ev[0], s.timer_ev[1]));
+    out = ms * 1e-3;
+  });
+  return st == TLSPH_OK ? out : -1.0;
+}
+
 tlsph_status tlsph_dev_link_peer(tlsph_dev* dev, int side, tlsph_dev* peer) {
   return guarded([&] {
     if (!peer) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer must not be null");

@@ -552,6 +552,8 @@ unsigned grid_for(long long n, int block) { return static_cast<unsigned>((n + bl
 
 // ====================================================================== DevSystem
 DevSystem::~DevSystem() {
+  for (cudaEvent_t e : timer_ev)
+    if (e) cudaEventDestroy(e);
   for (IpcPeer& ip : ipc_peer) ip.close();
   for (cudaEvent_t e : phase_events) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);

@@ -200,6 +200,7 @@ class DevSystem {
   void link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start);
   void sweep_phase_ipc(int scheme, double eta_tilde, double dt, int q, int wait_q);
   IpcPeer ipc_peer[2];
+  cudaEvent_t timer_ev[2] = {nullptr, nullptr};  // tlsph_dev_timer_start / _stop
   bool phase_events_ipc = false;
   // x-slab halo columns (sweep.cu)
   long long column_count(int x) const;

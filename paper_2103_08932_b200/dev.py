@@ -134,6 +134,9 @@ def lib():
     L.tlsph_dev_link_peer_ipc.argtypes = [P, I, C.c_char_p, C.POINTER(C.c_int64)]
     L.tlsph_dev_sweep_phase_ipc.argtypes = [P, I, C.c_double, C.c_double, I, I]
     L.tlsph_dev_synchronize.argtypes = [P]
+    L.tlsph_dev_timer_start.argtypes = [P]
+    L.tlsph_dev_timer_stop.argtypes = [P]
+    L.tlsph_dev_timer_stop.restype = C.c_double
     L.tlsph_dev_grid_info.argtypes = [P, C.POINTER(I), D, D, C.POINTER(C.c_int64)]
     L.tlsph_dev_grid_cells.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.tlsph_dev_get_neighborhood.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), D, D, D, D]
@@ -395,6 +398,16 @@ class DeviceSystem:
 
     def synchronize(self):
         _check(lib().tlsph_dev_synchronize(self._h))
+
+    def timer_start(self):
+        """Start a device-time span on this system's stream (timer_stop returns its seconds)."""
+        _check(lib().tlsph_dev_timer_start(self._h))
+
+    def timer_stop(self):
+        t = float(lib().tlsph_dev_timer_stop(self._h))
+        if t < 0:
+            raise TlsphError(1, lib().tlsph_dev_last_error().decode())
+        return t
 
     def link_peer(self, side, peer):
         """Fused exchange: this slab's phases also store the shared columns into `peer` (0 left, 1 right)."""
