@@ -10,9 +10,14 @@ Workload (default, the config BASELINE's metric is quoted on that fits one GPU):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3]
   python bench.py --impl reference ...   # the reference CPU path (oracle port, all host cores)
 
-Multi-GPU (torchrun, one rank per GPU): every rank runs its own cfg2 body
-(replicas: the single 64^3 block is not slab-partitioned in round 1), timed
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own cfg2 body for the
+headline `value` (replicas of the 64^3 block, so per-GPU work matches N = 1), timed
 with CUDA events on the library's stream, max over ranks; value = total DPU / max time.
+The line adds `sweep_sharded`: BASELINE cfg5's weak scaling, one x-slab of an
+N x 250-layer body per rank with the fused cross-process exchange (slabs.IpcSlabSweep);
+at N = 1 `sweep_at_scale` times the same per-GPU body undivided.
+Other legs: `particle_steps` (cfg3 full loop, PS/s), `parity` (500 cfg2 sweeps vs the
+oracle), `cpu_baseline` (oracle port on the host cores).
 """
 from __future__ import annotations
 
