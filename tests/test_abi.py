@@ -86,3 +86,24 @@ def test_no_gpu_fails_loudly():
     with pytest.raises(dev.TlsphError) as e:
         dev.DeviceSystem(np.zeros((2, 2)) + [[0, 0], [0.1, 0]], 1.0, 1.0, 0.1)
     assert e.value.kind == "internal-error"
+
+
+def test_device_abi_argument_validation_without_gpu():
+    """The slab-linking and timing entry points validate their arguments on the host, exception-free
+    (status codes, thread-local message), before touching a device."""
+    L = C.CDLL(os.path.join(LIB, "libtlsph_cuda.so"))
+    L.tlsph_dev_last_error.restype = C.c_char_p
+    L.tlsph_dev_ipc_size.restype = C.c_size_t
+    L.tlsph_dev_timer_stop.restype = C.c_double
+    L.tlsph_dev_sweep_linked.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int]
+    # IpcExport: header + 3 memory handles + 54 event handles (64 bytes each)
+    assert L.tlsph_dev_ipc_size() >= 16 + 57 * 64
+    assert L.tlsph_dev_sweep_linked(None, 0, 1, 1.0, 1e-4, 1) == 1
+    assert b"no slabs" in L.tlsph_dev_last_error()
+    arr = (C.c_void_p * 1)(None)
+    assert L.tlsph_dev_sweep_linked(arr, 1, 1, 1.0, 1e-4, 1) == 1
+    assert b"null slab" in L.tlsph_dev_last_error()
+    assert L.tlsph_dev_sweep_linked(arr, 1, 0, 1.0, 1e-4, 1) == 1  # the explicit scheme is not swept
+    assert L.tlsph_dev_ipc_export(None, None) == 1
+    assert L.tlsph_dev_link_peer_ipc(None, 0, None, None) == 1
+    assert L.tlsph_dev_timer_stop(None) < 0
