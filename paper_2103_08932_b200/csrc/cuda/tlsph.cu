@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include "system.cuh"
+#include "tma.cuh"
 
 namespace tlsph_cuda {
 
@@ -115,8 +116,14 @@ struct SlotView {
   }
 };
 
+// PDL (FAST passes B and C): launched with programmatic stream serialization, the kernel lets
+// the next pass launch early and waits for the previous one before reading its output.
+#ifndef TLSPH_TL_PDL
+#define TLSPH_TL_PDL 1
+#endif
 template <int D, int G, int U, bool POST>
 __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars* sc, double dt, int loop) {
+  if (TLSPH_TL_PDL && G > 1) grid_dependency_wait();  // v of pass B's kick, F of pass A
   if (loop && sc->halt) return;
   const double half = 0.5 * (loop ? sc->dt : dt);
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -230,6 +237,7 @@ __global__ void k_update_density(DFields f, DScalars* sc) {
 // PRE: fused head of verlet pass A (density from J^n, half-kick, constraints).
 template <int D, bool PRE>
 __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int loop) {
+  if (TLSPH_TL_PDL) grid_launch_dependents();  // pass B may launch and wait
   if (loop && sc->halt) return;
   const double half = 0.5 * (loop ? sc->dt : dt);
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -287,6 +295,10 @@ __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int 
 // KICK: fused tail of verlet pass B (v += dt a, constraints).
 template <int D, int G, int U, bool KICK>
 __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, double dt_arg, int loop) {
+  if (TLSPH_TL_PDL && G > 1) {
+    grid_launch_dependents();  // pass C may launch and wait
+    grid_dependency_wait();    // pass A's records
+  }
   if (loop && sc->halt) return;
   const double dt = loop ? sc->dt : dt_arg;
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -507,6 +519,20 @@ void DevSystem::momentum_rhs(const DMaterial& mat) {
 }
 
 // Enqueues one verlet pass (0: A, 1: B, 2: C) on the handle's stream (no sync).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), long long threads, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_for(threads, 128));
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = TLSPH_TL_PDL ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop, int pass) {
   DFields f = s.fields();
   const long long n = s.n;
@@ -515,15 +541,15 @@ void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop
   if (s.D == 2) {
     if (pass == 0) k_stress<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
     else if (pass == 1 && ord) k_momentum_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    else if (pass == 1) k_momentum<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1) launch_pdl(k_momentum<2, 4, true>, n * 4, st, f, s.scal.p, dt, loop);
     else if (ord) k_deformation_rate_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    else k_deformation_rate<2, 4, true><<<grid_for(n * 4, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else launch_pdl(k_deformation_rate<2, 4, true>, n * 4, st, f, s.scal.p, dt, loop);
   } else {
     if (pass == 0) k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
     else if (pass == 1 && ord) k_momentum_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    else if (pass == 1) k_momentum<3, kGB3, true><<<grid_for(n * kGB3, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1) launch_pdl(k_momentum<3, kGB3, true>, n * kGB3, st, f, s.scal.p, dt, loop);
     else if (ord) k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
-    else k_deformation_rate<3, kGC3, true><<<grid_for(n * kGC3, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else launch_pdl(k_deformation_rate<3, kGC3, true>, n * kGC3, st, f, s.scal.p, dt, loop);
   }
 }
 
