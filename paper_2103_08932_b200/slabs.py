@@ -463,11 +463,14 @@ def step_dt(spec, vmax, amax, dim):
     return dt
 
 
-def run_loop(group, spec, dim):
+def run_loop(group, spec, dim, sweeper=None):
     """runner.cpp:341-391 over the slabs of a group, step for step as DevSystem::run executes
     it: step_begin (finite check of the previous step, dt from the combined maxima), verlet
     passes A, B, C with the halo refreshes between them, the random-choice sweep. The slabs
-    must be prepared (runner.cpp:306-312) after their task ranges are set."""
+    must be prepared (runner.cpp:306-312) after their task ranges are set. `sweeper(scheme,
+    eta_tilde, dt)`, if given, runs the damped steps' sweeps instead of the group's per-phase
+    exchange -- the fused forms (`sweep_linked` over peer-linked slabs, `IpcSlabSweep.sweep`),
+    which leave the shared columns current on both sides as the exchange does."""
     from . import dev
 
     if spec.scheme not in ("particle_split", "pairwise_split"):
@@ -490,7 +493,10 @@ def run_loop(group, spec, dim):
             group.exchange(halo, "velocity")
             group.each(lambda e: e.verlet_pass(spec.material, dt, 2))
         if flags[k]:
-            sweep(group, spec.scheme, eta_tilde, dt, dim)
+            if sweeper is not None:
+                sweeper(spec.scheme, eta_tilde, dt)
+            else:
+                sweep(group, spec.scheme, eta_tilde, dt, dim)
         t = t + dt
     group.reduce(False, spec.steps)  # check_finite of the last step
     return {"steps": spec.steps, "damped": int(flags.sum()), "t": t, "last_dt": dt}

@@ -470,7 +470,8 @@ def test_gloo_toy_loop_equals_undivided(tmp_path, world):
 @pytest.mark.gpu
 @pytest.mark.parametrize("dim,world,mode", [(2, 2, "ordered"), (2, 3, "fast"), (3, 2, "ordered"),
                                             (3, 3, "fast")])
-def test_slab_loop_equals_undivided_device_loop(dim, world, mode):
+@pytest.mark.parametrize("fused", [False, True])
+def test_slab_loop_equals_undivided_device_loop(dim, world, mode, fused):
     """TL-SPH passes on owned particles + halo refreshes + decomposed random-choice sweeps
     reproduce tlsph_dev_run on the undivided body bit for bit (elastic, gravity, clamped root)."""
     from paper_2103_08932_b200 import dev, scenarios as S
@@ -497,8 +498,13 @@ def test_slab_loop_equals_undivided_device_loop(dim, world, mode):
         d.set("body", g[s.ids])
         d.prepare(mat)
         engines.append(slabs.DeviceSlabEngine(d, dim))
+    sweeper = None
+    if fused:  # damped steps through the linked sweep (peer stores, device-side phase barrier)
+        systems = [e.d for e in engines]
+        slabs.link_peers(systems)
+        sweeper = lambda scheme, et, dt: slabs.sweep_linked(systems, scheme, et, dt)  # noqa: E731
     out = slabs.run_loop(slabs.LocalGroup(engines, [(s.x0, s.x1) for s in parts]),
-                         slabs.LoopSpec(mat, H, eta, alpha, steps, seed=seed), dim)
+                         slabs.LoopSpec(mat, H, eta, alpha, steps, seed=seed), dim, sweeper=sweeper)
     assert out["damped"] == ref["damped"] > 0 and out["t"] == ref["t"] and out["last_dt"] == ref["last_dt"]
     cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
     for name in ("v", "r", "F", "dFdt", "rho", "a"):
