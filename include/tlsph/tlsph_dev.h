@@ -187,6 +187,16 @@ tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const do
 tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host);
 tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode);
 
+/* Per-step re-sort (BASELINE cfg4): with `on`, every step of tlsph_dev_run
+ * first rebuilds a storage permutation keyed by each particle's CURRENT-position
+ * cell (the r0 grid, out-of-grid positions clamped to border cells): cell_start
+ * and the particles of each cell in ascending storage order. The colouring,
+ * neighbourhoods and sweep order stay r0-based, so no result changes; the
+ * rebuild's time is part of the step. tlsph_dev_current_cells returns the last
+ * one: cell_start (ncells + 1) and the reference ids in current-cell order (n). */
+tlsph_status tlsph_dev_set_resort(tlsph_dev* dev, int on);
+tlsph_status tlsph_dev_current_cells(const tlsph_dev* dev, int64_t* cell_start, int32_t* order);
+
 /* Where the FAST particle-split sweep keeps a cell's slot block (pair factors,
  * stencil indices) while its chain runs: staged in shared memory (four cells
  * per SM; the latency-bound form for colours of up to ~600 cells) or streamed

@@ -345,6 +345,17 @@ tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode) {
   });
 }
 
+tlsph_status tlsph_dev_set_resort(tlsph_dev* dev, int on) {
+  return guarded([&] { sys(dev).set_resort(on != 0); });
+}
+
+tlsph_status tlsph_dev_current_cells(const tlsph_dev* dev, int64_t* cell_start, int32_t* order) {
+  return guarded([&] {
+    if (!cell_start || !order) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null output array");
+    sys(dev).current_cells(cell_start, order);
+  });
+}
+
 tlsph_status tlsph_dev_set_sweep_tiling(tlsph_dev* dev, tlsph_dev_sweep_tiling mode) {
   return guarded([&] {
     if (mode != TLSPH_SWEEP_TILING_AUTO && mode != TLSPH_SWEEP_TILING_STAGED && mode != TLSPH_SWEEP_TILING_STREAMED)

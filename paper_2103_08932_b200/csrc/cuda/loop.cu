@@ -249,7 +249,10 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     if (D == 2) k_step_begin<2><<<nb, 256, 0, stream>>>(f, scal.p, red.p, finalize);
     else k_step_begin<3><<<nb, 256, 0, stream>>>(f, scal.p, red.p, finalize);
   };
-  capture(stream, g_begin, [&] { begin_launch(0); });
+  capture(stream, g_begin, [&] {
+    begin_launch(0);
+    enqueue_resort();  // BASELINE cfg4's per-step re-sort (no-op unless set_resort)
+  });
   if (p.elastic) capture(stream, g_elastic, [&] { enqueue_verlet(*this, mat, 0.0, 1); });
   if (damping_active) {
     capture(stream, g_damp, [&] {

@@ -139,6 +139,21 @@ __global__ void k_cell_scatter(const int* __restrict__ key, long long n, const l
   perm[pos] = static_cast<int>(i);
 }
 
+// Current-position cell key of every particle (the per-step re-sort, DevSystem::enqueue_resort).
+template <int D>
+__global__ void k_cell_keys_current(DFields f, int* __restrict__ key, int* __restrict__ count) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) p[d] = f.r[d][i];
+  int c[D];
+  cell_coords<D>(p, f.origin, f.cell, f.dims, c);
+  const int k = static_cast<int>(cell_linear<D>(c, f.dims));
+  key[i] = k;
+  atomicAdd(&count[k], 1);
+}
+
 // Insertion sort of each cell's ids: the atomic scatter above is unordered,
 // the reference lists ascending ids per cell (neighbors.cpp:52-57).
 __global__ void k_cell_sort(const long long* __restrict__ cell_start, long long ncells, int* __restrict__ perm,
@@ -846,6 +861,58 @@ void DevSystem::refresh_minvf() {
   }
   fold_valid = false;  // constrained particles are marked in the fold constants
   pkf_valid = false;   // pairwise factors use the masses
+}
+
+// ------------------------------------------------------------------ per-step re-sort (BASELINE cfg4)
+// A storage permutation keyed by the *current*-position cell (the same grid as the r0 cells, out-of-
+// grid positions clamped to the border cells): cell_start and the particles of each cell in ascending
+// storage order. The colouring, the CSR and the sweep order stay r0-based, so
+// this changes no result; with resort on, the device loop rebuilds it every step (its time is part of
+// the step). Capture-safe: preallocated buffers, no host synchronisation.
+void DevSystem::set_resort(bool on) {
+  resort = on;
+  if (!on) return;
+  const size_t N = static_cast<size_t>(n), C = static_cast<size_t>(ncells);
+  rs_key.alloc(N);
+  rs_perm.alloc(N);
+  rs_count.alloc(C);
+  rs_fill.alloc(C);
+  rs_start.alloc(C + 1);
+  const long long tiles = (ncells + 1 + kScanTile - 1) / kScanTile;
+  if (tiles + 1 > kScanTile) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "cell grid too large for the re-sort scan");
+  rs_sums.alloc(static_cast<size_t>(tiles) + 1);
+  rs_sums2.alloc(static_cast<size_t>(tiles) + 2);
+  rs_maxc.alloc(1);
+}
+
+void DevSystem::enqueue_resort() {
+  if (!resort) return;
+  const DFields f = fields();
+  CK(cudaMemsetAsync(rs_count.p, 0, static_cast<size_t>(ncells) * sizeof(int), stream));
+  CK(cudaMemsetAsync(rs_fill.p, 0, static_cast<size_t>(ncells) * sizeof(int), stream));
+  if (D == 2) k_cell_keys_current<2><<<grid_for(n, 256), 256, 0, stream>>>(f, rs_key.p, rs_count.p);
+  else k_cell_keys_current<3><<<grid_for(n, 256), 256, 0, stream>>>(f, rs_key.p, rs_count.p);
+  const long long n_out = ncells + 1, tiles = (n_out + kScanTile - 1) / kScanTile;
+  k_scan_tile<int><<<static_cast<unsigned>(tiles), kScanThreads, 0, stream>>>(rs_count.p, ncells, rs_start.p, n_out,
+                                                                              rs_sums.p);
+  if (tiles > 1) {
+    k_scan_tile<long long><<<1, kScanThreads, 0, stream>>>(rs_sums.p, tiles, rs_sums2.p, tiles + 1, rs_sums2.p + tiles + 1);
+    k_scan_add<<<static_cast<unsigned>((n_out + 255) / 256), 256, 0, stream>>>(rs_start.p, n_out, rs_sums2.p);
+  }
+  k_cell_scatter<<<grid_for(n, 256), 256, 0, stream>>>(rs_key.p, n, rs_start.p, rs_fill.p, rs_perm.p);
+  k_cell_sort<<<grid_for(ncells, 128), 128, 0, stream>>>(rs_start.p, ncells, rs_perm.p, rs_maxc.p);
+  CK_LAUNCH("re-sort");
+}
+
+void DevSystem::current_cells(int64_t* cell_start_h, int32_t* order_ref) const {
+  if (!resort) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "the per-step re-sort is off");
+  std::vector<int> sorted(static_cast<size_t>(n)), pm(static_cast<size_t>(n));
+  CK(cudaMemcpyAsync(cell_start_h, rs_start.p, static_cast<size_t>(ncells + 1) * sizeof(long long),
+                     cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(sorted.data(), rs_perm.p, sorted.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(pm.data(), perm.p, pm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  for (size_t k = 0; k < sorted.size(); ++k) order_ref[k] = pm[static_cast<size_t>(sorted[k])];
 }
 
 void DevSystem::compute_sweep_stats() {

@@ -130,6 +130,13 @@ class DevSystem {
   DBuf<double> qf;  // pf * RN(1/m_j), 0 for clamped j: the FAST sweep's per-slot mass factor
   DBuf<double> pf_sum, pf_sq;  // per-particle sums of pf and pf^2 (static)
   DBuf<int> snbr;              // rows in neighbour-index order (k_sorted_rows): FAST passes B, C
+  // per-step re-sort by current-position cell (set_resort / enqueue_resort, state.cu)
+  bool resort = false;
+  DBuf<int> rs_key, rs_perm, rs_count, rs_fill, rs_maxc;
+  DBuf<long long> rs_start, rs_sums, rs_sums2;
+  void set_resort(bool on);
+  void enqueue_resort();
+  void current_cells(int64_t* cell_start_h, int32_t* order_ref) const;
   DBuf<double> sdw, se0[3];
   DBuf<uint16_t> nloc;
   DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)

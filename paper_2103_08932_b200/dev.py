@@ -128,6 +128,8 @@ def lib():
     L.tlsph_dev_set_reduction.argtypes = [P, I]
     L.tlsph_dev_sweep_linked.argtypes = [C.POINTER(P), I, I, C.c_double, C.c_double, I]
     L.tlsph_dev_set_sweep_tiling.argtypes = [P, I]
+    L.tlsph_dev_set_resort.argtypes = [P, I]
+    L.tlsph_dev_current_cells.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.tlsph_dev_ipc_size.argtypes = []
     L.tlsph_dev_ipc_size.restype = S
     L.tlsph_dev_ipc_export.argtypes = [P, C.c_void_p]
@@ -257,6 +259,19 @@ class DeviceSystem:
 
     def set_reduction(self, mode):
         _check(lib().tlsph_dev_set_reduction(self._h, {"fast": 0, "ordered": 1}[mode]))
+
+    def set_resort(self, on=True):
+        """BASELINE cfg4's per-step re-sort: the device loop rebuilds the current-position cell list."""
+        _check(lib().tlsph_dev_set_resort(self._h, 1 if on else 0))
+
+    def current_cells(self):
+        """(cell_start, reference ids in current-cell order) of the last re-sort."""
+        g = self.grid()
+        cs = np.zeros(len(g["cell_start"]), dtype=np.int64)
+        order = np.zeros(self.n, dtype=np.int32)
+        _check(lib().tlsph_dev_current_cells(self._h, cs.ctypes.data_as(C.POINTER(C.c_int64)),
+                                             order.ctypes.data_as(C.POINTER(C.c_int32))))
+        return cs, order
 
     def set_sweep_tiling(self, mode):
         """FAST sweep slot-block placement: "auto", "staged" (shared memory) or "streamed" (L2)."""
