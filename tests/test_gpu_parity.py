@@ -527,3 +527,30 @@ def test_per_step_resort_is_a_pure_storage_permutation():
                 ids = np.nonzero(lin == k)[0]
                 assert np.array_equal(order[cs[k]:cs[k + 1]], ids[np.argsort(rank[ids])])
     assert np.array_equal(out[False][0], out[True][0]) and np.array_equal(out[False][1], out[True][1])
+
+
+def test_ke_stop_step_count_matches_reference_path():
+    """cfg3's stop rule (KE < ratio x peak KE after the peak) on a reduced-resolution beam (10,000
+    particles): FAST and ORDERED stop at the same step (north_star: +-1 %), and the ORDERED state at
+    that step matches the oracle run for the same number of steps (relative L2 1e-10)."""
+    cfg = S.cfg3(scale=4)
+    mat = S.material()
+    stops = {}
+    for mode in ("ordered", "fast"):
+        d = S.build_device(cfg, prepare=True)
+        d.set_reduction(mode)
+        r = d.run(mat, eta=cfg["eta"], alpha=cfg["alpha"], steps=200000, seed=cfg["seed"], ke_stop=True,
+                  ke_ratio=1e-3)
+        assert r["stopped_on_ke"]
+        stops[mode] = (r["steps"], d.get("v"), d.get("r"))
+    n_o, n_f = stops["ordered"][0], stops["fast"][0]
+    assert abs(n_f - n_o) <= max(1, 0.01 * n_o)
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+    o.set_material(S.E_MOD, S.NU, S.RHO0)
+    o.set("v", cfg["v0"])
+    o.set("body", cfg["body"])
+    o.prepare(threads=O.openmp_threads())
+    ro = o.run(eta=cfg["eta"], alpha=cfg["alpha"], steps=n_o, seed=cfg["seed"], threads=O.openmp_threads())
+    assert ro["steps"] == n_o
+    assert rel_l2(stops["ordered"][1], o.get("v")) <= TOL
+    assert rel_l2(stops["ordered"][2], o.get("r")) <= TOL
