@@ -195,6 +195,10 @@ tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode);
  * rebuild's time is part of the step. tlsph_dev_current_cells returns the last
  * one: cell_start (ncells + 1) and the reference ids in current-cell order (n). */
 tlsph_status tlsph_dev_set_resort(tlsph_dev* dev, int on);
+/* Completed steps and time of the last tlsph_dev_run, also when it stopped on an
+ * error (inverted element, NaN): the step the reference would have reported. */
+int64_t tlsph_dev_last_run_steps(const tlsph_dev* dev);
+double tlsph_dev_last_run_time(const tlsph_dev* dev);
 tlsph_status tlsph_dev_current_cells(const tlsph_dev* dev, int64_t* cell_start, int32_t* order);
 
 /* Where the FAST particle-split sweep keeps a cell's slot block (pair factors,

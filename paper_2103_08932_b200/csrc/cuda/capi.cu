@@ -509,6 +509,8 @@ tlsph_status tlsph_random_choice(double eta, double alpha, uint64_t seed, size_t
 }
 
 double tlsph_dev_last_elapsed(const tlsph_dev* dev) { return dev ? dev->sys.last_elapsed : -1.0; }
+int64_t tlsph_dev_last_run_steps(const tlsph_dev* dev) { return dev ? dev->sys.last_run_steps : -1; }
+double tlsph_dev_last_run_time(const tlsph_dev* dev) { return dev ? dev->sys.last_run_t : -1.0; }
 
 tlsph_status tlsph_dev_selftest_division(int64_t n, uint64_t seed, uint64_t* mismatches) {
   return guarded([&] {

@@ -332,6 +332,8 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     CK(cudaMemcpy(p.probe_out, probe_dev.p, ncopy * 4 * sizeof(double), cudaMemcpyDeviceToHost));
   }
   last_elapsed = loop_tot;
+  last_run_steps = static_cast<long long>(hs.steps);  // also when the loop stopped on an error
+  last_run_t = hs.t;
   loop_paused = hs.paused != 0 && !hs.failed;
   if (hs.failed) raise_if_failed("run");
 }

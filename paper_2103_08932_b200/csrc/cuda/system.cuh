@@ -150,6 +150,8 @@ class DevSystem {
   DBuf<int> tmp_i32;
   DBuf<double> red;        // reduction partials
   double last_elapsed = 0.0;
+  long long last_run_steps = 0;  // completed steps of the last tlsph_dev_run (also on failure)
+  double last_run_t = 0.0;
 
   DevSystem() = default;
   ~DevSystem();

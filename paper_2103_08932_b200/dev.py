@@ -129,6 +129,10 @@ def lib():
     L.tlsph_dev_sweep_linked.argtypes = [C.POINTER(P), I, I, C.c_double, C.c_double, I]
     L.tlsph_dev_set_sweep_tiling.argtypes = [P, I]
     L.tlsph_dev_set_resort.argtypes = [P, I]
+    L.tlsph_dev_last_run_steps.argtypes = [P]
+    L.tlsph_dev_last_run_steps.restype = C.c_int64
+    L.tlsph_dev_last_run_time.argtypes = [P]
+    L.tlsph_dev_last_run_time.restype = C.c_double
     L.tlsph_dev_current_cells.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.tlsph_dev_ipc_size.argtypes = []
     L.tlsph_dev_ipc_size.restype = S
@@ -481,6 +485,10 @@ class DeviceSystem:
         return {"steps": r.steps, "damped": r.damped_steps, "t": r.t, "last_dt": r.last_dt,
                 "elastic_s": r.elastic_seconds, "damping_s": r.damping_seconds, "total_s": r.total_seconds,
                 "peak_ke": r.peak_ke, "final_ke": r.final_ke, "stopped_on_ke": bool(r.stopped_on_ke)}
+
+    def last_run(self):
+        """(completed steps, t) of the last run, also when it stopped on an error."""
+        return int(lib().tlsph_dev_last_run_steps(self._h)), float(lib().tlsph_dev_last_run_time(self._h))
 
     def prepare(self, material):
         """runner.cpp:306-312: B0, constraints, initial momentum RHS and deformation rate."""

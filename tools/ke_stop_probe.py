@@ -21,8 +21,14 @@ for ratio in ratios:
         d = S.build_device(cfg, prepare=True)
         d.set_reduction(mode)
         t0 = time.perf_counter()
-        r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=2_000_000, seed=cfg["seed"],
-                  ke_stop=True, ke_ratio=ratio)
+        try:
+            r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=2_000_000, seed=cfg["seed"],
+                      ke_stop=True, ke_ratio=ratio)
+        except Exception as e:  # the reference stops with the same error kinds
+            steps, t = d.last_run()
+            print(f"n={d.n} ratio={ratio:g} {mode:7s}: stopped by '{e}' after {steps} steps, t = {t:.6g} s "
+                  f"({time.perf_counter() - t0:.1f} s)", flush=True)
+            continue
         res[mode] = r
         print(f"n={d.n} ratio={ratio:g} {mode:7s}: steps {r['steps']} damped {r['damped']} stopped {r['stopped_on_ke']} "
               f"peak KE {r['peak_ke']:.6e} final {r['final_ke']:.6e} ({time.perf_counter() - t0:.1f} s)", flush=True)
