@@ -106,6 +106,7 @@ struct DFields {
   // a clamped j (the streamed FAST sweep forms qf = pf * minv_uniform from them); null otherwise
   const uint16_t* nlocf;
   double minv_uniform;
+  double v0_uniform;  // every V0 equal: that value (the FAST dF/dt pass skips the V0_j gather); 0 otherwise
   // x-slab peers (slabs.py): per particle of a column shared with a neighbouring slab, the
   // particle's index in that slab's arrays (-1: not shared; >= 0: right peer; <= -2: left
   // peer at -2 - index); the peers' velocity arrays (device memory reachable from here)

@@ -636,6 +636,7 @@ DFields DevSystem::fields() const {
   f.nloc = nloc.p;
   f.nlocf = uniform_mass ? nlocf.p : nullptr;
   f.minv_uniform = minv_uniform;
+  f.v0_uniform = v0_uniform;
   f.cell_start = cell_start.p;
   f.cell = cutoff;
   f.has_body = has_body ? 1 : 0;
@@ -915,8 +916,25 @@ void DevSystem::current_cells(int64_t* cell_start_h, int32_t* order_ref) const {
   for (size_t k = 0; k < sorted.size(); ++k) order_ref[k] = pm[static_cast<size_t>(sorted[k])];
 }
 
+void DevSystem::refresh_v0_uniform() {
+  v0_uniform = 0.0;
+  if (n <= 0) return;
+  DBuf<int> differs_d;
+  differs_d.alloc(1);
+  CK(cudaMemsetAsync(differs_d.p, 0, sizeof(int), stream));
+  k_mass_differs<<<grid_for(n, 256), 256, 0, stream>>>(V0.p, n, differs_d.p);  // any array of doubles
+  CK_LAUNCH("k_mass_differs");
+  int differs = 1;
+  double v00 = 0.0;
+  CK(cudaMemcpyAsync(&differs, differs_d.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(&v00, V0.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  if (!differs && v00 > 0.0) v0_uniform = v00;
+}
+
 void DevSystem::compute_sweep_stats() {
   refresh_minvf();
+  refresh_v0_uniform();
   if (nslots > 0) {
     const size_t S = static_cast<size_t>(nslots);
     snbr.alloc(S);
@@ -1081,6 +1099,7 @@ void DevSystem::set_field(int field, const double* host) {
     refresh_minvf();
     fold_valid = false;  // diag = sum b - m_i
   }
+  if (field == TLSPH_FIELD_V0) refresh_v0_uniform();
   sync();
 }
 

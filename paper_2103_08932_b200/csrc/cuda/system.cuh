@@ -142,6 +142,8 @@ class DevSystem {
   DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)
   bool uniform_mass = false;  // every particle has the same mass
   double minv_uniform = 0.0;  // RN(1/m) then
+  double v0_uniform = 0.0;    // every V0 equal (> 0): that value; 0 otherwise (refresh_v0_uniform)
+  void refresh_v0_uniform();
 
   // scratch
   DBuf<DScalars> scal;

@@ -121,7 +121,8 @@ struct SlotView {
 #ifndef TLSPH_TL_PDL
 #define TLSPH_TL_PDL 1
 #endif
-template <int D, int G, int U, bool POST>
+// UV0: every reference volume equals f.v0_uniform, so the neighbour's V0 is not gathered
+template <int D, int G, int U, bool POST, bool UV0 = false>
 __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars* sc, double dt, int loop) {
   if (TLSPH_TL_PDL && G > 1) grid_dependency_wait();  // v of pass B's kick, F of pass A
   if (loop && sc->halt) return;
@@ -157,7 +158,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        v0[u] = f.V0[j[u]];
+        v0[u] = UV0 ? f.v0_uniform : f.V0[j[u]];
 #pragma unroll
         for (int d = 0; d < D; ++d) vj[u][d] = f.v[d][j[u]];
       }
@@ -211,9 +212,9 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
   }
 }
 
-template <int D, int G, bool POST>
+template <int D, int G, bool POST, bool UV0 = false>
 __global__ void TL_BOUNDS_C k_deformation_rate(DFields f, DScalars* sc, double dt, int loop) {
-  deformation_rate_body<D, G, TLSPH_TL_U, POST>(f, sc, dt, loop);
+  deformation_rate_body<D, G, TLSPH_TL_U, POST, UV0>(f, sc, dt, loop);
 }
 template <int D, bool POST>
 __global__ void k_deformation_rate_ordered(DFields f, DScalars* sc, double dt, int loop) {
@@ -543,12 +544,15 @@ void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop
     else if (pass == 1 && ord) k_momentum_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
     else if (pass == 1) launch_pdl(k_momentum<2, 4, true>, n * 4, st, f, s.scal.p, dt, loop);
     else if (ord) k_deformation_rate_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (f.v0_uniform > 0.0) launch_pdl(k_deformation_rate<2, 4, true, true>, n * 4, st, f, s.scal.p, dt, loop);
     else launch_pdl(k_deformation_rate<2, 4, true>, n * 4, st, f, s.scal.p, dt, loop);
   } else {
     if (pass == 0) k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
     else if (pass == 1 && ord) k_momentum_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
     else if (pass == 1) launch_pdl(k_momentum<3, kGB3, true>, n * kGB3, st, f, s.scal.p, dt, loop);
     else if (ord) k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (f.v0_uniform > 0.0)
+      launch_pdl(k_deformation_rate<3, kGC3, true, true>, n * kGC3, st, f, s.scal.p, dt, loop);
     else launch_pdl(k_deformation_rate<3, kGC3, true>, n * kGC3, st, f, s.scal.p, dt, loop);
   }
 }
