@@ -413,6 +413,25 @@ def sweep_sharded(args, ws, rank):
     dist.all_gather_object(tot, (s_free_local, int(own.sum())), group=gloo)
     s_free = sum(x[0] for x in tot)
     n_owned = sum(x[1] for x in tot)
+    # the full loop over the slabs (cfg5: TL-SPH step + random-choice damping, alpha 0.2): halo
+    # pushes and sweeps through the IPC links, dt from an all-reduce of the step scalars
+    loop = None
+    if args.scale_steps > 0:
+        mat = S.material()
+        g = np.zeros((d.n, 3))
+        g[:, 1] = -S.GRAVITY
+        d.set("body", g)
+        d.prepare(mat)
+        group = slabs.IpcGroup(slabs.DeviceSlabEngine(d, 3), [(p.x0, p.x1) for p in parts], rank, sweep)
+        spec = slabs.LoopSpec(mat, h, S.eta_for(h), 0.2, args.scale_steps, seed=0)
+        dist.barrier(group=gloo)
+        d.timer_start()
+        res = slabs.run_loop(group, spec, 3, sweeper=lambda scheme, et, dt_: sweep.sweep(scheme, et, dt_))
+        t_loop = barrier_and_max(d.timer_stop(), ws)
+        loop = {"metric": "particle-steps/s (fp64 TL-SPH step + splitting damping, random choice)",
+                "value": n_owned * res["steps"] / t_loop, "unit": "PS/s", "steps": res["steps"],
+                "damped_steps": res["damped"], "ms_per_step": t_loop / res["steps"] * 1e3,
+                "exchange": "halo pushes and sweeps through CUDA IPC; dt from an all-reduce per step"}
     sweep.close()
     del d
     peak, peak_src = load_peaks()
@@ -426,7 +445,8 @@ def sweep_sharded(args, ws, rank):
             "roofline": {"bound": "hbm", "achieved_per_gpu": b_sweep / ws / (t_max / sweeps) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": b_sweep / ws / (t_max / sweeps) / 1e9 / peak,
                          "peak_source": peak_src},
-            "timing": "CUDA events on each slab's stream between a barrier and the last phase, max over ranks"}
+            "timing": "CUDA events on each slab's stream between a barrier and the last phase, max over ranks",
+            "loop": loop}
 
 
 def cfg3_oracle_steps(threads, steps):
@@ -507,6 +527,7 @@ def main():
     ap.add_argument("--no-ps", action="store_true", help="skip the particle-steps/s leg")
     ap.add_argument("--scale-sweeps", type=int, default=10, help="sweeps of the large-body (cfg5-weak) leg")
     ap.add_argument("--no-scale", action="store_true", help="skip the large-body sweep leg")
+    ap.add_argument("--scale-steps", type=int, default=20, help="loop steps of the N > 1 sharded leg (0: sweep only)")
     ap.add_argument("--scale-layers", type=int, default=250,
                     help="x-layers of 250 x 250 per GPU of the N > 1 sharded leg (cfg5 weak scaling)")
     ap.add_argument("--parity-sweeps", type=int, default=500, help="cfg2 sweeps of the GPU-vs-oracle check (0: skip)")

@@ -176,6 +176,14 @@ int tlsph_dev_column_width(const tlsph_dev* dev, tlsph_dev_column_field field); 
 tlsph_status tlsph_dev_pack_column_field(tlsph_dev* dev, tlsph_dev_column_field field, int x, double* device_dst);
 tlsph_status tlsph_dev_unpack_column_field(tlsph_dev* dev, tlsph_dev_column_field field, int x,
                                            const double* device_src);
+/* Halo refresh of the full loop across processes (the exchange after verlet
+ * passes A and B, with the same host ordering rule as the phases): push stores
+ * this slab's owned boundary columns of `field` straight into the linked
+ * neighbours' halo copies and records the slab's halo event; wait makes the
+ * slab's stream wait on the neighbours' halo events of `field` (their pushes
+ * into this slab). Both asynchronous. */
+tlsph_status tlsph_dev_push_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field field);
+tlsph_status tlsph_dev_wait_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field field);
 
 void tlsph_dev_destroy(tlsph_dev* dev);
 

@@ -225,6 +225,14 @@ tlsph_status tlsph_dev_sweep_phase_ipc(tlsph_dev* dev, tlsph_dev_scheme scheme, 
   });
 }
 
+tlsph_status tlsph_dev_push_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field field) {
+  return guarded([&] { sys(dev).push_halo_ipc(field); });
+}
+
+tlsph_status tlsph_dev_wait_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field field) {
+  return guarded([&] { sys(dev).wait_halo_ipc(field); });
+}
+
 tlsph_status tlsph_dev_synchronize(tlsph_dev* dev) {
   return guarded([&] {
     DevSystem& s = sys(dev);

@@ -567,6 +567,8 @@ unsigned grid_for(long long n, int block) { return static_cast<unsigned>((n + bl
 
 // ====================================================================== DevSystem
 DevSystem::~DevSystem() {
+  for (cudaEvent_t e : halo_events)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : timer_ev)
     if (e) cudaEventDestroy(e);
   for (IpcPeer& ip : ipc_peer) ip.close();

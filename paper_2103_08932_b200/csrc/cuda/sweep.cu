@@ -1244,7 +1244,11 @@ void DevSystem::ensure_phase_events(bool interprocess) {
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (interprocess ? cudaEventInterprocess : 0)));
     phase_events.push_back(e);
   }
-  if (interprocess) phase_events_ipc = true;
+  if (interprocess) {
+    phase_events_ipc = true;
+    for (cudaEvent_t& e : halo_events)
+      if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventInterprocess));
+  }
 }
 
 void DevSystem::ipc_export(IpcExport* out) {
@@ -1254,8 +1258,11 @@ void DevSystem::ipc_export(IpcExport* out) {
   out->dim = D;
   out->device = device;
   out->nphase = static_cast<int>(phase_events.size());
+  out->n = n;
   for (int d = 0; d < D; ++d) CK(cudaIpcGetMemHandle(&out->vel[d], v[d].p));
+  CK(cudaIpcGetMemHandle(&out->pbv, pbv.p));
   for (int q = 0; q < out->nphase; ++q) CK(cudaIpcGetEventHandle(&out->ev[q], phase_events[q]));
+  for (int k = 0; k < 2; ++k) CK(cudaIpcGetEventHandle(&out->hev[k], halo_events[k]));
 }
 
 void DevSystem::link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start) {
@@ -1277,14 +1284,28 @@ void DevSystem::link_peer_ipc(int side, const IpcExport& peer, const long long* 
     CK(cudaIpcOpenEventHandle(&e, peer.ev[q]));
     ip.ev.push_back(e);
   }
+  {
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, peer.pbv, cudaIpcMemLazyEnablePeerAccess));
+    ip.mem.push_back(p);
+    ip.pbv = static_cast<double*>(p);
+    ip.n = peer.n;
+  }
+  for (int k = 0; k < 2; ++k) CK(cudaIpcOpenEventHandle(&ip.hev[k], peer.hev[k]));
   link_peer_arrays(side, peer_cell_start, pv);
 }
 
 void IpcPeer::close() {
   for (void* p : mem) cudaIpcCloseMemHandle(p);
   for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  for (cudaEvent_t& e : hev)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
   mem.clear();
   ev.clear();
+  pbv = nullptr;
 }
 
 // Phase q of the decomposed sweep of this slab, asynchronous: the stream first waits on the
@@ -1471,6 +1492,66 @@ void column_copy(DevSystem& s, int field, int x, double* buf, bool pack) {
 }  // namespace
 
 long long DevSystem::column_count(int x) const { return column_offsets(*this, x).back(); }
+// Halo push of a cross-process slab (tlsph_dev_push_halo_ipc): the particles of our owned boundary
+// column x, stored straight into the neighbour's copy of that column (its halo) through the IPC
+// mapping, at the indices link_peer_arrays recorded (peer_idx: >= 0 right peer, <= -2 left).
+__global__ void k_column_push(const long long* __restrict__ cell_start, int x, int dims0, int ncol_cells,
+                              ColumnField src, ColumnField dst, const int* __restrict__ peer_idx) {
+  const int q = blockIdx.x;
+  if (q >= ncol_cells) return;
+  const long long lin = static_cast<long long>(q) * dims0 + x;
+  for (long long p = cell_start[lin] + threadIdx.x; p < cell_start[lin + 1]; p += blockDim.x) {
+    const int pi = peer_idx[p];
+    if (pi == -1) continue;
+    const long long idx = pi >= 0 ? pi : -2 - pi;
+    for (int c = 0; c < src.ncomp; ++c) dst.ptr[c][idx * dst.stride] = src.ptr[c][p * src.stride];
+  }
+}
+
+// The neighbour's side of a column field, from its IPC mapping (same layout rules as column_field).
+ColumnField peer_column_field(const DevSystem& s, int side, int field) {
+  ColumnField cf{};
+  const IpcPeer& ip = s.ipc_peer[side];
+  if (field == TLSPH_DEV_COLUMN_VELOCITY) {
+    cf.ncomp = s.D;
+    cf.stride = 1;
+    for (int d = 0; d < s.D; ++d) cf.ptr[d] = s.peer_v[side][d];
+  } else {
+    cf.ncomp = s.D * s.D + 1;
+    const auto at = [&](long long p, int c) { return s.D == 2 ? pbv_at<2>(ip.n, p, c) : pbv_at<3>(ip.n, p, c); };
+    cf.stride = at(1, 0) - at(0, 0);
+    for (int c = 0; c < cf.ncomp; ++c) cf.ptr[c] = ip.pbv + at(0, c);
+  }
+  return cf;
+}
+
+void DevSystem::push_halo_ipc(int field) {
+  if (field != TLSPH_DEV_COLUMN_VELOCITY && field != TLSPH_DEV_COLUMN_STRESS)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown column field " + std::to_string(field));
+  ensure_phase_events(true);
+  CK(cudaSetDevice(device));
+  const int x0 = task_x0, x1 = task_x1 < 0 ? dims[0] : task_x1;
+  const int nq = static_cast<int>(ncells / dims[0]);
+  const ColumnField src = column_field(*this, field);
+  for (int side = 0; side < 2; ++side) {
+    if (ipc_peer[side].ev.empty()) continue;
+    const ColumnField dst = peer_column_field(*this, side, field);
+    if (dst.ncomp != src.ncomp) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "peer column layout differs");
+    k_column_push<<<static_cast<unsigned>(nq), 64, 0, stream>>>(cell_start.p, side == 0 ? x0 : x1 - 1, dims[0], nq,
+                                                               src, dst, peer_idx.p);
+  }
+  CK_LAUNCH("k_column_push");
+  CK(cudaEventRecord(halo_events[field], stream));
+}
+
+void DevSystem::wait_halo_ipc(int field) {
+  if (field != TLSPH_DEV_COLUMN_VELOCITY && field != TLSPH_DEV_COLUMN_STRESS)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown column field " + std::to_string(field));
+  CK(cudaSetDevice(device));
+  for (int side = 0; side < 2; ++side)
+    if (ipc_peer[side].hev[field]) CK(cudaStreamWaitEvent(stream, ipc_peer[side].hev[field], 0));
+}
+
 int DevSystem::column_width(int field) const { return column_field(*this, field).ncomp; }
 void DevSystem::pack_column(int field, int x, double* dev_dst) { column_copy(*this, field, x, dev_dst, true); }
 void DevSystem::unpack_column(int field, int x, const double* dev_src) {

@@ -45,16 +45,22 @@ struct SweepPlan;  // damping.cu
 // A slab's export for cross-process linking: its velocity arrays and colour-phase events as
 // CUDA IPC handles (tlsph_dev_ipc_export); plain bytes, exchanged by the host.
 struct IpcExport {
-  static constexpr unsigned kMagic = 0x74736c31u;  // "tsl1"
+  static constexpr unsigned kMagic = 0x74736c32u;  // "tsl2"
   unsigned magic;
   int dim, device, nphase;
+  long long n;                  // particles of the slab (the stress record's layout depends on it)
   cudaIpcMemHandle_t vel[3];
-  cudaIpcEventHandle_t ev[54];
+  cudaIpcMemHandle_t pbv;       // packed P B0 / V0 records (pass A output, pass B input)
+  cudaIpcEventHandle_t ev[54];  // colour phases
+  cudaIpcEventHandle_t hev[2];  // halo pushes: TLSPH_DEV_COLUMN_VELOCITY, _STRESS
 };
-// A neighbour opened from its export (mapped velocity arrays, its phase events)
+// A neighbour opened from its export (mapped arrays, its phase and halo events)
 struct IpcPeer {
   std::vector<void*> mem;
   std::vector<cudaEvent_t> ev;
+  cudaEvent_t hev[2] = {nullptr, nullptr};
+  double* pbv = nullptr;
+  long long n = 0;
   void close();
 };
 
@@ -211,6 +217,9 @@ class DevSystem {
   void link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start);
   void sweep_phase_ipc(int scheme, double eta_tilde, double dt, int q, int wait_q);
   IpcPeer ipc_peer[2];
+  cudaEvent_t halo_events[2] = {nullptr, nullptr};  // interprocess: this slab's halo pushes
+  void push_halo_ipc(int field);
+  void wait_halo_ipc(int field);
   cudaEvent_t timer_ev[2] = {nullptr, nullptr};  // tlsph_dev_timer_start / _stop
   bool phase_events_ipc = false;
   // x-slab halo columns (sweep.cu)

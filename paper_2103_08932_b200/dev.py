@@ -140,6 +140,8 @@ def lib():
     L.tlsph_dev_link_peer_ipc.argtypes = [P, I, C.c_char_p, C.POINTER(C.c_int64)]
     L.tlsph_dev_sweep_phase_ipc.argtypes = [P, I, C.c_double, C.c_double, I, I]
     L.tlsph_dev_synchronize.argtypes = [P]
+    L.tlsph_dev_push_halo_ipc.argtypes = [P, I]
+    L.tlsph_dev_wait_halo_ipc.argtypes = [P, I]
     L.tlsph_dev_timer_start.argtypes = [P]
     L.tlsph_dev_timer_stop.argtypes = [P]
     L.tlsph_dev_timer_stop.restype = C.c_double
@@ -417,6 +419,14 @@ class DeviceSystem:
 
     def synchronize(self):
         _check(lib().tlsph_dev_synchronize(self._h))
+
+    def push_halo_ipc(self, field):
+        """Store this slab's owned boundary columns of `field` into the linked neighbours (async)."""
+        _check(lib().tlsph_dev_push_halo_ipc(self._h, COLUMN_FIELDS[field]))
+
+    def wait_halo_ipc(self, field):
+        """This slab's stream waits on the neighbours' halo pushes of `field` (async)."""
+        _check(lib().tlsph_dev_wait_halo_ipc(self._h, COLUMN_FIELDS[field]))
 
     def timer_start(self):
         """Start a device-time span on this system's stream (timer_stop returns its seconds)."""

@@ -384,10 +384,13 @@ class IpcSlabSweep:
         path = os.path.join("/dev/shm", f"tlsph_slab_{token[0]}")
         if rank == 0:
             self.counters = PhaseCounters(path, world, create=True)
+            self.halo_counters = PhaseCounters(path + "_halo", world, create=True)
         dist.barrier(group=group)
         if rank != 0:
             self.counters = PhaseCounters(path, world, create=False)
+            self.halo_counters = PhaseCounters(path + "_halo", world, create=False)
         dist.barrier(group=group)
+        self.pushed = 0
         self.neighbours = [r for r in (rank - 1, rank + 1) if 0 <= r < world]
         if rank > 0:
             system.link_peer_ipc(0, *items[rank - 1])
@@ -412,11 +415,49 @@ class IpcSlabSweep:
                 self.counters.set(self.rank, self.enqueued)
         self.d.synchronize()
 
+    def halo(self, field):
+        """The full loop's halo refresh across processes: push this slab's owned boundary columns of
+        `field` into the neighbours, then (once they have pushed theirs) wait for their pushes on
+        this slab's stream. No host synchronisation."""
+        self.d.push_halo_ipc(field)
+        self.pushed += 1
+        self.halo_counters.set(self.rank, self.pushed)
+        self.halo_counters.wait(self.neighbours, self.pushed)
+        self.d.wait_halo_ipc(field)
+
     def close(self):
         import torch.distributed as dist
 
         dist.barrier(group=self._group)
         self.counters.close(unlink=self.rank == 0)
+        self.halo_counters.close(unlink=self.rank == 0)
+
+
+class IpcGroup(DistGroup):
+    """run_loop's group for one process per GPU with the fused exchange: halo refreshes through
+    IpcSlabSweep.halo (peer stores + IPC events), step scalars through torch.distributed
+    all-reduces; pair it with sweeper=ipc_sweep.sweep."""
+
+    def __init__(self, engine, ranges, rank, ipc_sweep):
+        super().__init__(engine, ranges, rank)
+        self.ipc = ipc_sweep
+
+    def exchange(self, transfers, field="velocity"):
+        self.ipc.halo(field)
+
+    def reduce(self, want_ke, check_step):
+        import torch
+        import torch.distributed as dist
+
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        vm, am, ke = self.e.reduce(want_ke, check_step)
+        mx = torch.tensor([vm, am], dtype=torch.float64, device=dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        if want_ke:
+            t = torch.tensor([ke], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            ke = float(t[0])
+        return float(mx[0]), float(mx[1]), ke
 
 
 class SlabSweep:
