@@ -64,7 +64,24 @@ namespace tlsph_cuda {
 
 namespace {
 
-constexpr int kThreads = 128;  // one CTA per cell
+// k_sweep_phase: one CTA of D warps per cell (warp d: component d)
+
+// Launch chained to the preceding kernel by programmatic dependent launch.
+template <typename... KArgs, typename... Args>
+void launch_pdl_phase(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                      Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
 
 struct Phase {
   const int* cells;  // this colour's task cells (linear index), fuller first; blockIdx -> cell
@@ -460,9 +477,10 @@ __device__ __forceinline__ void writeback_peers(const DFields& f, const Tile<D>&
 // ------------------------------------------------------------------ colour phase
 // K > 0: rows up to 32 K slots run the branch-free register path; K = 0: generic loop only.
 template <int D, int SCHEME, bool ORDERED, int K>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(32 * D)
 k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   if (ph.dt_from_scalars && sc->halt) return;
+  grid_launch_dependents();  // PDL: the next phase stages its static data while this one runs
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid / kWarp, lane = tid % kWarp;
@@ -483,7 +501,7 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   if (cs.p0 == cs.p1) return;  // empty cell (uniform across the CTA)
   const long long p0 = cs.p0, p1 = cs.p1, s0 = cs.s0;
   const int np = static_cast<int>(p1 - p0);
-  if (warp == 0) issue_staging<D, SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT, true>(f, t, cs, sstart, send, lane);
+  if (warp == 0) issue_staging<D, SCHEME == TLSPH_SCHEME_PARTICLE_SPLIT, true, true>(f, t, cs, sstart, send, lane);
   if (warp == 0) cp_async_wait_all();
   __syncthreads();  // barrier initialised and row copies landed before anyone waits on it
   mbar_wait(t.bar, 0);
@@ -627,12 +645,12 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   for (int q = 0; q < kSegs; ++q) {
     const long long g0 = t.seg_start[q];
     const int b = t.seg_base[q], len = t.seg_len[q];
-    for (int e = tid; e < len; e += kThreads) {
+    for (int e = tid; e < len; e += 32 * D) {
 #pragma unroll
       for (int d = 0; d < D; ++d) f.v[d][g0 + e] = t.sv[d][b + e];
     }
   }
-  writeback_peers<D>(f, t, c, tid, kThreads);
+  writeback_peers<D>(f, t, c, tid, 32 * D);
 }
 
 // ------------------------------------------------------------------ FAST particle split, one warp per cell
@@ -1024,7 +1042,7 @@ void launch_phase(const DevSystem& s, const DFields& f, const Phase& ph) {
                             static_cast<int>(smem)));
     configured = smem;
   }
-  k_sweep_phase<D, SCHEME, ORDERED, K><<<static_cast<unsigned>(ph.ncol), kThreads, smem, s.stream>>>(f, ph,
+  launch_pdl_phase(k_sweep_phase<D, SCHEME, ORDERED, K>, static_cast<unsigned>(ph.ncol), 32 * D, smem, s.stream, f, ph,
                                                                                                     s.scal.p);
 }
 
