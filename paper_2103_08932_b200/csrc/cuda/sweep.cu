@@ -1033,6 +1033,175 @@ void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
   else launch_fast_impl<D, K, true, false>(s, f, ph);
 }
 
+// ------------------------------------------------------------------ ORDERED particle split, one warp per cell
+// The bit-exact chain (damping.cpp:53-89 in the reference's operation order) with all D components
+// in one warp: lanes form every slot's terms b (v_i - v_j) of every component, lane d folds
+// component d's terms in slot order (the D folds run side by side), and the rate (corrected
+// division), v_i and the scatter follow for all components at once. One pass over the slot
+// metadata per particle instead of one per component warp (k_sweep_phase).
+template <int D, int K>
+__global__ void __launch_bounds__(kWarp)
+k_sweep_ordered(DFields f, Phase ph, const DScalars* __restrict__ sc) {
+  if (ph.dt_from_scalars && sc->halt) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  grid_launch_dependents();
+  int c[3];
+  const long long lin = phase_cell<D>(ph, f, blockIdx.x, c);
+  Tile<D> t = carve<D>(smem, ph);
+  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
+  const double dt_op = 0.5 * dt;  // particle split: dt/2 (damping.cpp:133)
+  const double eta = ph.eta;
+  const CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
+  long long sstart, send;
+  locate_row<D>(f, c, lane, sstart, send);
+  if (cs.p0 == cs.p1) return;
+  issue_staging<D, true, true, true>(f, t, cs, sstart, send, lane);
+  wait_staging(t);
+  __syncwarp();
+  const int lbase = reinterpret_cast<const int*>(t.bar + 1)[0];
+  const long long s0 = cs.s0;
+  const long long* offc = t.soff + (cs.p0 - cs.o0());
+  const double* pfc = t.spf + (s0 - cs.f0());
+  const uint16_t* nlc = t.snl + (s0 - cs.n0());
+  const double* fdg = t.sdiag + (cs.p0 - cs.q0());
+  const double* fdn = t.sden + (cs.p0 - cs.q0());
+  const double* fyy = t.sy + (cs.p0 - cs.q0());
+  const int np = static_cast<int>(cs.p1 - cs.p0);
+  double* const term = t.skf;  // D x MR: component d's terms at term[d * MR + slot]
+
+  int pk_n = ph.forward ? 0 : np - 1;
+  int lo_n = static_cast<int>(offc[pk_n] - s0), cnt_n = static_cast<int>(offc[pk_n + 1] - s0) - lo_n;
+  int jq_n[K];
+  bool up_n[K];
+  double b_n[K], bm_n[K];
+  auto meta = [&](int lo_, int cnt_, int li_) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const int sl = lane + u * kWarp;
+      const bool v = sl < cnt_;
+      const int j = v ? nlc[lo_ + sl] : li_;  // invalid lanes point at i itself with b = 0
+      const double mf = t.smf[j];
+      jq_n[u] = j;
+      up_n[u] = v && mf > 0.0;  // clamped j: writes discarded (damping.cpp:84-86)
+      b_n[u] = v ? eta * pfc[lo_ + sl] * dt_op : 0.0;
+      bm_n[u] = up_n[u] ? div_by(b_n[u], t.sm[j], mf) : 0.0;
+    }
+  };
+  meta(lo_n, cnt_n, lbase + pk_n);
+  for (int kk = 0; kk < np; ++kk) {
+    const int pk = pk_n, cnt = cnt_n;
+    int jq[K];
+    bool up[K];
+    double bq[K], bmq[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      jq[u] = jq_n[u];
+      up[u] = up_n[u];
+      bq[u] = b_n[u];
+      bmq[u] = bm_n[u];
+    }
+    if (kk + 1 < np) {  // next particle's metadata, off the chain
+      pk_n = ph.forward ? kk + 1 : np - 2 - kk;
+      lo_n = static_cast<int>(offc[pk_n] - s0);
+      cnt_n = static_cast<int>(offc[pk_n + 1] - s0) - lo_n;
+      meta(lo_n, cnt_n, lbase + pk_n);
+    }
+    const int li = lbase + pk;
+    if (t.smf[li] < 0.0 || cnt == 0) continue;  // constrained i (damping.cpp:151) / no neighbours (:54)
+    const double diag = fdg[pk], den = fdn[pk], y = fyy[pk];
+    double vi[D], vq[K][D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) vi[d] = t.sv[d][li];
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int d = 0; d < D; ++d) vq[u][d] = t.sv[d][jq[u]];
+    // terms b (v_i - v_j) exactly as the reference forms them (damping.cpp:65-71)
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+      if (lane + u * kWarp < cnt)
+#pragma unroll
+        for (int d = 0; d < D; ++d) term[d * ph.MR + lane + u * kWarp] = bq[u] * (vi[d] - vq[u][d]);
+    __syncwarp();
+    double Rl = 0.0;
+    if (lane < D) {  // lane d folds component d in slot order; loads run 8 terms ahead of the adds
+      const double* tc = term + lane * ph.MR;
+      const double2* t2 = reinterpret_cast<const double2*>(tc);
+      const int npair = cnt >> 1;
+      double2 a = npair > 0 ? t2[0] : make_double2(0.0, 0.0), b = npair > 1 ? t2[1] : a;
+      double2 c2 = npair > 2 ? t2[2] : a, e = npair > 3 ? t2[3] : a;
+      int q = 0;
+      for (; q + 4 <= npair; q += 4) {
+        const double2 a1 = q + 4 < npair ? t2[q + 4] : a, b1 = q + 5 < npair ? t2[q + 5] : a;
+        const double2 c1 = q + 6 < npair ? t2[q + 6] : a, e1 = q + 7 < npair ? t2[q + 7] : a;
+        Rl = Rl - a.x;
+        Rl = Rl - a.y;
+        Rl = Rl - b.x;
+        Rl = Rl - b.y;
+        Rl = Rl - c2.x;
+        Rl = Rl - c2.y;
+        Rl = Rl - e.x;
+        Rl = Rl - e.y;
+        a = a1;
+        b = b1;
+        c2 = c1;
+        e = e1;
+      }
+      const double2 rest[3] = {a, b, c2};
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        if (q + r < npair) {
+          Rl = Rl - rest[r].x;
+          Rl = Rl - rest[r].y;
+        }
+      if (cnt & 1) Rl = Rl - tc[cnt - 1];
+    }
+    double rate[D], vnew[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double R = __shfl_sync(kFull, Rl, d);
+      rate[d] = div_by(R, den, y);
+      vnew[d] = vi[d] + diag * rate[d];
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const double pred = vq[u][d] - bq[u] * rate[d];
+        const double nv = vq[u][d] - bmq[u] * (vnew[d] - pred);
+        if (up[u]) t.sv[d][jq[u]] = nv;
+      }
+    // i is not its own neighbour, so this store cannot race the scatter above
+    if (lane == 0)
+#pragma unroll
+      for (int d = 0; d < D; ++d) t.sv[d][li] = vnew[d];
+    __syncwarp();
+  }
+  writeback_peers<D>(f, t, c, lane, kWarp);
+  writeback_rows<D>(f, t, lane);
+}
+
+inline bool ordered_warps() {  // TLSPH_SWEEP_ORDERED_WARPS=1: one warp per component (k_sweep_phase), A/B
+  static const bool on = [] {
+    const char* e = std::getenv("TLSPH_SWEEP_ORDERED_WARPS");
+    return e && *e == '1';
+  }();
+  return on;
+}
+
+template <int D, int K>
+void launch_ordered(const DevSystem& s, const DFields& f, Phase ph) {
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    CK(cudaFuncSetAttribute(k_sweep_ordered<D, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    configured = smem;
+  }
+  launch_pdl_phase(k_sweep_ordered<D, K>, static_cast<unsigned>(ph.ncol), kWarp, smem, s.stream, f, ph, s.scal.p);
+}
+
 template <int D, int SCHEME, bool ORDERED, int K>
 void launch_phase(const DevSystem& s, const DFields& f, const Phase& ph) {
   const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
@@ -1055,6 +1224,13 @@ void launch_particle_split(const DevSystem& s, const DFields& f, const Phase& ph
     else if (K == 2) launch_fast<D, 2>(s, f, ph);
     else if (K == 3) launch_fast<D, 3>(s, f, ph);
     else launch_fast<D, 4>(s, f, ph);
+    return;
+  }
+  if (ORDERED && K <= 4 && !ordered_warps()) {
+    if (K <= 1) launch_ordered<D, 1>(s, f, ph);
+    else if (K == 2) launch_ordered<D, 2>(s, f, ph);
+    else if (K == 3) launch_ordered<D, 3>(s, f, ph);
+    else launch_ordered<D, 4>(s, f, ph);
     return;
   }
   if (K <= 1) launch_phase<D, TLSPH_SCHEME_PARTICLE_SPLIT, ORDERED, 1>(s, f, ph);
