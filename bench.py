@@ -384,17 +384,19 @@ def sweep_sharded(args, ws, rank):
     from paper_2103_08932_b200 import scenarios as S
     from paper_2103_08932_b200 import slabs
 
+    from paper_2103_08932_b200 import dev
+
     layers, dp = args.scale_layers, 0.004
-    r0, _ = S.box_lattice([0.0, 0.0, 0.0], [layers * ws * dp, 1.0, 1.0], dp)
     h = 1.3 * dp
-    cons = (r0[:, 0] < 5 * dp).astype(np.uint8)
-    grid, parts = slabs.decompose(r0, h, ws)
-    part = parts[rank]
-    d = slabs.make_device_slab(grid, part, r0, dp ** 3, S.RHO0, h, cons)
-    cols = slabs.cell_columns(r0[part.ids], grid[0], grid[2], grid[1][0])
+    # this rank's held particles only (slabs.lattice_slab == decompose on the whole lattice)
+    grid, ranges, part, r0 = slabs.lattice_slab([0.0, 0.0, 0.0], [layers * ws * dp, 1.0, 1.0], dp, h, ws, rank)
+    parts = [slabs.Slab(r, x0, x1, None) for r, (x0, x1) in enumerate(ranges)]
+    cons_local = (r0[:, 0] < 5 * dp).astype(np.uint8)
+    d = dev.DeviceSystem(r0, dp ** 3, S.RHO0, h, cons_local, grid=grid[:2])
+    d.set_task_range(part.x0, part.x1)
+    cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
     own = (cols >= part.x0) & (cols < part.x1)
-    cons_local = cons[part.ids]
-    del r0, cons
+    del r0
     d.set_reduction("fast")
     off = d.row_offsets()
     rows = off[1:] - off[:-1]

@@ -153,6 +153,40 @@ def decompose(r0, h, world):
     return (origin, dims, cell), slabs
 
 
+def lattice_slab(lo, hi, dp, h, world, rank):
+    """decompose() for a box lattice (generate_box_lattice, cases.cpp:21-46) without building the
+    whole body: the global grid and column counts follow from the lattice axes, and only this
+    rank's held particles are generated (reference order, x fastest). Returns (grid, ranges, slab,
+    r0 of the held particles); identical to decompose() on the full lattice."""
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    if not (dp > 0.0) or np.any(hi - lo < dp * (1.0 - 1e-12)):
+        raise ValueError("degenerate lattice")
+    counts = []
+    for d in range(len(lo)):
+        q = (hi[d] - lo[d]) / dp
+        counts.append(max(1, int(math.floor(q + 0.5))))
+    axes = [lo[d] + (np.arange(counts[d], dtype=np.float64) + 0.5) * dp for d in range(len(lo))]
+    cutoff = 2.0 * float(h)
+    origin = np.array([a.min() for a in axes])
+    dims = [max(1, int(math.floor((axes[d].max() - axes[d].min()) / cutoff)) + 1) for d in range(len(lo))]
+    col_layer = np.clip(np.floor((axes[0] - origin[0]) / cutoff).astype(np.int64), 0, dims[0] - 1)
+    per_layer = int(np.prod(counts[1:]))
+    ranges = plan(np.bincount(col_layer, minlength=dims[0]) * per_layer, world)
+    x0, x1 = ranges[rank]
+    lo_col, hi_col = held_columns(x0, x1, dims[0])
+    layers = np.nonzero((col_layer >= lo_col) & (col_layer < hi_col))[0]
+    rest = np.meshgrid(*[axes[d] for d in range(len(lo) - 1, 0, -1)], indexing="ij")  # slowest first
+    rest = [g.reshape(-1) for g in rest][::-1]  # axis 1 .. D-1, axis 1 fastest
+    m = len(rest[0])
+    r0 = np.empty((m * len(layers), len(lo)))
+    r0[:, 0] = np.tile(axes[0][layers], m)
+    for d in range(1, len(lo)):
+        r0[:, d] = np.repeat(rest[d - 1], len(layers))
+    ids = (np.arange(m)[:, None] * counts[0] + layers[None, :]).reshape(-1)
+    return (origin, dims, cutoff), ranges, Slab(rank, x0, x1, ids), r0
+
+
 def make_device_slab(grid, slab, r0, V0, rho0, h, constrained=None):
     """DeviceSystem of one slab: the held particles binned in the global grid, tasks = owned columns."""
     from . import dev

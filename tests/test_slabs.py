@@ -670,3 +670,19 @@ def test_ipc_slab_loop_equals_undivided_device_loop(tmp_path, dim, world, mode):
         own = (cols[ids] >= int(z["x0"])) & (cols[ids] < int(z["x1"]))
         for name in ("v", "r", "F", "dFdt", "rho", "a"):
             assert np.array_equal(z[name][own], whole.get(name)[ids[own]]), (r, name)
+
+
+@pytest.mark.parametrize("lo,hi,world", [([0, 0, 0], [0.4, 0.1, 0.08], 3), ([0, -0.2, -0.2], [0.8, 0.2, 0.2], 4),
+                                         ([0, 0], [1.0, 0.1], 2)])
+def test_lattice_slab_equals_decompose(lo, hi, world):
+    """The per-rank lattice generator (no whole body on the host) reproduces decompose() exactly."""
+    from paper_2103_08932_b200 import scenarios as S
+
+    r0, _ = S.box_lattice(lo, hi, DP)
+    grid, parts = slabs.decompose(r0, H, world)
+    for r in range(world):
+        g2, ranges, sl, lr0 = slabs.lattice_slab(lo, hi, DP, H, world, r)
+        assert np.array_equal(g2[0], grid[0]) and g2[1] == grid[1] and g2[2] == grid[2]
+        assert (sl.x0, sl.x1) == (parts[r].x0, parts[r].x1)
+        assert np.array_equal(sl.ids, parts[r].ids) and np.array_equal(lr0, r0[parts[r].ids])
+
