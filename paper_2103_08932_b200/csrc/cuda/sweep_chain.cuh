@@ -237,7 +237,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
 
 // The same chain with the slot block streamed from global memory (L2) instead
 // of shared memory (k_sweep_fast<STREAM>): neighbour indices and pair factors
-// are loaded two particles ahead, and the per-slot mass factor is formed as
+// are loaded three particles ahead, and the per-slot mass factor is formed as
 // pair_factor * RN(1/m_j) from the staged stencil -- exactly the stored qf
 // (state.cu k_qf), so the arithmetic is that of fast_chain. UNI (uniform
 // masses): no stencil 1/m either; the factor is pair_factor * RN(1/m) unless
@@ -246,6 +246,7 @@ template <int D, int K, bool UNI>
 __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lane) {
   const int np = t.np;
   auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
+  auto pclamp = [&](int kk) { return pidx(kk < np ? kk : np - 1); };
   auto row = [&](int p, int& lo, int& cnt) {
     lo = static_cast<int>(t.offs[p] - t.s0);
     cnt = static_cast<int>(t.offs[p + 1] - t.s0) - lo;
@@ -292,15 +293,16 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     if (skip) upm = 0;
   };
 
-  // particle 0: coefficients; particle 1: raw loads in flight; particle 2: row extents
+  // particle 0: coefficients; particles 1, 2: raw loads in flight; particle 3: row extents
   int pk = pidx(0);
-  const int pk1i = np > 1 ? pidx(1) : pk;
-  int pk1 = pk1i, pk2 = np > 2 ? pidx(2) : pk1i;
-  int jn[K], lo1, cnt1, lo2, cnt2;
-  double pfn[K];
+  int pk1 = pclamp(1), pk2 = pclamp(2), pk3 = pclamp(3);
+  int jn[K], jn2[K], lo1, cnt1, lo2, cnt2, lo3, cnt3;
+  double pfn[K], pfn2[K];
   row(pk1, lo1, cnt1);
   row(pk2, lo2, cnt2);
+  row(pk3, lo3, cnt3);
   load_raw(lo1, cnt1, t.lbase + pk1, jn, pfn);
+  load_raw(lo2, cnt2, t.lbase + pk2, jn2, pfn2);
   {
     int lo, cnt, j0[K];
     double pf0[K], q0[K];
@@ -314,13 +316,13 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
 
   for (int kk = 0; kk < np; ++kk) {
     const int li = t.lbase + pk;
-    // particle kk+2: raw loads (two iterations of latency cover)
-    int jn2[K];
-    double pfn2[K];
-    load_raw(lo2, cnt2, t.lbase + pk2, jn2, pfn2);
-    const int pk3 = kk + 3 < np ? pidx(kk + 3) : pk2;
-    int lo3, cnt3;
-    row(pk3, lo3, cnt3);
+    // particle kk+3: raw loads (three iterations of latency cover)
+    int jn3[K];
+    double pfn3[K];
+    load_raw(lo3, cnt3, t.lbase + pk3, jn3, pfn3);
+    const int pk4 = pclamp(kk + 4);
+    int lo4, cnt4;
+    row(pk4, lo4, cnt4);
 
     // the chain: gathers
     double vi[D], vq[K][D];
@@ -364,13 +366,17 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     for (int u = 0; u < K; ++u) {
       jn[u] = jn2[u];
       pfn[u] = pfn2[u];
+      jn2[u] = jn3[u];
+      pfn2[u] = pfn3[u];
     }
     pk = pk1;
     pk1 = pk2;
     pk2 = pk3;
+    pk3 = pk4;
     cnt1 = cnt2;
-    lo2 = lo3;
     cnt2 = cnt3;
+    lo3 = lo4;
+    cnt3 = cnt4;
   }
 }
 
