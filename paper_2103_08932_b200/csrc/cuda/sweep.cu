@@ -335,7 +335,10 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   } else if (SLOTS && QF && !UNI && lane == 4) {
     tma_load_1d(t.sqf, f.qf + cs.f0(), mybytes, t.bar);
   }
-  if (!SLOTS) {  // streamed slot block: bring it into L2 ahead of the chain's register loads
+#ifndef TLSPH_STREAM_L2PF
+#define TLSPH_STREAM_L2PF 1
+#endif
+  if (!SLOTS && TLSPH_STREAM_L2PF) {  // streamed slot block: bring it into L2 ahead of the chain's register loads
     if (lane == 1) tma_prefetch_l2(f.pf + cs.f0(), static_cast<uint32_t>((cs.f1() - cs.f0()) * 8));
     else if (lane == 2)
       tma_prefetch_l2((nl_src ? nl_src : f.nloc) + cs.n0(), static_cast<uint32_t>((cs.n1() - cs.n0()) * 2));
