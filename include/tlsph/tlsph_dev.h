@@ -210,10 +210,11 @@ double tlsph_dev_last_run_time(const tlsph_dev* dev);
 tlsph_status tlsph_dev_current_cells(const tlsph_dev* dev, int64_t* cell_start, int32_t* order);
 
 /* Where the FAST particle-split sweep keeps a cell's slot block (pair factors,
- * stencil indices) while its chain runs: staged in shared memory (four cells
- * per SM; the latency-bound form for colours of up to ~600 cells) or streamed
- * from L2 (a tile of stencil velocities only, 12-16 cells per SM; the
- * throughput form for large bodies). AUTO picks by the colour's cell count.
+ * stencil indices) while its chain runs: staged in shared memory (four to six
+ * cells per SM; the form for colours of up to two waves of staged tiles, e.g.
+ * 600-1,500 cells) or streamed from L2 (a tile of stencil velocities only,
+ * 15 cells per SM; the throughput form for large bodies). AUTO picks by the
+ * colour's cell count.
  * Results are identical in every mode. */
 typedef enum tlsph_dev_sweep_tiling {
   TLSPH_SWEEP_TILING_AUTO = 0,

@@ -951,7 +951,7 @@ void launch_pairwise_any(const DevSystem& s, const DFields& f, const Phase& ph) 
 }
 
 // Staged or streamed slot block (tlsph_dev_set_sweep_tiling); AUTO: streamed
-// when the colour's cells exceed one wave of staged tiles
+// when the colour's cells exceed two waves of staged tiles
 // (TLSPH_SWEEP_STREAM=0/1 overrides AUTO, for A/B runs).
 inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_bytes) {
   if (s.sweep_tiling != TLSPH_SWEEP_TILING_AUTO) return s.sweep_tiling == TLSPH_SWEEP_TILING_STREAMED;
@@ -963,8 +963,10 @@ inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_byte
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // measured crossover: staged still wins at ~1.6 waves (cfg3: 1.133 vs 1.188 ms per sweep) and
+  // loses from ~11 waves on (cfg4 12.5 vs 10.4, cfg5-weak 24.2 vs 18.0)
   const long long per_sm = std::max<long long>(1, static_cast<long long>((228 * 1024) / (staged_bytes + 1024)));
-  return ph.ncol > per_sm * sms;
+  return ph.ncol > 2 * per_sm * sms;
 }
 
 inline bool uniform_disabled() {  // TLSPH_SWEEP_UNIFORM=0: the stencil-1/m form even for uniform masses (A/B)
