@@ -75,8 +75,22 @@ __global__ void k_step_begin(DFields f, DScalars* sc, double* __restrict__ parti
     last = atomicAdd(&sc->block_counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
+  // the last block sums the per-block KE partials in parallel (fixed order: strided per thread,
+  // then the shared-memory tree), so the serial tail does not walk them one by one
+  if (want_ke) {
+    const volatile double* pv = partials;
+    double e = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) e += pv[b];
+    s_k[threadIdx.x] = e;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+      if (threadIdx.x < off) s_k[threadIdx.x] += s_k[threadIdx.x + off];
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x != 0) return;
   // ---- serial tail (one thread)
   sc->block_counter = 0;
   const double vm = from_ordered_bits(atomicExch(&sc->vmax_bits, 0ull));
@@ -109,9 +123,7 @@ __global__ void k_step_begin(DFields f, DScalars* sc, double* __restrict__ parti
     return;
   }
   if (want_ke) {
-    double e = 0.0;
-    const volatile double* pv = partials;
-    for (unsigned b = 0; b < gridDim.x; ++b) e += pv[b];
+    const double e = s_k[0];
     sc->ke = e;
     if (e > sc->ke_peak) sc->ke_peak = e;
     if (sc->steps > 0 && e < sc->ke_peak && e < sc->ke_ratio * sc->ke_peak) {
