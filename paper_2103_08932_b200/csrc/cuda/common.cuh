@@ -138,6 +138,13 @@ struct DFields {
   // the same slots with each row re-ordered by ascending (cell-sorted) neighbour index: the FAST
   // neighbour passes B and C gather from neighbours grouped by cell (fewer cache lines per warp
   // load than the reference's ascending-reference-id order, which the ORDERED kernels keep)
+  // ORDERED neighbour passes: the slot arrays interleaved by groups of 32 consecutive particles
+  // (slot k of particle i at ogbase[i / 32] + 32 k + i % 32), so the one-thread-per-particle
+  // slot-order loops load coalesced; null until the reduction mode is ORDERED (build_ordered_rows)
+  const int* onbr;
+  const double* odw;
+  const double* oe0[3];
+  const long long* ogbase;
   const int* snbr;
   const double* sdw;
   const double* se0[3];

@@ -144,6 +144,10 @@ class DevSystem {
   void enqueue_resort();
   void current_cells(int64_t* cell_start_h, int32_t* order_ref) const;
   DBuf<double> sdw, se0[3];
+  DBuf<int> onbr;              // ORDERED passes: group-interleaved slot copy (build_ordered_rows)
+  DBuf<double> odw, oe0[3];
+  DBuf<long long> ogbase;
+  void build_ordered_rows();
   DBuf<uint16_t> nloc;
   DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)
   bool uniform_mass = false;  // every particle has the same mass

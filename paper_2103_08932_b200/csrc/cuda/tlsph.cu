@@ -15,6 +15,7 @@
 //   C  neighbour sum: dF/dt, density(J^{n+1/2}), half-kick F and r, constraints
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "system.cuh"
 #include "tma.cuh"
@@ -102,17 +103,27 @@ constexpr int kGB3 = TLSPH_TL_GB3, kGC3 = TLSPH_TL_GC3;  // lanes per particle i
 #ifndef TLSPH_TL_SORTED
 #define TLSPH_TL_SORTED 1
 #endif
-template <int D, int G>
+template <int D, int G, bool OI = false>
 struct SlotView {
   const int* nbr;
   const double* dw;
   const double* e0[D];
   __device__ explicit SlotView(const DFields& f) {
     const bool s = TLSPH_TL_SORTED && G > 1 && f.snbr;
-    nbr = s ? f.snbr : f.nbr;
-    dw = s ? f.sdw : f.dwdr0;
+    const bool o = OI;
+    nbr = s ? f.snbr : o ? f.onbr : f.nbr;
+    dw = s ? f.sdw : o ? f.odw : f.dwdr0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) e0[d] = s ? f.se0[d] : f.e0[d];
+    for (int d = 0; d < D; ++d) e0[d] = s ? f.se0[d] : o ? f.oe0[d] : f.e0[d];
+  }
+  // physical index of slot s of particle i (row start lo): the ORDERED (G == 1) passes read the
+  // group-interleaved copy, slot k of particle i at ogbase[i / 32] + 32 k + i % 32
+  __device__ __forceinline__ long long base(const DFields& f, long long i) const {
+    return OI ? f.ogbase[i >> 5] + (i & 31) : 0;
+  }
+  __device__ __forceinline__ long long at(const DFields& f, long long ob, long long lo, long long s) const {
+    if (OI) return ob + 32 * (s - lo);
+    return s;
   }
 };
 
@@ -122,7 +133,7 @@ struct SlotView {
 #define TLSPH_TL_PDL 1
 #endif
 // UV0: every reference volume equals f.v0_uniform, so the neighbour's V0 is not gathered
-template <int D, int G, int U, bool POST, bool UV0 = false>
+template <int D, int G, int U, bool POST, bool UV0 = false, bool OI = false>
 __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars* sc, double dt, int loop) {
   if (TLSPH_TL_PDL && G > 1) grid_dependency_wait();  // v of pass B's kick, F of pass A
   if (loop && sc->halt) return;
@@ -131,7 +142,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
   const long long i = tid / G;
   const int l = static_cast<int>(tid % G);
   const bool active = i < f.n && is_owned(f, i);
-  const SlotView<D, G> sv(f);
+  const SlotView<D, G, OI> sv(f);
   double rate[D][D];
 #pragma unroll
   for (int r = 0; r < D; ++r)
@@ -141,7 +152,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
     double vi[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) vi[d] = f.v[d][i];
-    const long long hi = f.offs[i + 1];
+    const long long hi = f.offs[i + 1], lo_i = f.offs[i], ob_i = sv.base(f, i);
     // U slots per lane per iteration: their loads and gathers are issued together (more bytes in
     // flight per thread); the lane still accumulates its slots in ascending order
     for (long long s = f.offs[i] + l; s < hi; s += U * G) {
@@ -150,7 +161,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool ok = s + u * G < hi;
-        const long long su = ok ? s + u * G : s;
+        const long long su = sv.at(f, ob_i, lo_i, ok ? s + u * G : s);
         j[u] = sv.nbr[su];
         dw[u] = sv.dw[su];
 #pragma unroll
@@ -216,9 +227,9 @@ template <int D, int G, bool POST, bool UV0 = false>
 __global__ void TL_BOUNDS_C k_deformation_rate(DFields f, DScalars* sc, double dt, int loop) {
   deformation_rate_body<D, G, TLSPH_TL_U, POST, UV0>(f, sc, dt, loop);
 }
-template <int D, bool POST>
+template <int D, bool POST, bool OI = false>
 __global__ void k_deformation_rate_ordered(DFields f, DScalars* sc, double dt, int loop) {
-  deformation_rate_body<D, 1, 1, POST>(f, sc, dt, loop);
+  deformation_rate_body<D, 1, 1, POST, false, OI>(f, sc, dt, loop);
 }
 
 // ------------------------------------------------------------------ density (integrator.cpp:60-78)
@@ -294,7 +305,7 @@ __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int 
 
 // ------------------------------------------------------------------ momentum RHS (integrator.cpp:105-115)
 // KICK: fused tail of verlet pass B (v += dt a, constraints).
-template <int D, int G, int U, bool KICK>
+template <int D, int G, int U, bool KICK, bool OI = false>
 __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, double dt_arg, int loop) {
   if (TLSPH_TL_PDL && G > 1) {
     grid_launch_dependents();  // pass C may launch and wait
@@ -306,7 +317,7 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
   const long long i = tid / G;
   const int l = static_cast<int>(tid % G);
   const bool active = i < f.n && is_owned(f, i);
-  const SlotView<D, G> sv(f);
+  const SlotView<D, G, OI> sv(f);
   double acc[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) acc[d] = 0.0;
@@ -322,13 +333,13 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
       }
     }
     const double V0i = pbi[D * D];
-    const long long hi = f.offs[i + 1];
+    const long long hi = f.offs[i + 1], lo_i = f.offs[i], ob_i = sv.base(f, i);
     for (long long s = f.offs[i] + l; s < hi; s += U * G) {
       int j[U];
       double dw[U], e[U][D];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const long long su = s + u * G < hi ? s + u * G : s;
+        const long long su = sv.at(f, ob_i, lo_i, s + u * G < hi ? s + u * G : s);
         j[u] = sv.nbr[su];
         dw[u] = sv.dw[su];
 #pragma unroll
@@ -398,9 +409,9 @@ template <int D, int G, bool KICK>
 __global__ void TL_BOUNDS_B k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
   momentum_body<D, G, TLSPH_TL_UB, KICK>(f, sc, dt_arg, loop);
 }
-template <int D, bool KICK>
+template <int D, bool KICK, bool OI = false>
 __global__ void k_momentum_ordered(DFields f, DScalars* sc, double dt_arg, int loop) {
-  momentum_body<D, 1, 1, KICK>(f, sc, dt_arg, loop);
+  momentum_body<D, 1, 1, KICK, OI>(f, sc, dt_arg, loop);
 }
 
 template <int D>
@@ -481,10 +492,16 @@ void DevSystem::deformation_rate() {
   DFields f = fields();
   const bool ord = reduction == TLSPH_REDUCTION_ORDERED;
   if (D == 2) {
-    if (ord) k_deformation_rate_ordered<2, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    if (ord) {
+      if (f.onbr) k_deformation_rate_ordered<2, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+      else k_deformation_rate_ordered<2, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    }
     else k_deformation_rate<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   } else {
-    if (ord) k_deformation_rate_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    if (ord) {
+      if (f.onbr) k_deformation_rate_ordered<3, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+      else k_deformation_rate_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    }
     else k_deformation_rate<3, kGC3, false><<<grid_for(n * kGC3, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   }
   CK_LAUNCH("k_deformation_rate");
@@ -509,10 +526,16 @@ void DevSystem::momentum_rhs(const DMaterial& mat) {
   CK_LAUNCH("k_stress");
   raise_if_failed("compute_momentum_rhs");  // the reference throws before the pair loop
   if (D == 2) {
-    if (ord) k_momentum_ordered<2, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    if (ord) {
+      if (f.onbr) k_momentum_ordered<2, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+      else k_momentum_ordered<2, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    }
     else k_momentum<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   } else {
-    if (ord) k_momentum_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    if (ord) {
+      if (f.onbr) k_momentum_ordered<3, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+      else k_momentum_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
+    }
     else k_momentum<3, kGB3, false><<<grid_for(n * kGB3, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   }
   CK_LAUNCH("k_momentum");
@@ -537,20 +560,38 @@ void launch_pdl(void (*kernel)(KArgs...), long long threads, cudaStream_t st, Ar
 void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop, int pass) {
   DFields f = s.fields();
   const long long n = s.n;
-  const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED;
+  // large bodies (group-interleaved slot copy present): both modes run the slot-order one-thread
+  // kernels (build_ordered_rows, state.cu); TLSPH_TL_EIGHT_LANES=1 keeps FAST on eight lanes (A/B)
+  static const bool eight_lanes = [] {
+    const char* e = std::getenv("TLSPH_TL_EIGHT_LANES");
+    return e && *e == '1';
+  }();
+  const bool ord = s.reduction == TLSPH_REDUCTION_ORDERED || (f.onbr && !eight_lanes);
   cudaStream_t st = s.stream;
   if (s.D == 2) {
     if (pass == 0) k_stress<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
-    else if (pass == 1 && ord) k_momentum_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1 && ord) {
+      if (f.onbr) k_momentum_ordered<2, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      else k_momentum_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    }
     else if (pass == 1) launch_pdl(k_momentum<2, 4, true>, n * 4, st, f, s.scal.p, dt, loop);
-    else if (ord) k_deformation_rate_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (ord) {
+      if (f.onbr) k_deformation_rate_ordered<2, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      else k_deformation_rate_ordered<2, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    }
     else if (f.v0_uniform > 0.0) launch_pdl(k_deformation_rate<2, 4, true, true>, n * 4, st, f, s.scal.p, dt, loop);
     else launch_pdl(k_deformation_rate<2, 4, true>, n * 4, st, f, s.scal.p, dt, loop);
   } else {
     if (pass == 0) k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
-    else if (pass == 1 && ord) k_momentum_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (pass == 1 && ord) {
+      if (f.onbr) k_momentum_ordered<3, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      else k_momentum_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    }
     else if (pass == 1) launch_pdl(k_momentum<3, kGB3, true>, n * kGB3, st, f, s.scal.p, dt, loop);
-    else if (ord) k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    else if (ord) {
+      if (f.onbr) k_deformation_rate_ordered<3, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      else k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+    }
     else if (f.v0_uniform > 0.0)
       launch_pdl(k_deformation_rate<3, kGC3, true, true>, n * kGC3, st, f, s.scal.p, dt, loop);
     else launch_pdl(k_deformation_rate<3, kGC3, true>, n * kGC3, st, f, s.scal.p, dt, loop);
