@@ -554,3 +554,25 @@ def test_ke_stop_step_count_matches_reference_path():
     assert ro["steps"] == n_o
     assert rel_l2(stops["ordered"][1], o.get("v")) <= TOL
     assert rel_l2(stops["ordered"][2], o.get("r")) <= TOL
+
+
+@pytest.mark.parametrize("mode", ["fast", "ordered"])
+def test_large_body_loop_matches_oracle(mode):
+    """Bodies of >= 65,536 particles run the TL-SPH neighbour passes as one thread per particle over
+    the group-interleaved slot copy (in both modes): a reduced cfg3 beam (80,000 particles) against
+    the oracle, 6 loop steps with random-choice damping."""
+    cfg = S.cfg3(scale=2)
+    assert len(cfg["r0"]) >= 65536
+    mat = S.material()
+    d = S.build_device(cfg, prepare=True)
+    d.set_reduction(mode)
+    r = d.run(mat, eta=cfg["eta"], alpha=0.5, steps=6, seed=cfg["seed"])
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+    o.set_material(S.E_MOD, S.NU, S.RHO0)
+    o.set("v", cfg["v0"])
+    o.set("body", cfg["body"])
+    o.prepare(threads=O.openmp_threads())
+    ro = o.run(eta=cfg["eta"], alpha=0.5, steps=6, seed=cfg["seed"], threads=O.openmp_threads())
+    assert r["steps"] == ro["steps"] == 6 and r["damped"] == ro["damped"] > 0
+    for name in ("v", "r"):
+        assert rel_l2(d.get(name), o.get(name)) <= TOL, name
