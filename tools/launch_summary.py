@@ -17,7 +17,8 @@ def main(path, header=()):
     for r in csv.DictReader(lines):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = r["Kernel Name"].replace("(anonymous namespace)::", "").split("(")[0].replace("void ", "")
+        name = r["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = name.split("(")[0].replace("void ", "")
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "ns")
         us = v / 1e3 if unit == "ns" else v * 1e3 if unit == "ms" else v
