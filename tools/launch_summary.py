@@ -17,7 +17,7 @@ def main(path, header=()):
     for r in csv.DictReader(lines):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = r["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = r["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
         name = name.split("(")[0].replace("void ", "")
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "ns")
