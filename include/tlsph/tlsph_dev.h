@@ -184,6 +184,17 @@ tlsph_status tlsph_dev_unpack_column_field(tlsph_dev* dev, tlsph_dev_column_fiel
  * into this slab). Both asynchronous. */
 tlsph_status tlsph_dev_push_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field field);
 tlsph_status tlsph_dev_wait_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field field);
+/* Data-free ordering points of the cross-process protocol (same host counter
+ * rule as the halo pushes). mark records this slab's mark event after all work
+ * enqueued so far; wait_mark makes the slab's stream wait on the neighbours'
+ * marks. A sweep starts with mark + wait_mark, so its first phase cannot store
+ * into a neighbour that is still reading its velocities (verlet pass C).
+ * wait_phase(q) makes the stream wait on the neighbours' phase-q events: a
+ * sweep ends with wait_phase(last), so no neighbour store into this slab is
+ * still in flight when the caller reads it. All asynchronous. */
+tlsph_status tlsph_dev_mark_ipc(tlsph_dev* dev);
+tlsph_status tlsph_dev_wait_mark_ipc(tlsph_dev* dev);
+tlsph_status tlsph_dev_wait_phase_ipc(tlsph_dev* dev, int q);
 
 void tlsph_dev_destroy(tlsph_dev* dev);
 

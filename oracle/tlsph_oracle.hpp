@@ -383,66 +383,82 @@ struct Neighborhood {
   std::size_t count(std::size_t i) const { return static_cast<std::size_t>(offsets[i + 1] - offsets[i]); }
 };
 
-// reference: neighbors.cpp:79-141
+// reference: neighbors.cpp:79-141. The per-particle scans are independent, so the checker runs
+// them on an OpenMP team (`threads`, default all): the lists, slot values and the error (the
+// coincident pair the serial loop meets first: lowest i, then that i's first j in stencil order)
+// are those of the reference's serial loop.
 template <int D>
 inline Neighborhood<D> build_reference_neighborhoods(const std::vector<Vec<D>>& r0,
                                                      const std::vector<double>& V0,
                                                      const SmoothingKernel& kernel,
-                                                     const CellGrid<D>& grid) {
+                                                     const CellGrid<D>& grid, int threads = 0) {
   const std::size_t n = r0.size();
   require(V0.size() == n, ErrorKind::InvalidArgument, "volume array size does not match particle count");
+  if (threads <= 0) threads = omp_get_max_threads();
   const double cutoff = kernel.support_radius();
   Neighborhood<D> nbh;
   nbh.offsets.assign(n + 1, 0);
   std::vector<std::vector<int>> lists(n);
-  for (std::size_t i = 0; i < n; ++i) {
-    const auto base = grid.coords_of_position(r0[i]);
-    std::array<int, D> c{};
-    const int stencil = (D == 2) ? 9 : 27;
-    for (int s = 0; s < stencil; ++s) {
-      int rem = s;
-      bool in_range = true;
-      for (int d = 0; d < D; ++d) {
-        c[d] = base[d] + (rem % 3) - 1;
-        rem /= 3;
-        if (c[d] < 0 || c[d] >= grid.dims[d]) in_range = false;
+  std::vector<int> coincident(n, -1);  // first coincident j of particle i (-1: none)
+  parallel_for_range(n, threads, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto base = grid.coords_of_position(r0[i]);
+      std::array<int, D> c{};
+      const int stencil = (D == 2) ? 9 : 27;
+      for (int s = 0; s < stencil && coincident[i] < 0; ++s) {
+        int rem = s;
+        bool in_range = true;
+        for (int d = 0; d < D; ++d) {
+          c[d] = base[d] + (rem % 3) - 1;
+          rem /= 3;
+          if (c[d] < 0 || c[d] >= grid.dims[d]) in_range = false;
+        }
+        if (!in_range) continue;
+        for (int j : grid.cells[static_cast<std::size_t>(grid.linear_index(c))]) {
+          if (static_cast<std::size_t>(j) == i) continue;
+          Vec<D> diff;
+          for (int d = 0; d < D; ++d) diff[d] = r0[i][d] - r0[static_cast<std::size_t>(j)][d];
+          const double dist = norm(diff);
+          if (dist >= cutoff) continue;
+          if (!(dist > 0.0)) {
+            coincident[i] = j;
+            break;
+          }
+          lists[i].push_back(j);
+        }
       }
-      if (!in_range) continue;
-      for (int j : grid.cells[static_cast<std::size_t>(grid.linear_index(c))]) {
-        if (static_cast<std::size_t>(j) == i) continue;
-        Vec<D> diff;
-        for (int d = 0; d < D; ++d) diff[d] = r0[i][d] - r0[static_cast<std::size_t>(j)][d];
-        const double dist = norm(diff);
-        if (dist >= cutoff) continue;
-        require(dist > 0.0, ErrorKind::DegenerateGeometry,
-                "coincident particles " + std::to_string(i) + " and " + std::to_string(j) +
-                    " in reference configuration");
-        lists[i].push_back(j);
-      }
+      std::sort(lists[i].begin(), lists[i].end());
     }
-    std::sort(lists[i].begin(), lists[i].end());
+  });
+  for (std::size_t i = 0; i < n; ++i) {
+    require(coincident[i] < 0, ErrorKind::DegenerateGeometry,
+            "coincident particles " + std::to_string(i) + " and " + std::to_string(coincident[i]) +
+                " in reference configuration");
     nbh.offsets[i + 1] = nbh.offsets[i] + static_cast<std::int64_t>(lists[i].size());
   }
   const std::size_t total = static_cast<std::size_t>(nbh.offsets[n]);
   nbh.neighbor.resize(total); nbh.r0_len.resize(total); nbh.e0.resize(total);
   nbh.dwdr0.resize(total); nbh.pair_factor.resize(total);
-  for (std::size_t i = 0; i < n; ++i) {
-    std::int64_t slot = nbh.offsets[i];
-    for (int j : lists[i]) {
-      Vec<D> diff;
-      for (int d = 0; d < D; ++d) diff[d] = r0[i][d] - r0[static_cast<std::size_t>(j)][d];
-      const double dist = norm(diff);
-      const double dw = kernel.grad_mag(dist);
-      nbh.neighbor[static_cast<std::size_t>(slot)] = j;
-      nbh.r0_len[static_cast<std::size_t>(slot)] = dist;
-      Vec<D> e;
-      for (int d = 0; d < D; ++d) e[d] = diff[d] / dist;
-      nbh.e0[static_cast<std::size_t>(slot)] = e;
-      nbh.dwdr0[static_cast<std::size_t>(slot)] = dw;
-      nbh.pair_factor[static_cast<std::size_t>(slot)] = 2.0 * V0[i] * V0[static_cast<std::size_t>(j)] * dw / dist;
-      ++slot;
+  parallel_for_range(n, threads, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      std::int64_t slot = nbh.offsets[i];
+      for (int j : lists[i]) {
+        Vec<D> diff;
+        for (int d = 0; d < D; ++d) diff[d] = r0[i][d] - r0[static_cast<std::size_t>(j)][d];
+        const double dist = norm(diff);
+        const double dw = kernel.grad_mag(dist);
+        nbh.neighbor[static_cast<std::size_t>(slot)] = j;
+        nbh.r0_len[static_cast<std::size_t>(slot)] = dist;
+        Vec<D> e;
+        for (int d = 0; d < D; ++d) e[d] = diff[d] / dist;
+        nbh.e0[static_cast<std::size_t>(slot)] = e;
+        nbh.dwdr0[static_cast<std::size_t>(slot)] = dw;
+        nbh.pair_factor[static_cast<std::size_t>(slot)] = 2.0 * V0[i] * V0[static_cast<std::size_t>(j)] * dw / dist;
+        ++slot;
+      }
+      std::vector<int>().swap(lists[i]);
     }
-  }
+  });
   return nbh;
 }
 

@@ -233,6 +233,18 @@ tlsph_status tlsph_dev_wait_halo_ipc(tlsph_dev* dev, tlsph_dev_column_field fiel
   return guarded([&] { sys(dev).wait_halo_ipc(field); });
 }
 
+tlsph_status tlsph_dev_mark_ipc(tlsph_dev* dev) {
+  return guarded([&] { sys(dev).mark_ipc(); });
+}
+
+tlsph_status tlsph_dev_wait_mark_ipc(tlsph_dev* dev) {
+  return guarded([&] { sys(dev).wait_mark_ipc(); });
+}
+
+tlsph_status tlsph_dev_wait_phase_ipc(tlsph_dev* dev, int q) {
+  return guarded([&] { sys(dev).wait_phase_ipc(q); });
+}
+
 tlsph_status tlsph_dev_synchronize(tlsph_dev* dev) {
   return guarded([&] {
     DevSystem& s = sys(dev);

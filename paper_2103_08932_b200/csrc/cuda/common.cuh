@@ -138,9 +138,11 @@ struct DFields {
   // the same slots with each row re-ordered by ascending (cell-sorted) neighbour index: the FAST
   // neighbour passes B and C gather from neighbours grouped by cell (fewer cache lines per warp
   // load than the reference's ascending-reference-id order, which the ORDERED kernels keep)
-  // ORDERED neighbour passes: the slot arrays interleaved by groups of 32 consecutive particles
-  // (slot k of particle i at ogbase[i / 32] + 32 k + i % 32), so the one-thread-per-particle
-  // slot-order loops load coalesced; null until the reduction mode is ORDERED (build_ordered_rows)
+  // (snbr/sdw/se0: built for bodies below 65,536 particles only, which run the eight-lane FAST
+  // kernels). Slot-order neighbour passes: the slot arrays interleaved by groups of 32 consecutive
+  // particles (slot k of particle i at ogbase[i / 32] + 32 k + i % 32), so the one-thread-per-
+  // particle loops load coalesced; built for every body of >= 65,536 particles (both modes run the
+  // one-thread kernels there) and for ORDERED mode on smaller ones (build_ordered_rows)
   const int* onbr;
   const double* odw;
   const double* oe0[3];

@@ -1461,7 +1461,7 @@ void DevSystem::ipc_export(IpcExport* out) {
   for (int d = 0; d < D; ++d) CK(cudaIpcGetMemHandle(&out->vel[d], v[d].p));
   CK(cudaIpcGetMemHandle(&out->pbv, pbv.p));
   for (int q = 0; q < out->nphase; ++q) CK(cudaIpcGetEventHandle(&out->ev[q], phase_events[q]));
-  for (int k = 0; k < 2; ++k) CK(cudaIpcGetEventHandle(&out->hev[k], halo_events[k]));
+  for (int k = 0; k < 3; ++k) CK(cudaIpcGetEventHandle(&out->hev[k], halo_events[k]));
 }
 
 void DevSystem::link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start) {
@@ -1490,7 +1490,7 @@ void DevSystem::link_peer_ipc(int side, const IpcExport& peer, const long long* 
     ip.pbv = static_cast<double*>(p);
     ip.n = peer.n;
   }
-  for (int k = 0; k < 2; ++k) CK(cudaIpcOpenEventHandle(&ip.hev[k], peer.hev[k]));
+  for (int k = 0; k < 3; ++k) CK(cudaIpcOpenEventHandle(&ip.hev[k], peer.hev[k]));
   link_peer_arrays(side, peer_cell_start, pv);
 }
 
@@ -1749,6 +1749,33 @@ void DevSystem::wait_halo_ipc(int field) {
   CK(cudaSetDevice(device));
   for (int side = 0; side < 2; ++side)
     if (ipc_peer[side].hev[field]) CK(cudaStreamWaitEvent(stream, ipc_peer[side].hev[field], 0));
+}
+
+// Cross-process ordering points that carry no data. mark_ipc records this slab's mark event after
+// everything enqueued so far (e.g. verlet pass C, which reads the velocities the neighbours' first
+// sweep phase stores into); wait_mark_ipc puts the neighbours' marks in front of this slab's next
+// work. wait_phase_ipc(q) makes the stream wait on the neighbours' phase-q events, so a sweep ends
+// only after every store of theirs into this slab landed. Host ordering as for the halo pushes.
+void DevSystem::mark_ipc() {
+  ensure_phase_events(true);
+  CK(cudaSetDevice(device));
+  CK(cudaEventRecord(halo_events[2], stream));
+}
+
+void DevSystem::wait_mark_ipc() {
+  CK(cudaSetDevice(device));
+  for (int side = 0; side < 2; ++side)
+    if (ipc_peer[side].hev[2]) CK(cudaStreamWaitEvent(stream, ipc_peer[side].hev[2], 0));
+}
+
+void DevSystem::wait_phase_ipc(int q) {
+  CK(cudaSetDevice(device));
+  for (int side = 0; side < 2; ++side) {
+    const IpcPeer& ip = ipc_peer[side];
+    if (ip.ev.empty()) continue;
+    if (q < 0 || q >= static_cast<int>(ip.ev.size())) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "phase out of range");
+    CK(cudaStreamWaitEvent(stream, ip.ev[q], 0));
+  }
 }
 
 int DevSystem::column_width(int field) const { return column_field(*this, field).ncomp; }

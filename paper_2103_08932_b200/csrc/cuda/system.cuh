@@ -52,13 +52,13 @@ struct IpcExport {
   cudaIpcMemHandle_t vel[3];
   cudaIpcMemHandle_t pbv;       // packed P B0 / V0 records (pass A output, pass B input)
   cudaIpcEventHandle_t ev[54];  // colour phases
-  cudaIpcEventHandle_t hev[2];  // halo pushes: TLSPH_DEV_COLUMN_VELOCITY, _STRESS
+  cudaIpcEventHandle_t hev[3];  // halo pushes: TLSPH_DEV_COLUMN_VELOCITY, _STRESS; [2] the mark (tlsph_dev_mark_ipc)
 };
 // A neighbour opened from its export (mapped arrays, its phase and halo events)
 struct IpcPeer {
   std::vector<void*> mem;
   std::vector<cudaEvent_t> ev;
-  cudaEvent_t hev[2] = {nullptr, nullptr};
+  cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
   double* pbv = nullptr;
   long long n = 0;
   void close();
@@ -221,9 +221,12 @@ class DevSystem {
   void link_peer_ipc(int side, const IpcExport& peer, const long long* peer_cell_start);
   void sweep_phase_ipc(int scheme, double eta_tilde, double dt, int q, int wait_q);
   IpcPeer ipc_peer[2];
-  cudaEvent_t halo_events[2] = {nullptr, nullptr};  // interprocess: this slab's halo pushes
+  cudaEvent_t halo_events[3] = {nullptr, nullptr, nullptr};  // interprocess: halo pushes (velocity, stress), mark
   void push_halo_ipc(int field);
   void wait_halo_ipc(int field);
+  void mark_ipc();
+  void wait_mark_ipc();
+  void wait_phase_ipc(int q);
   cudaEvent_t timer_ev[2] = {nullptr, nullptr};  // tlsph_dev_timer_start / _stop
   bool phase_events_ipc = false;
   // x-slab halo columns (sweep.cu)

@@ -490,7 +490,9 @@ void DevSystem::correction_matrices() {
 
 void DevSystem::deformation_rate() {
   DFields f = fields();
-  const bool ord = reduction == TLSPH_REDUCTION_ORDERED;
+  // bodies with the group-interleaved slot copy run the slot-order kernels in both modes, as the
+  // loop does (enqueue_verlet_pass): the standalone operator matches the loop bit for bit
+  const bool ord = reduction == TLSPH_REDUCTION_ORDERED || f.onbr;
   if (D == 2) {
     if (ord) {
       if (f.onbr) k_deformation_rate_ordered<2, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
@@ -520,11 +522,12 @@ void DevSystem::update_density() {
 void DevSystem::momentum_rhs(const DMaterial& mat) {
   reset_errors();
   DFields f = fields();
-  const bool ord = reduction == TLSPH_REDUCTION_ORDERED;
+  bool ord = reduction == TLSPH_REDUCTION_ORDERED;
   dispatch(D, [&] { k_stress<2, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, mat, 0.0, 0); },
            [&] { k_stress<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, mat, 0.0, 0); });
   CK_LAUNCH("k_stress");
   raise_if_failed("compute_momentum_rhs");  // the reference throws before the pair loop
+  ord = ord || f.onbr;  // as deformation_rate: the loop's kernels wherever the interleaved copy exists
   if (D == 2) {
     if (ord) {
       if (f.onbr) k_momentum_ordered<2, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);

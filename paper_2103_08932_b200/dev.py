@@ -142,6 +142,9 @@ def lib():
     L.tlsph_dev_synchronize.argtypes = [P]
     L.tlsph_dev_push_halo_ipc.argtypes = [P, I]
     L.tlsph_dev_wait_halo_ipc.argtypes = [P, I]
+    L.tlsph_dev_mark_ipc.argtypes = [P]
+    L.tlsph_dev_wait_mark_ipc.argtypes = [P]
+    L.tlsph_dev_wait_phase_ipc.argtypes = [P, I]
     L.tlsph_dev_timer_start.argtypes = [P]
     L.tlsph_dev_timer_stop.argtypes = [P]
     L.tlsph_dev_timer_stop.restype = C.c_double
@@ -427,6 +430,18 @@ class DeviceSystem:
     def wait_halo_ipc(self, field):
         """This slab's stream waits on the neighbours' halo pushes of `field` (async)."""
         _check(lib().tlsph_dev_wait_halo_ipc(self._h, COLUMN_FIELDS[field]))
+
+    def mark_ipc(self):
+        """Records this slab's mark event after all work enqueued so far (async)."""
+        _check(lib().tlsph_dev_mark_ipc(self._h))
+
+    def wait_mark_ipc(self):
+        """This slab's stream waits on the neighbours' mark events (async)."""
+        _check(lib().tlsph_dev_wait_mark_ipc(self._h))
+
+    def wait_phase_ipc(self, q):
+        """This slab's stream waits on the neighbours' colour-phase-q events (async)."""
+        _check(lib().tlsph_dev_wait_phase_ipc(self._h, int(q)))
 
     def timer_start(self):
         """Start a device-time span on this system's stream (timer_stop returns its seconds)."""

@@ -436,18 +436,41 @@ class IpcSlabSweep:
         self._group = group
 
     def sweep(self, scheme, eta_tilde, dt, count=1):
-        """`count` sweeps, enqueued phase by phase; returns after this slab's last phase ran."""
+        """`count` sweeps, enqueued phase by phase; returns after this slab's last phase ran and
+        every neighbour store into this slab landed.
+
+        Ordering at the ends of the call: the first phase stores into the neighbours' shared
+        columns, so it waits on their marks (recorded after everything they enqueued before this
+        sweep, e.g. verlet pass C reading those velocities); the last phase of a neighbour may
+        still store into our owned boundary column, so the stream waits on its final phase event
+        before the call returns (the next step's reductions read those velocities)."""
         if eta_tilde == 0.0:
             return
-        for _ in range(count):
+        self._barrier_mark()
+        for k in range(count):
             for q in range(self.nphase):
                 g = self.enqueued
-                if g > 0:
+                first = k == 0 and q == 0
+                if not first:
                     self.counters.wait(self.neighbours, g)
-                self.d.sweep_phase_ipc(scheme, eta_tilde, dt, q, (q - 1) % self.nphase if g > 0 else -1)
+                # the first phase is ordered by the marks; every later one by the neighbours'
+                # previous phase (phase 0 of a later sweep: their last phase)
+                self.d.sweep_phase_ipc(scheme, eta_tilde, dt, q, -1 if first else (q - 1) % self.nphase)
                 self.enqueued = g + 1
                 self.counters.set(self.rank, self.enqueued)
+        self.counters.wait(self.neighbours, self.enqueued)
+        self.d.wait_phase_ipc(self.nphase - 1)
         self.d.synchronize()
+
+    def _barrier_mark(self):
+        """Data-free cross-process ordering point: this slab's stream waits on the neighbours'
+        work enqueued so far (shares the halo counter sequence: every rank issues the same
+        sequence of halo pushes and marks)."""
+        self.d.mark_ipc()
+        self.pushed += 1
+        self.halo_counters.set(self.rank, self.pushed)
+        self.halo_counters.wait(self.neighbours, self.pushed)
+        self.d.wait_mark_ipc()
 
     def halo(self, field):
         """The full loop's halo refresh across processes: push this slab's owned boundary columns of

@@ -686,3 +686,99 @@ def test_lattice_slab_equals_decompose(lo, hi, world):
         assert (sl.x0, sl.x1) == (parts[r].x0, parts[r].x1)
         assert np.array_equal(sl.ids, parts[r].ids) and np.array_equal(lr0, r0[parts[r].ids])
 
+
+
+# ---------------------------------------------------------------- cross-process sweep ordering
+class _RecordingSlab:
+    """Stands in for a DeviceSystem slab in IpcSlabSweep: records the asynchronous calls."""
+
+    def __init__(self, dim):
+        self.dim = dim
+        self.log = []
+
+    def ipc_export(self):
+        return b"x"
+
+    def grid(self):
+        return {"cell_start": np.zeros(2, np.int64)}
+
+    def link_peer_ipc(self, side, blob, cell_start):
+        self.log.append(("link", side))
+
+    def sweep_phase_ipc(self, scheme, eta_tilde, dt, q, wait_q):
+        self.log.append(("phase", q, wait_q))
+
+    def mark_ipc(self):
+        self.log.append(("mark",))
+
+    def wait_mark_ipc(self):
+        self.log.append(("wait_mark",))
+
+    def wait_phase_ipc(self, q):
+        self.log.append(("wait_phase", q))
+
+    def push_halo_ipc(self, field):
+        self.log.append(("push", field))
+
+    def wait_halo_ipc(self, field):
+        self.log.append(("wait_halo", field))
+
+    def synchronize(self):
+        self.log.append(("sync",))
+
+
+def _ipc_order_rank(rank, world, port, result_dir):
+    import pickle
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d = _RecordingSlab(3)
+        sw = slabs.IpcSlabSweep(d, rank, world)
+        sw.halo("stress")
+        sw.halo("velocity")
+        sw.sweep("particle_split", 1.0, 1e-5, count=2)
+        sw.halo("stress")
+        sw.sweep("particle_split", 1.0, 1e-5)
+        sw.close()
+        with open(os.path.join(result_dir, f"log{rank}.pkl"), "wb") as fh:
+            pickle.dump(d.log, fh)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_sweep_ordering_points(tmp_path, world):
+    """IpcSlabSweep.sweep: every sweep call starts with a mark + wait on the
+    neighbours' marks before its first phase (whose stores reach the neighbours' shared columns
+    while they may still run verlet pass C), chains every later phase on the neighbours' previous
+    phase, and ends with a wait on their last phase before the host synchronises."""
+    import pickle
+
+    import torch.multiprocessing as mp
+
+    mp.spawn(_ipc_order_rank, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    nphase = 54
+    for r in range(world):
+        with open(os.path.join(tmp_path, f"log{r}.pkl"), "rb") as fh:
+            log = [x for x in pickle.load(fh) if x[0] != "link"]
+        calls = []
+        i = 0
+        while i < len(log):
+            if log[i][0] == "mark":
+                j = log.index(("sync",), i)
+                calls.append(log[i:j + 1])
+                i = j + 1
+            else:
+                i += 1
+        assert [len(c) for c in calls] == [2 + 2 * nphase + 2, 2 + nphase + 2]
+        for c, count in zip(calls, (2, 1)):
+            assert c[:2] == [("mark",), ("wait_mark",)]
+            phases = c[2:-2]
+            assert phases[0] == ("phase", 0, -1)
+            for g, p in enumerate(phases[1:], start=1):
+                assert p == ("phase", g % nphase, (g - 1) % nphase)
+            assert c[-2:] == [("wait_phase", nphase - 1), ("sync",)]
