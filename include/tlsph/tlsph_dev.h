@@ -205,6 +205,26 @@ int64_t tlsph_dev_slot_count(const tlsph_dev* dev);
 tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const double* host);
 tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host);
 tlsph_status tlsph_dev_set_reduction(tlsph_dev* dev, tlsph_dev_reduction mode);
+/* Transfers in the caller's own per-particle record storage (reference
+ * order), the form the C++ operator API moves ParticleSystem<D> fields in
+ * without repacking: a vector field is D doubles per particle, a matrix field
+ * D*D doubles, row-major (TLSPH_LAYOUT_ROW_MAJOR) or column-major
+ * (TLSPH_LAYOUT_COL_MAJOR: tlsph::Mat<D>, Eigen's storage order);
+ * TLSPH_FIELD_CONSTRAINED is one byte (0/1) per particle here.
+ * tlsph_dev_refresh uploads, compares bitwise with the resident copy on the
+ * device and keeps it when equal (*changed = 0), so derived per-particle data
+ * (inverse masses, clamp bits, fold constants) is rebuilt only when the
+ * caller really changed the field. For TLSPH_FIELD_R0 a difference is an
+ * error (the cell order is built from r0). A null host array for
+ * TLSPH_FIELD_BODY removes the body term (ExternalAccel<D>::body empty). */
+typedef enum tlsph_dev_layout { TLSPH_LAYOUT_ROW_MAJOR = 0, TLSPH_LAYOUT_COL_MAJOR = 1 } tlsph_dev_layout;
+tlsph_status tlsph_dev_put(tlsph_dev* dev, tlsph_dev_field field, const void* host, int layout);
+tlsph_status tlsph_dev_refresh(tlsph_dev* dev, tlsph_dev_field field, const void* host, int layout, int* changed);
+tlsph_status tlsph_dev_take(const tlsph_dev* dev, tlsph_dev_field field, void* host, int layout);
+/* Cumulative bytes moved between host memory and the device by the field
+ * transfers of all handles of this process (set/get_field, put/refresh/take). */
+void tlsph_dev_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+
 
 /* Per-step re-sort (BASELINE cfg4): with `on`, every step of tlsph_dev_run
  * first rebuilds a storage permutation keyed by each particle's CURRENT-position

@@ -180,17 +180,26 @@ class OracleSystem:
         _check(lib().orc_blocks(self._h, bs.ctypes.data_as(C.POINTER(C.c_longlong)), bc.ctypes.data_as(C.POINTER(C.c_int))))
         return [bc[bs[b]:bs[b + 1]].tolist() for b in range(nb)]
 
-    def neighborhood(self):
+    def neighborhood(self, fields=None):
+        """ReferenceNeighborhood arrays; `fields` (names) limits which are copied out."""
+        want = set(fields) if fields is not None else {"offsets", "neighbor", "r0_len", "e0", "dwdr0", "pair_factor"}
         S = int(lib().orc_slot_count(self._h))
         off = np.empty(self.n + 1, dtype=np.int64)
-        nb = np.empty(S, dtype=np.int32)
-        ln = np.empty(S)
-        e0 = np.empty((S, self.dim))
-        dw = np.empty(S)
-        pf = np.empty(S)
-        _check(lib().orc_get_neighborhood(self._h, off.ctypes.data_as(C.POINTER(C.c_longlong)),
-                                          nb.ctypes.data_as(C.POINTER(C.c_int)), _dp(ln), _dp(e0), _dp(dw), _dp(pf)))
-        return {"offsets": off, "neighbor": nb, "r0_len": ln, "e0": e0, "dwdr0": dw, "pair_factor": pf}
+        nb = np.empty(S if "neighbor" in want else 0, dtype=np.int32)
+        ln = np.empty(S if "r0_len" in want else 0)
+        e0 = np.empty((S if "e0" in want else 0, self.dim))
+        dw = np.empty(S if "dwdr0" in want else 0)
+        pf = np.empty(S if "pair_factor" in want else 0)
+
+        def ptr(a, name, t=None):
+            if name not in want:
+                return None
+            return a.ctypes.data_as(C.POINTER(t)) if t is not None else _dp(a)
+
+        _check(lib().orc_get_neighborhood(self._h, off.ctypes.data_as(C.POINTER(C.c_longlong)), ptr(nb, "neighbor", C.c_int),
+                        ptr(ln, "r0_len"), ptr(e0, "e0"), ptr(dw, "dwdr0"), ptr(pf, "pair_factor")))
+        out = {"offsets": off, "neighbor": nb, "r0_len": ln, "e0": e0, "dwdr0": dw, "pair_factor": pf}
+        return {k: v for k, v in out.items() if k in want or k == "offsets"}
 
     def set_neighborhood(self, offsets, neighbor, r0_len, e0, dwdr0, pf):
         off = np.ascontiguousarray(offsets, dtype=np.int64)

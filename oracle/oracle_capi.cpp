@@ -238,12 +238,14 @@ int orc_get_neighborhood(void* hv, long long* offsets, int* neighbor, double* r0
     with_sim(hv, [&](auto& s) {
       constexpr int D = std::remove_reference_t<decltype(s)>::dim;
       const auto& b = s.nbh;
-      std::copy(b.offsets.begin(), b.offsets.end(), offsets);
-      std::copy(b.neighbor.begin(), b.neighbor.end(), neighbor);
-      std::copy(b.r0_len.begin(), b.r0_len.end(), r0_len);
-      for (std::size_t k = 0; k < b.e0.size(); ++k) for (int d = 0; d < D; ++d) e0[k * D + d] = b.e0[k][d];
-      std::copy(b.dwdr0.begin(), b.dwdr0.end(), dwdr0);
-      std::copy(b.pair_factor.begin(), b.pair_factor.end(), pf);
+      // any output may be null (not copied)
+      if (offsets) std::copy(b.offsets.begin(), b.offsets.end(), offsets);
+      if (neighbor) std::copy(b.neighbor.begin(), b.neighbor.end(), neighbor);
+      if (r0_len) std::copy(b.r0_len.begin(), b.r0_len.end(), r0_len);
+      if (e0)
+        for (std::size_t k = 0; k < b.e0.size(); ++k) for (int d = 0; d < D; ++d) e0[k * D + d] = b.e0[k][d];
+      if (dwdr0) std::copy(b.dwdr0.begin(), b.dwdr0.end(), dwdr0);
+      if (pf) std::copy(b.pair_factor.begin(), b.pair_factor.end(), pf);
     });
   });
 }

@@ -1,3 +1,4 @@
+#include <atomic>
 // extern "C" boundary of libtlsph_cuda.so (declared in include/tlsph/tlsph_dev.h).
 // Exception-free: every entry point maps DevError / std::exception to a
 // tlsph_status and a thread-local message, as the reference C API does
@@ -351,6 +352,23 @@ int64_t tlsph_dev_slot_count(const tlsph_dev* dev) { return dev ? dev->sys.nslot
 
 tlsph_status tlsph_dev_set_field(tlsph_dev* dev, tlsph_dev_field field, const double* host) {
   return guarded([&] { sys(dev).set_field(field, host); });
+}
+
+tlsph_status tlsph_dev_put(tlsph_dev* dev, tlsph_dev_field field, const void* host, int layout) {
+  return guarded([&] { sys(dev).put_record(field, host, layout, false, nullptr); });
+}
+
+tlsph_status tlsph_dev_refresh(tlsph_dev* dev, tlsph_dev_field field, const void* host, int layout, int* changed) {
+  return guarded([&] { sys(dev).put_record(field, host, layout, true, changed); });
+}
+
+void tlsph_dev_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+  if (h2d) *h2d = tlsph_cuda::g_h2d_bytes.load();
+  if (d2h) *d2h = tlsph_cuda::g_d2h_bytes.load();
+}
+
+tlsph_status tlsph_dev_take(const tlsph_dev* dev, tlsph_dev_field field, void* host, int layout) {
+  return guarded([&] { sys(dev).take_record(field, host, layout); });
 }
 
 tlsph_status tlsph_dev_get_field(const tlsph_dev* dev, tlsph_dev_field field, double* host) {

@@ -1,3 +1,4 @@
+#include <atomic>
 // Device system construction: the GPU splitting cell-linked list.
 //
 //   bbox -> cell keys -> counting sort (histogram, exclusive scan, scatter,
@@ -16,6 +17,10 @@
 #include "system.cuh"
 
 namespace tlsph_cuda {
+
+// Bytes moved between the caller's host memory and the device by field transfers (all handles).
+std::atomic<unsigned long long> g_h2d_bytes{0}, g_d2h_bytes{0};
+
 
 namespace {
 
@@ -373,6 +378,57 @@ __global__ void k_soa_to_aos(double* __restrict__ dst, int comps, long long n, c
   if (s >= n) return;
   const long long i = perm[s];
   for (int c = 0; c < comps; ++c) dst[i * comps + c] = src.p[c][s];
+}
+
+// Record transfers in the caller's storage: component c of a D x D matrix (row r = c / D, column
+// c % D) sits at c in row-major records and at (c % D) * D + c / D in column-major ones (cm = D).
+__device__ __forceinline__ int record_index(int c, int cm) { return cm ? (c % cm) * cm + c / cm : c; }
+
+__global__ void k_records_in(const double* __restrict__ src, int comps, int cm, long long n,
+                             const int* __restrict__ perm, FieldPtrs dst) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const long long i = perm[s];
+  for (int c = 0; c < comps; ++c) dst.p[c][s] = src[i * comps + record_index(c, cm)];
+}
+
+__global__ void k_records_out(double* __restrict__ dst, int comps, int cm, long long n, const int* __restrict__ perm,
+                              FieldPtrs src) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const long long i = perm[s];
+  for (int c = 0; c < comps; ++c) dst[i * comps + record_index(c, cm)] = src.p[c][s];
+}
+
+// Sets *differs when any staged record differs bitwise from the resident field.
+__global__ void k_records_differ(const double* __restrict__ src, int comps, int cm, long long n,
+                                 const int* __restrict__ perm, FieldPtrs cur, int* differs) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool d = false;
+  if (s < n) {
+    const long long i = perm[s];
+    for (int c = 0; c < comps; ++c)
+      d = d || __double_as_longlong(src[i * comps + record_index(c, cm)]) != __double_as_longlong(cur.p[c][s]);
+  }
+  if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) atomicOr(differs, 1);
+}
+
+__global__ void k_flags_in(const uint8_t* __restrict__ src, long long n, const int* __restrict__ perm, uint8_t* flag,
+                           int* differs) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool d = false;
+  if (s < n) {
+    const uint8_t v = src[perm[s]] != 0 ? 1 : 0;
+    d = v != flag[s];
+    if (!differs) flag[s] = v;
+  }
+  if (differs && __any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) atomicOr(differs, 1);
+}
+
+__global__ void k_flags_out(uint8_t* __restrict__ dst, long long n, const int* __restrict__ perm,
+                            const uint8_t* __restrict__ flag) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s < n) dst[perm[s]] = flag[s];
 }
 
 __global__ void k_minvf(const double* __restrict__ m, const uint8_t* __restrict__ flag, double* __restrict__ y,
@@ -1152,6 +1208,7 @@ void DevSystem::set_field(int field, const double* host) {
   FieldSpec fs = field_spec(*this, field);
   tmp.alloc(N * fs.comps);
   CK(cudaMemcpyAsync(tmp.p, host, N * fs.comps * sizeof(double), cudaMemcpyHostToDevice, stream));
+  g_h2d_bytes += N * fs.comps * sizeof(double);
   k_aos_to_soa<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, fs.pack());
   CK_LAUNCH("k_aos_to_soa");
   if (field == TLSPH_FIELD_BODY) has_body = true;
@@ -1180,6 +1237,96 @@ void DevSystem::get_field(int field, double* host) const {
   k_soa_to_aos<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, fs.pack());
   CK_LAUNCH("k_soa_to_aos");
   CK(cudaMemcpyAsync(host, tmp.p, N * fs.comps * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  sync();
+}
+
+void DevSystem::put_record(int field, const void* host, int layout, bool only_if_changed, int* changed) {
+  if (!host && field == TLSPH_FIELD_BODY) {  // no body term (ExternalAccel::body empty)
+    if (changed) *changed = has_body ? 1 : 0;
+    has_body = false;
+    return;
+  }
+  if (!host) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null host array");
+  if (layout != 0 && layout != 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "record layout must be 0 or 1");
+  const size_t N = static_cast<size_t>(n);
+  if (changed) *changed = 1;
+  DBuf<int>& differs = flag_buf;
+  differs.alloc(1);
+  auto any_differs = [&] {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, differs.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    return h != 0;
+  };
+  if (field == TLSPH_FIELD_CONSTRAINED) {
+    tmp.alloc((N + 7) / 8);
+    auto* staged = reinterpret_cast<uint8_t*>(tmp.p);
+    CK(cudaMemcpyAsync(staged, host, N, cudaMemcpyHostToDevice, stream));
+    g_h2d_bytes += N;
+    if (only_if_changed) {
+      CK(cudaMemsetAsync(differs.p, 0, sizeof(int), stream));
+      k_flags_in<<<grid_for(n, 256), 256, 0, stream>>>(staged, n, perm.p, flag.p, differs.p);
+      CK_LAUNCH("k_flags_in");
+      if (!any_differs()) {
+        if (changed) *changed = 0;
+        return;
+      }
+    }
+    k_flags_in<<<grid_for(n, 256), 256, 0, stream>>>(staged, n, perm.p, flag.p, nullptr);
+    CK_LAUNCH("k_flags_in");
+    refresh_minvf();
+    sync();
+    return;
+  }
+  FieldSpec fs = field_spec(*this, field == TLSPH_FIELD_R0 ? TLSPH_FIELD_R0 : field);
+  const int cm = layout == 1 && fs.comps == D * D ? D : 0;
+  tmp.alloc(N * fs.comps);
+  CK(cudaMemcpyAsync(tmp.p, host, N * fs.comps * sizeof(double), cudaMemcpyHostToDevice, stream));
+  g_h2d_bytes += N * fs.comps * sizeof(double);
+  if (only_if_changed || field == TLSPH_FIELD_R0) {
+    CK(cudaMemsetAsync(differs.p, 0, sizeof(int), stream));
+    k_records_differ<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, cm, n, perm.p, fs.pack(), differs.p);
+    CK_LAUNCH("k_records_differ");
+    if (!any_differs()) {
+      if (changed) *changed = 0;
+      return;
+    }
+    if (field == TLSPH_FIELD_R0)
+      throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "r0 is fixed at construction (the cell grid is built from it)");
+  }
+  k_records_in<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, cm, n, perm.p, fs.pack());
+  CK_LAUNCH("k_records_in");
+  if (field == TLSPH_FIELD_BODY) has_body = true;
+  if (field == TLSPH_FIELD_M) {
+    refresh_minvf();
+    fold_valid = false;  // diag = sum b - m_i
+  }
+  if (field == TLSPH_FIELD_V0) refresh_v0_uniform();
+  sync();
+}
+
+void DevSystem::take_record(int field, void* host, int layout) const {
+  if (!host) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null host array");
+  if (layout != 0 && layout != 1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "record layout must be 0 or 1");
+  const size_t N = static_cast<size_t>(n);
+  auto* self = const_cast<DevSystem*>(this);
+  if (field == TLSPH_FIELD_CONSTRAINED) {
+    self->tmp.alloc((N + 7) / 8);
+    auto* staged = reinterpret_cast<uint8_t*>(tmp.p);
+    k_flags_out<<<grid_for(n, 256), 256, 0, stream>>>(staged, n, perm.p, flag.p);
+    CK_LAUNCH("k_flags_out");
+    CK(cudaMemcpyAsync(host, staged, N, cudaMemcpyDeviceToHost, stream));
+    g_d2h_bytes += N;
+    sync();
+    return;
+  }
+  FieldSpec fs = field_spec(*this, field);
+  const int cm = layout == 1 && fs.comps == D * D ? D : 0;
+  self->tmp.alloc(N * fs.comps);
+  k_records_out<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, cm, n, perm.p, fs.pack());
+  CK_LAUNCH("k_records_out");
+  CK(cudaMemcpyAsync(host, tmp.p, N * fs.comps * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  g_d2h_bytes += N * fs.comps * sizeof(double);
   sync();
 }
 

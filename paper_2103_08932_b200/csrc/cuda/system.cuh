@@ -2,6 +2,7 @@
 // the opaque tlsph_dev handle of include/tlsph/tlsph_dev.h).
 #pragma once
 
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -41,6 +42,9 @@ struct DBuf {
 };
 
 struct SweepPlan;  // damping.cu
+
+// bytes moved by field transfers between host memory and the device (state.cu)
+extern std::atomic<unsigned long long> g_h2d_bytes, g_d2h_bytes;
 
 // A slab's export for cross-process linking: its velocity arrays and colour-phase events as
 // CUDA IPC handles (tlsph_dev_ipc_export); plain bytes, exchanged by the host.
@@ -158,6 +162,7 @@ class DevSystem {
   // scratch
   DBuf<DScalars> scal;
   DBuf<double> tmp;        // AoS staging for host transfers
+  DBuf<int> flag_buf;      // put_record change detection
   DBuf<long long> tmp_i64;
   DBuf<int> tmp_i32;
   DBuf<double> red;        // reduction partials
@@ -182,6 +187,12 @@ class DevSystem {
   // transfers (state.cu)
   void set_field(int field, const double* host);
   void get_field(int field, double* host) const;
+  // the caller's own record storage (tlsph_dev_put / _take / _refresh): vectors D doubles,
+  // matrices D*D doubles row-major (layout 0) or column-major (layout 1: tlsph::Mat, Eigen);
+  // TLSPH_FIELD_CONSTRAINED as one byte per particle. only_if_changed: upload, compare with the
+  // resident copy on the device and keep it when bitwise equal (*changed = 0).
+  void put_record(int field, const void* host, int layout, bool only_if_changed, int* changed);
+  void take_record(int field, void* host, int layout) const;
   void grid_cells(int32_t* cell_of, int64_t* cell_start_h, int32_t* cell_particles) const;
   void get_neighborhood(int64_t* offsets, int32_t* neighbor, double* r0_len_h, double* e0_h, double* dwdr0_h,
                         double* pf_h) const;

@@ -1,13 +1,15 @@
 // Random-choice splitting damping through the device (reference:
 // proj/src/tlsph/damping.cpp:12-182). Scalar helpers stay on the host; the
-// operators upload the system and neighbourhood, run the sm_100a kernels in
-// ORDERED mode (bit-identical to the reference arithmetic) and download v.
+// operators run the sm_100a kernels on the device system kept resident for
+// the caller's neighbourhood (resident.hpp), moving only v (and the masses and
+// clamp flags the update reads) per call. Default ORDERED reductions:
+// bit-identical to the reference arithmetic (tlsph/device.hpp).
 #include "tlsph/damping.hpp"
 
 #include <cmath>
 #include <string>
 
-#include "devbridge.hpp"
+#include "resident.hpp"
 #include "tlsph/errors.hpp"
 
 namespace tlsph {
@@ -34,36 +36,45 @@ double random_choice_eta(double eta, double alpha, RandomSource& rng) {
   return phi < alpha ? eta / alpha : 0.0;
 }
 
+// Inputs of the local damping operators: v and the masses / clamp flags (damping.cpp:53-106).
+template <int D>
+void put_damping_inputs(tlsph_dev* dev, const ParticleSystem<D>& system) {
+  host::put(dev, TLSPH_FIELD_V, system.v);
+  host::refresh(dev, TLSPH_FIELD_M, system.m);
+  host::refresh(dev, TLSPH_FIELD_CONSTRAINED, system.constrained);
+}
+
 template <int D>
 void explicit_damping_accel(const ParticleSystem<D>& system, const ReferenceNeighborhood<D>& nbh, double eta,
                             std::vector<Vec<D>>& out, int threads) {
   (void)threads;
   out.resize(system.size());
-  auto h = host::upload<D>(system, nbh, host::coarse_cutoff<D>(system, nbh));
-  host::put<D>(h.get(), TLSPH_FIELD_V, system.v);
-  std::vector<double> flat(system.size() * D);
-  host::check(tlsph_dev_explicit_damping_accel(h.get(), eta, flat.data()));
-  host::unflatten<D>(flat, out);
+  auto lease = host::resident<D>(system, nbh, nullptr);
+  put_damping_inputs<D>(lease.get(), system);
+  static_assert(sizeof(Vec<D>) == D * sizeof(double));
+  host::check(tlsph_dev_explicit_damping_accel(lease.get(), eta, reinterpret_cast<double*>(out.data())));
 }
 
 template <int D>
 void particle_split_update(std::size_t i, ParticleSystem<D>& system, const ReferenceNeighborhood<D>& nbh, double eta,
                            double dt_half) {
-  auto h = host::upload<D>(system, nbh, host::coarse_cutoff<D>(system, nbh));
-  host::put<D>(h.get(), TLSPH_FIELD_V, system.v);
-  host::check(tlsph_dev_particle_split_update(h.get(), i, eta, dt_half));
-  host::get<D>(h.get(), TLSPH_FIELD_V, system.v);
+  auto lease = host::resident<D>(system, nbh, nullptr);
+  put_damping_inputs<D>(lease.get(), system);
+  host::check(tlsph_dev_particle_split_update(lease.get(), i, eta, dt_half));
+  host::take(lease.get(), TLSPH_FIELD_V, system.v);
 }
 
 template <int D>
 void pairwise_split_update(std::size_t i, std::int64_t slot, ParticleSystem<D>& system,
                            const ReferenceNeighborhood<D>& nbh, double eta, double dt_half) {
-  auto h = host::upload<D>(system, nbh, host::coarse_cutoff<D>(system, nbh));
-  host::put<D>(h.get(), TLSPH_FIELD_V, system.v);
-  host::check(tlsph_dev_pairwise_split_update(h.get(), i, slot, eta, dt_half));
-  host::get<D>(h.get(), TLSPH_FIELD_V, system.v);
+  auto lease = host::resident<D>(system, nbh, nullptr);
+  put_damping_inputs<D>(lease.get(), system);
+  host::check(tlsph_dev_pairwise_split_update(lease.get(), i, slot, eta, dt_half));
+  host::take(lease.get(), TLSPH_FIELD_V, system.v);
 }
 
+// The sweep runs over the caller's grid: the resident system's cell order is checked against it
+// once (build_cell_grid of the same r0 and cell size gives the same cells bit for bit).
 template <int D>
 void strang_damping_sweep(ParticleSystem<D>& system, const ReferenceNeighborhood<D>& nbh, const CellGrid<D>& grid,
                           const BlockDecomposition<D>& blocks, DampingScheme scheme, double eta_tilde, double dt,
@@ -73,11 +84,11 @@ void strang_damping_sweep(ParticleSystem<D>& system, const ReferenceNeighborhood
   if (eta_tilde == 0.0) return;
   require(scheme != DampingScheme::Explicit, ErrorKind::InvalidArgument,
           "the explicit scheme is integrated directly, not swept");
-  auto h = host::upload<D>(system, nbh, grid.cell_size);
-  host::put<D>(h.get(), TLSPH_FIELD_V, system.v);
+  auto lease = host::resident<D>(system, nbh, &grid);
+  put_damping_inputs<D>(lease.get(), system);
   const auto s = scheme == DampingScheme::ParticleSplit ? TLSPH_SCHEME_PARTICLE_SPLIT : TLSPH_SCHEME_PAIRWISE_SPLIT;
-  host::check(tlsph_dev_damping_sweep(h.get(), s, eta_tilde, dt));
-  host::get<D>(h.get(), TLSPH_FIELD_V, system.v);
+  host::check(tlsph_dev_damping_sweep(lease.get(), s, eta_tilde, dt));
+  host::take(lease.get(), TLSPH_FIELD_V, system.v);
 }
 
 #define TLSPH_INSTANTIATE(D)                                                                                    \

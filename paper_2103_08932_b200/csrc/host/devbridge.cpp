@@ -54,25 +54,7 @@ double coarse_cutoff(const ParticleSystem<D>& system, const ReferenceNeighborhoo
   return c > 0.0 ? c : 1.0;
 }
 
-template <int D>
-DevHandle upload(const ParticleSystem<D>& system, const ReferenceNeighborhood<D>& nbh, double cutoff) {
-  const size_t n = system.size();
-  require(n > 0, ErrorKind::InvalidArgument, "particle system is empty");
-  require(nbh.offsets.size() == n + 1, ErrorKind::InvalidArgument, "neighbourhood does not match the system");
-  const auto r0 = flatten<D>(system.r0);
-  const auto e0 = flatten<D>(nbh.e0);
-  DevHandle h;
-  check(tlsph_dev_create_with_csr(D, n, r0.data(), system.V0.data(), system.rho0.data(), system.constrained.data(),
-                                  0.5 * cutoff, nbh.offsets.data(), nbh.neighbor.data(), nbh.r0_len.data(),
-                                  e0.data(), nbh.dwdr0.data(), nbh.pair_factor.data(), h.out()));
-  check(tlsph_dev_set_reduction(h.get(), TLSPH_REDUCTION_ORDERED));
-  put(h.get(), TLSPH_FIELD_M, system.m);  // masses may differ from rho0 V0 in hand-built systems
-  return h;
-}
-
 template double coarse_cutoff<2>(const ParticleSystem<2>&, const ReferenceNeighborhood<2>&);
 template double coarse_cutoff<3>(const ParticleSystem<3>&, const ReferenceNeighborhood<3>&);
-template DevHandle upload<2>(const ParticleSystem<2>&, const ReferenceNeighborhood<2>&, double);
-template DevHandle upload<3>(const ParticleSystem<3>&, const ReferenceNeighborhood<3>&, double);
 
 }  // namespace tlsph::host

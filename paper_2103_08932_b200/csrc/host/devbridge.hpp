@@ -48,72 +48,7 @@ class DevHandle {
   tlsph_dev* p_ = nullptr;
 };
 
-template <int D>
-std::vector<double> flatten(const std::vector<Vec<D>>& a) {
-  std::vector<double> out(a.size() * D);
-  for (size_t i = 0; i < a.size(); ++i)
-    for (int d = 0; d < D; ++d) out[i * D + d] = a[i][d];
-  return out;
-}
-
-template <int D>
-std::vector<double> flatten(const std::vector<Mat<D>>& a) {
-  std::vector<double> out(a.size() * D * D);
-  for (size_t i = 0; i < a.size(); ++i)
-    for (int r = 0; r < D; ++r)
-      for (int c = 0; c < D; ++c) out[(i * D + r) * D + c] = a[i](r, c);
-  return out;
-}
-
-template <int D>
-void unflatten(const std::vector<double>& in, std::vector<Vec<D>>& a) {
-  for (size_t i = 0; i < a.size(); ++i)
-    for (int d = 0; d < D; ++d) a[i][d] = in[i * D + d];
-}
-
-template <int D>
-void unflatten(const std::vector<double>& in, std::vector<Mat<D>>& a) {
-  for (size_t i = 0; i < a.size(); ++i)
-    for (int r = 0; r < D; ++r)
-      for (int c = 0; c < D; ++c) a[i](r, c) = in[(i * D + r) * D + c];
-}
-
-template <int D>
-void put(tlsph_dev* dev, tlsph_dev_field f, const std::vector<Vec<D>>& a) {
-  const auto flat = flatten<D>(a);
-  check(tlsph_dev_set_field(dev, f, flat.data()));
-}
-template <int D>
-void put(tlsph_dev* dev, tlsph_dev_field f, const std::vector<Mat<D>>& a) {
-  const auto flat = flatten<D>(a);
-  check(tlsph_dev_set_field(dev, f, flat.data()));
-}
-inline void put(tlsph_dev* dev, tlsph_dev_field f, const std::vector<double>& a) {
-  check(tlsph_dev_set_field(dev, f, a.data()));
-}
-template <int D>
-void get(tlsph_dev* dev, tlsph_dev_field f, std::vector<Vec<D>>& a) {
-  std::vector<double> flat(a.size() * D);
-  check(tlsph_dev_get_field(dev, f, flat.data()));
-  unflatten<D>(flat, a);
-}
-template <int D>
-void get(tlsph_dev* dev, tlsph_dev_field f, std::vector<Mat<D>>& a) {
-  std::vector<double> flat(a.size() * D * D);
-  check(tlsph_dev_get_field(dev, f, flat.data()));
-  unflatten<D>(flat, a);
-}
-inline void get(tlsph_dev* dev, tlsph_dev_field f, std::vector<double>& a) {
-  check(tlsph_dev_get_field(dev, f, a.data()));
-}
-
 tlsph_dev_material to_dev(const Material& m);
-
-// A device system holding `system` and the caller's neighbourhood (reference
-// order), with the cell grid for cutoff `cutoff`; ORDERED reductions so the
-// operator API reproduces the reference arithmetic bit for bit.
-template <int D>
-DevHandle upload(const ParticleSystem<D>& system, const ReferenceNeighborhood<D>& nbh, double cutoff);
 
 // Grid cutoff for operators that never sweep: a single cell over the body.
 template <int D>

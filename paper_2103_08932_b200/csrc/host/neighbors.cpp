@@ -10,6 +10,7 @@
 #include <string>
 
 #include "devbridge.hpp"
+#include "resident.hpp"
 #include "tlsph/errors.hpp"
 
 namespace tlsph {
@@ -89,10 +90,13 @@ ReferenceNeighborhood<D> build_reference_neighborhoods(std::span<const Vec<D>> r
   nbh.dwdr0.resize(static_cast<size_t>(S));
   nbh.pair_factor.resize(static_cast<size_t>(S));
   nbh.e0.resize(static_cast<size_t>(S));
-  std::vector<double> e0(static_cast<size_t>(S) * D);
-  host::check(tlsph_dev_get_neighborhood(h.get(), nbh.offsets.data(), nbh.neighbor.data(), nbh.r0_len.data(), e0.data(),
-                                         nbh.dwdr0.data(), nbh.pair_factor.data()));
-  host::unflatten<D>(e0, nbh.e0);
+  static_assert(sizeof(Vec<D>) == D * sizeof(double));
+  host::check(tlsph_dev_get_neighborhood(h.get(), nbh.offsets.data(), nbh.neighbor.data(), nbh.r0_len.data(),
+                                         reinterpret_cast<double*>(nbh.e0.data()), nbh.dwdr0.data(),
+                                         nbh.pair_factor.data()));
+  // the device system that built the CSR stays resident for the operators that will use it
+  // (returned by value, the vectors keep their storage, so the registered identity holds)
+  host::adopt<D>(std::move(h), nbh);
   return nbh;
 }
 
