@@ -333,7 +333,8 @@ typedef struct tlsph_dev_loop_params {
   double* probe_out;
   size_t probe_capacity;
   int pause_on_mark;     /* 1: return after each recorded mark (snapshots "all"); resume with resume = 1 */
-  int resume;            /* 1: continue the paused loop (same eta~ stream, t, step count) */
+  int resume;            /* 1: continue the previous loop, paused at a mark or stopped at max_steps
+                          * (same eta~ stream, t, step count; max_steps counts from the start) */
 } tlsph_dev_loop_params;
 
 typedef struct tlsph_dev_loop_result {
@@ -341,7 +342,7 @@ typedef struct tlsph_dev_loop_result {
   uint64_t damped_steps;
   double t;
   double last_dt;
-  double elastic_seconds; /* device time of the elastic kernels */
+  double elastic_seconds; /* device time of step_begin (stable_dt, checks, re-sort) + the elastic kernels */
   double damping_seconds; /* device time of the damping kernels */
   double total_seconds;   /* device time of the whole loop */
   double peak_ke;

@@ -258,9 +258,12 @@ class OracleSystem:
         return out
 
     def run(self, *, eta, alpha, scheme="particle_split", steps, fixed_dt=0.0, end_time=0.0,
-            elastic=True, seed=0, threads=1):
+            elastic=True, seed=0, threads=1, resume=False):
+        """runner.cpp:341-391. resume=True continues the previous run (same damping stream, t and
+        step count; `steps` is then the cumulative cap; the returned counts are cumulative, the
+        times are those of this call)."""
         params = np.array([self.h, eta, alpha, SCHEMES[scheme], steps, fixed_dt, end_time,
-                           1.0 if elastic else 0.0, seed, threads], dtype=np.float64)
+                           1.0 if elastic else 0.0, seed, threads, 1.0 if resume else 0.0], dtype=np.float64)
         out = np.zeros(8)
         _check(lib().orc_run(self._h, _dp(params), _dp(out)))
         return {"steps": int(out[0]), "damped": int(out[1]), "t": out[2], "elastic_s": out[3],

@@ -39,6 +39,10 @@ struct Sim {
   orc::ExternalAccel<D> ext;
   orc::Material mat;
   double h = 0.0;
+  // loop state kept for a resumed run (orc_run with params[10] != 0): the damping stream, t, counts
+  std::unique_ptr<orc::RandomSource> loop_rng;
+  double loop_t = 0.0;
+  long long loop_steps = 0, loop_damped = 0;
 };
 
 struct Handle {
@@ -402,12 +406,20 @@ int orc_run(void* hv, const double* params, double* out) {
       const bool elastic = params[7] != 0.0;
       const auto seed = static_cast<std::uint64_t>(params[8]);
       const int threads = static_cast<int>(params[9]);
-      orc::RandomSource rng(seed);
+      // params[10] != 0: continue the previous run (same RandomSource stream, t and step count;
+      // max_steps is cumulative), as the device loop's resume does
+      const bool resume = params[10] != 0.0 && s.loop_rng;
+      if (!resume) {
+        s.loop_rng = std::make_unique<orc::RandomSource>(seed);
+        s.loop_t = 0.0;
+        s.loop_steps = s.loop_damped = 0;
+      }
+      orc::RandomSource& rng = *s.loop_rng;
       const bool damping_active = eta > 0.0;
       orc::ViscousBounds vb{};
       if (damping_active) vb = orc::viscous_dt_bounds(h, eta / (alpha * s.mat.rho0), std::remove_reference_t<decltype(s)>::dim);
-      double t = 0.0, el = 0.0, dm = 0.0, last_dt = 0.0;
-      long long steps = 0, damped = 0;
+      double t = s.loop_t, el = 0.0, dm = 0.0, last_dt = 0.0;
+      long long steps = s.loop_steps, damped = s.loop_damped;
       std::vector<orc::Vec<std::remove_reference_t<decltype(s)>::dim>> visc;
       while ((end_time <= 0.0 || t < end_time) && steps < max_steps) {
         double dt = fixed_dt > 0.0 ? fixed_dt : orc::stable_dt(s.sys, s.mat, h);
@@ -442,6 +454,9 @@ int orc_run(void* hv, const double* params, double* out) {
         ++steps;
         orc::check_finite(s.sys, static_cast<std::uint64_t>(steps));
       }
+      s.loop_t = t;
+      s.loop_steps = steps;
+      s.loop_damped = damped;
       out[0] = static_cast<double>(steps);
       out[1] = static_cast<double>(damped);
       out[2] = t;

@@ -197,7 +197,7 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   if (damping_active && !(p.alpha > 0.0 && p.alpha <= 1.0))
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "random-choice probability must lie in (0, 1], got " + std::to_string(p.alpha));
-  if (p.resume && !loop_paused) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "no paused loop to resume");
+  if (p.resume && !loop_paused) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "no paused or completed loop to resume");
   const DMaterial mat = to_dmat(p.material);
   const bool want_probe = p.probe_index >= 0 && p.output_interval > 0.0;
   if (want_probe && (p.probe_index >= n || (p.probe_capacity > 0 && !p.probe_out)))
@@ -242,7 +242,8 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     CK(cudaMemcpyAsync(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost, stream));
     sync();
     hs.paused = 0;
-    hs.halt = 0;
+    hs.halt = 0;  // a loop that reached max_steps continues like an uninterrupted one: its last
+                  // step is accounted for (pending 0), the next step_begin only forms dt
     hs.pause_on_mark = p.pause_on_mark;
     CK(cudaMemcpyAsync(scal.p, &hs, sizeof(DScalars), cudaMemcpyHostToDevice, stream));
   }
@@ -297,8 +298,8 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     const uint64_t todo = p.max_steps ? std::min<uint64_t>(chunk, p.max_steps - std::min(p.max_steps, enq)) : chunk;
     CK(cudaEventRecord(ev[3 * chunk], stream));
     for (uint64_t k = 0; k < todo; ++k) {
-      CK(cudaGraphLaunch(g_begin.e, stream));
       CK(cudaEventRecord(ev[3 * k], stream));
+      CK(cudaGraphLaunch(g_begin.e, stream));  // the elastic window includes step_begin (stable_dt, checks)
       if (p.elastic) CK(cudaGraphLaunch(g_elastic.e, stream));
       CK(cudaEventRecord(ev[3 * k + 1], stream));
       if (damping_active && outcome(enq + k)) CK(cudaGraphLaunch(g_damp.e, stream));
@@ -346,7 +347,8 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   last_elapsed = loop_tot;
   last_run_steps = static_cast<long long>(hs.steps);  // also when the loop stopped on an error
   last_run_t = hs.t;
-  loop_paused = hs.paused != 0 && !hs.failed;
+  // resumable: paused at a mark, or stopped at max_steps (not failed, not done by end time / KE)
+  loop_paused = !hs.failed && (hs.paused != 0 || (!hs.done && p.max_steps && hs.steps >= static_cast<long long>(p.max_steps)));
   if (hs.failed) raise_if_failed("run");
 }
 

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "hostio.cuh"
 #include "system.cuh"
 
 namespace tlsph_cuda {
@@ -1099,11 +1100,11 @@ void DevSystem::load_csr(const int64_t* offsets, const int32_t* neighbor, const 
   pf_ref.alloc(S);
   CK(cudaMemcpyAsync(off_ref.p, offsets, (N + 1) * sizeof(long long), cudaMemcpyHostToDevice, stream));
   if (nslots > 0) {
-    CK(cudaMemcpyAsync(nb_ref.p, neighbor, nslots * sizeof(int), cudaMemcpyHostToDevice, stream));
-    CK(cudaMemcpyAsync(ln_ref.p, r0_len_h, nslots * sizeof(double), cudaMemcpyHostToDevice, stream));
-    CK(cudaMemcpyAsync(e0_ref.p, e0_h, nslots * D * sizeof(double), cudaMemcpyHostToDevice, stream));
-    CK(cudaMemcpyAsync(dw_ref.p, dwdr0_h, nslots * sizeof(double), cudaMemcpyHostToDevice, stream));
-    CK(cudaMemcpyAsync(pf_ref.p, pf_h, nslots * sizeof(double), cudaMemcpyHostToDevice, stream));
+    copy_to_device(nb_ref.p, neighbor, nslots * sizeof(int), stream);
+    copy_to_device(ln_ref.p, r0_len_h, nslots * sizeof(double), stream);
+    copy_to_device(e0_ref.p, e0_h, nslots * D * sizeof(double), stream);
+    copy_to_device(dw_ref.p, dwdr0_h, nslots * sizeof(double), stream);
+    copy_to_device(pf_ref.p, pf_h, nslots * sizeof(double), stream);
   }
   cnt.alloc(N);
   offs.alloc(N + 1);
@@ -1196,7 +1197,7 @@ void DevSystem::set_field(int field, const double* host) {
   const size_t N = static_cast<size_t>(n);
   if (field == TLSPH_FIELD_CONSTRAINED) {
     tmp.alloc(N);
-    CK(cudaMemcpyAsync(tmp.p, host, N * sizeof(double), cudaMemcpyHostToDevice, stream));
+    copy_to_device(tmp.p, host, N * sizeof(double), stream);
     k_flag_in<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, n, perm.p, flag.p);
     CK_LAUNCH("k_flag_in");
     refresh_minvf();
@@ -1207,7 +1208,7 @@ void DevSystem::set_field(int field, const double* host) {
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "r0 is fixed at construction (the cell grid is built from it)");
   FieldSpec fs = field_spec(*this, field);
   tmp.alloc(N * fs.comps);
-  CK(cudaMemcpyAsync(tmp.p, host, N * fs.comps * sizeof(double), cudaMemcpyHostToDevice, stream));
+  copy_to_device(tmp.p, host, N * fs.comps * sizeof(double), stream);
   g_h2d_bytes += N * fs.comps * sizeof(double);
   k_aos_to_soa<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, fs.pack());
   CK_LAUNCH("k_aos_to_soa");
@@ -1228,7 +1229,7 @@ void DevSystem::get_field(int field, double* host) const {
     self->tmp.alloc(N);
     k_flag_out<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, n, perm.p, flag.p);
     CK_LAUNCH("k_flag_out");
-    CK(cudaMemcpyAsync(host, tmp.p, N * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    copy_to_host(host, tmp.p, N * sizeof(double), stream);
     sync();
     return;
   }
@@ -1236,14 +1237,17 @@ void DevSystem::get_field(int field, double* host) const {
   self->tmp.alloc(N * fs.comps);
   k_soa_to_aos<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, n, perm.p, fs.pack());
   CK_LAUNCH("k_soa_to_aos");
-  CK(cudaMemcpyAsync(host, tmp.p, N * fs.comps * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  copy_to_host(host, tmp.p, N * fs.comps * sizeof(double), stream);
   sync();
 }
 
 void DevSystem::put_record(int field, const void* host, int layout, bool only_if_changed, int* changed) {
   if (!host && field == TLSPH_FIELD_BODY) {  // no body term (ExternalAccel::body empty)
     if (changed) *changed = has_body ? 1 : 0;
+    if (has_body)  // the kernels always add body[i]: zero it once when the term goes away
+      for (int d = 0; d < D; ++d) CK(cudaMemsetAsync(body[d].p, 0, static_cast<size_t>(n) * sizeof(double), stream));
     has_body = false;
+    sync();
     return;
   }
   if (!host) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "null host array");
@@ -1261,7 +1265,7 @@ void DevSystem::put_record(int field, const void* host, int layout, bool only_if
   if (field == TLSPH_FIELD_CONSTRAINED) {
     tmp.alloc((N + 7) / 8);
     auto* staged = reinterpret_cast<uint8_t*>(tmp.p);
-    CK(cudaMemcpyAsync(staged, host, N, cudaMemcpyHostToDevice, stream));
+    copy_to_device(staged, host, N, stream);
     g_h2d_bytes += N;
     if (only_if_changed) {
       CK(cudaMemsetAsync(differs.p, 0, sizeof(int), stream));
@@ -1281,7 +1285,7 @@ void DevSystem::put_record(int field, const void* host, int layout, bool only_if
   FieldSpec fs = field_spec(*this, field == TLSPH_FIELD_R0 ? TLSPH_FIELD_R0 : field);
   const int cm = layout == 1 && fs.comps == D * D ? D : 0;
   tmp.alloc(N * fs.comps);
-  CK(cudaMemcpyAsync(tmp.p, host, N * fs.comps * sizeof(double), cudaMemcpyHostToDevice, stream));
+  copy_to_device(tmp.p, host, N * fs.comps * sizeof(double), stream);
   g_h2d_bytes += N * fs.comps * sizeof(double);
   if (only_if_changed || field == TLSPH_FIELD_R0) {
     CK(cudaMemsetAsync(differs.p, 0, sizeof(int), stream));
@@ -1315,7 +1319,7 @@ void DevSystem::take_record(int field, void* host, int layout) const {
     auto* staged = reinterpret_cast<uint8_t*>(tmp.p);
     k_flags_out<<<grid_for(n, 256), 256, 0, stream>>>(staged, n, perm.p, flag.p);
     CK_LAUNCH("k_flags_out");
-    CK(cudaMemcpyAsync(host, staged, N, cudaMemcpyDeviceToHost, stream));
+    copy_to_host(host, staged, N, stream);
     g_d2h_bytes += N;
     sync();
     return;
@@ -1325,7 +1329,7 @@ void DevSystem::take_record(int field, void* host, int layout) const {
   self->tmp.alloc(N * fs.comps);
   k_records_out<<<grid_for(n, 256), 256, 0, stream>>>(tmp.p, fs.comps, cm, n, perm.p, fs.pack());
   CK_LAUNCH("k_records_out");
-  CK(cudaMemcpyAsync(host, tmp.p, N * fs.comps * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  copy_to_host(host, tmp.p, N * fs.comps * sizeof(double), stream);
   g_d2h_bytes += N * fs.comps * sizeof(double);
   sync();
 }
@@ -1338,10 +1342,10 @@ void DevSystem::grid_cells(int32_t* cell_of, int64_t* cell_start_h, int32_t* cel
   if (D == 2) k_cell_of<2><<<grid_for(n, 256), 256, 0, stream>>>(f, co.p);
   else k_cell_of<3><<<grid_for(n, 256), 256, 0, stream>>>(f, co.p);
   CK_LAUNCH("k_cell_of");
-  if (cell_of) CK(cudaMemcpyAsync(cell_of, co.p, N * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (cell_of) copy_to_host(cell_of, co.p, N * sizeof(int), stream);
   if (cell_start_h)
     CK(cudaMemcpyAsync(cell_start_h, cell_start.p, (ncells + 1) * sizeof(long long), cudaMemcpyDeviceToHost, stream));
-  if (cell_particles) CK(cudaMemcpyAsync(cell_particles, perm.p, N * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (cell_particles) copy_to_host(cell_particles, perm.p, N * sizeof(int), stream);
   sync();
 }
 
@@ -1373,11 +1377,11 @@ void DevSystem::get_neighborhood(int64_t* offsets, int32_t* neighbor, double* r0
   CK_LAUNCH("k_csr_to_ref");
   if (offsets) CK(cudaMemcpyAsync(offsets, off_ref.p, (N + 1) * sizeof(long long), cudaMemcpyDeviceToHost, stream));
   if (nslots > 0) {
-    if (neighbor) CK(cudaMemcpyAsync(neighbor, nb.p, nslots * sizeof(int), cudaMemcpyDeviceToHost, stream));
-    if (r0_len_h) CK(cudaMemcpyAsync(r0_len_h, ln.p, nslots * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    if (e0_h) CK(cudaMemcpyAsync(e0_h, e.p, nslots * D * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    if (dwdr0_h) CK(cudaMemcpyAsync(dwdr0_h, dw.p, nslots * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    if (pf_h) CK(cudaMemcpyAsync(pf_h, p.p, nslots * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (neighbor) copy_to_host(neighbor, nb.p, nslots * sizeof(int), stream);
+    if (r0_len_h) copy_to_host(r0_len_h, ln.p, nslots * sizeof(double), stream);
+    if (e0_h) copy_to_host(e0_h, e.p, nslots * D * sizeof(double), stream);
+    if (dwdr0_h) copy_to_host(dwdr0_h, dw.p, nslots * sizeof(double), stream);
+    if (pf_h) copy_to_host(pf_h, p.p, nslots * sizeof(double), stream);
   }
   sync();
 }

@@ -511,10 +511,13 @@ class DeviceSystem:
         return out
 
     def run(self, material, *, eta, alpha, scheme="particle_split", steps=0, end_time=0.0, fixed_dt=0.0,
-            elastic=True, seed=0, ke_stop=False, ke_ratio=1e-8):
-        """Device-resident loop of runner.cpp:341-391 (state must be prepared as :306-312 does)."""
+            elastic=True, seed=0, ke_stop=False, ke_ratio=1e-8, resume=False):
+        """Device-resident loop of runner.cpp:341-391 (state must be prepared as :306-312 does).
+        resume=True continues the previous loop (same eta~ stream, t and step count; `steps` is the
+        cumulative cap); the returned times are then cumulative too."""
         p = LoopParams(material, self.h, eta, alpha, SCHEMES[scheme], seed, end_time, steps, fixed_dt,
-                       1 if elastic else 0, 1 if ke_stop else 0, ke_ratio, -1, 0.0, None, 0, 0, 0)
+                       1 if elastic else 0, 1 if ke_stop else 0, ke_ratio, -1, 0.0, None, 0, 0,
+                       1 if resume else 0)
         r = LoopResult()
         _check(lib().tlsph_dev_run(self._h, C.byref(p), C.byref(r)))
         return {"steps": r.steps, "damped": r.damped_steps, "t": r.t, "last_dt": r.last_dt,

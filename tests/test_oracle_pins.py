@@ -658,3 +658,26 @@ def test_box_lattice_counts():  # test_cases.cpp:10-31
         O.box_lattice([0.0, 0.0], [0.1, 0.001], 0.01)
     # same arithmetic as the fixture walk
     assert np.array_equal(O.box_lattice([0.0, 0.0], [0.04, 0.03], 0.01), lattice_r0([4, 3], 0.01))
+
+
+def test_oracle_resumed_run_equals_uninterrupted():
+    """The oracle loop continued across calls (orc_run resume: same RandomSource stream, t, step
+    count) equals one uninterrupted run bit for bit (bench.py times steps W..W+K this way)."""
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg1(scale=4)
+    out = []
+    for split in (None, 7):
+        o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+        o.set_material(S.E_MOD, S.NU, S.RHO0)
+        o.set("v", cfg["v0"])
+        o.set("body", cfg["body"])
+        o.prepare()
+        if split is None:
+            r = o.run(eta=cfg["eta"], alpha=0.5, steps=20, seed=3)
+        else:
+            o.run(eta=cfg["eta"], alpha=0.5, steps=split, seed=3)
+            r = o.run(eta=cfg["eta"], alpha=0.5, steps=20, seed=3, resume=True)
+        out.append((r["steps"], r["damped"], r["t"], o.get("v"), o.get("r")))
+    a, b = out
+    assert a[:3] == b[:3] and a[0] == 20 and a[1] > 0
+    assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
