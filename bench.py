@@ -1,23 +1,32 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 hot path (BASELINE.json metric), one JSON line on rank 0.
 
-Workload (default, the config BASELINE's metric is quoted on that fits one GPU):
-  cfg2 — 3D damping-only sweep, 64^3 = 262,144 particles, fp64, 27-colour
-  particle-split Strang sweep, alpha = 1, fixed dt = 0.6 h / c.
-  One "step" = one full damping sweep (forward + mirrored reverse pass).
-  metric = damping pair-updates per second (DPU/s): 2 * S_free per sweep.
+Headline (N = 1): BASELINE configs[3] (cfg4), the largest configuration that fits one GPU --
+a jittered 1 x 1 x 0.5 m block at dp 0.004 (7,812,500 particles, ~560 M neighbour slots), fp64
+TL-SPH step + random-choice splitting damping (alpha 0.1), stable_dt, per-step current-cell
+rebuild. One step = one iteration of runner.cpp:341-391 over the whole body.
+metric = particle-steps per second (PS/s). The timed window is loop steps W .. W+K-1 (after W
+untimed warm-up steps of the same run); the reference arm times the same window.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3]
+  python bench.py [--gpus N] [--steps K] [--warmup W]
   python bench.py --impl reference ...   # the reference CPU path (oracle port, all host cores)
 
-Multi-GPU (torchrun, one rank per GPU): every rank runs its own cfg2 body for the
-headline `value` (replicas of the 64^3 block, so per-GPU work matches N = 1), timed
-with CUDA events on the library's stream, max over ranks; value = total DPU / max time.
-The line adds `sweep_sharded`: BASELINE cfg5's weak scaling, one x-slab of an
-N x 250-layer body per rank with the fused cross-process exchange (slabs.IpcSlabSweep);
-at N = 1 `sweep_at_scale` times the same per-GPU body undivided.
-Other legs: `particle_steps` (cfg3 full loop, PS/s), `parity` (500 cfg2 sweeps vs the
-oracle), `cpu_baseline` (oracle port on the host cores).
+Keys of the line:
+  value      PS/s from CUDA events on the library's stream around the K steps (inputs resident);
+  e2e        the same metric through the reference's C++ operator API (stable_dt / verlet_step /
+             strang_damping_sweep<3> on a host ParticleSystem<3>, fields moved every call from and
+             into pageable host vectors; lib/tlsph-operator-loop);
+  roofline   the TL-SPH step kernels (k_step_begin + passes A-C + current-cell rebuild) against
+             the measured HBM copy bandwidth on BASELINE.md §4's algorithmic byte model;
+  cpu_baseline / parity   the oracle (reference arithmetic, OpenMP on every host core) over the
+             same W+K steps; its K timed steps are the baseline, its final state the parity check;
+  legs       cfg2 damping sweep (DPU/s, its e2e through strang_damping_sweep<3>, 500-sweep parity),
+             pairwise split sweep on cfg2, cfg1 full run, cfg3 loop, cfg5 weak-scaling share
+             (sweep DPU/s and loop PS/s on one GPU: the N = 1 base of the N > 1 line).
+
+Multi-GPU (torchrun, one rank per GPU): value = BASELINE cfg5's weak-scaling loop, one x-slab of
+an N x 250-layer body (15.6 M particles) per rank with the fused cross-process exchange
+(slabs.IpcSlabSweep / IpcGroup), PS/s over the whole body, device time max over ranks.
 """
 from __future__ import annotations
 
@@ -37,25 +46,26 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 BYTES_SLOT = 12          # neighbor i32 + pair_factor f64
 P_D = {3: 65, 2: 49}     # v r/w + m + flag + offset per free particle per half-pass
 P_S = {3: 1091, 2: 587}  # per particle-step minimal traffic
+OPERATOR_LOOP = os.path.join(ROOT, "paper_2103_08932_b200", "lib", "tlsph-operator-loop")
+
+METRIC_PS = "particle-steps/s (fp64 TL-SPH step + random-choice splitting damping)"
+METRIC_DPU = "damping pair-updates/s (fp64 particle-split Strang sweep)"
 
 
-def load_traffic():
-    """DRAM bytes per launch of the sweep phase from the committed ncu --set full capture (profiles/)."""
+# ----------------------------------------------------------------------------- plumbing
+def load_json(rel):
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return float(json.load(fh)["dram_bytes_per_launch"])
+        with open(os.path.join(ROOT, rel)) as fh:
+            return json.load(fh)
     except Exception:
         return None
 
 
 def load_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    try:
-        with open(path) as fh:
-            pk = json.load(fh)
+    pk = load_json("MEASURED_PEAKS.json")
+    if pk and "hbm_gbs" in pk:
         return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        return PEAKS_FALLBACK["hbm_gbs"], "fallback (B200_PROFILING.md 6.65 TB/s)"
+    return PEAKS_FALLBACK["hbm_gbs"], "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 class ClockSampler:
@@ -129,10 +139,8 @@ class ClockSampler:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
 
 
 def barrier_and_max(value, ws):
@@ -160,7 +168,18 @@ def cuda_sync():
         pass
 
 
-# ----------------------------------------------------------------------------- cfg2 (headline)
+def cpu_threads():
+    from oracle import oracle as O  # the checker / CPU baseline only
+    return min(os.cpu_count() or 1, O.openmp_threads())
+
+
+def rel_l2(a, b):
+    import numpy as np
+    a, b = np.asarray(a, dtype=np.float64).ravel(), np.asarray(b, dtype=np.float64).ravel()
+    den = float(np.linalg.norm(b))
+    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
 def free_slots(off, cons):
     if cons is None:
         return int(off[-1]), len(off) - 1
@@ -169,400 +188,446 @@ def free_slots(off, cons):
     return int(counts[free].sum()), int(free.sum())
 
 
-def cpu_sweep_sample(cfg, threads, budget_s, min_sweeps=1):
-    """Times full oracle sweeps (the reference CPU path, OpenMP over same-colour cells) within a budget."""
-    from oracle import oracle as O
-    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
-    o.set("v", cfg["v0"])
-    eta_t = cfg["eta"] / cfg["alpha"]
-    o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)  # warm
-    times = []
-    t_start = time.perf_counter()
-    while len(times) < min_sweeps or (time.perf_counter() - t_start) < budget_s:
-        t0 = time.perf_counter()
-        o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)
-        times.append(time.perf_counter() - t0)
-        if len(times) >= 1000:
-            break
-    return times, o
+def step_bytes(n, slots):
+    """algorithmic bytes of one elastic step (3D): S*2*(4+8+24) + N*P_s."""
+    return slots * 2 * (4 + 8 + 8 * 3) + n * P_S[3]
 
 
-def run_cfg2(args, ws, rank):
-    from paper_2103_08932_b200 import dev
-    from paper_2103_08932_b200 import scenarios as S
-    cfg = S.cfg2()
-    d = S.build_device(cfg, prepare=False)
-    offsets = d.row_offsets()
-    s_free, n_free = free_slots(offsets, cfg["constrained"])
-    dpu_per_sweep = 2 * s_free
-    b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_free)
-    eta_t = cfg["eta"] / cfg["alpha"]
-    dt = cfg["fixed_dt"]
-    # warmup
-    for _ in range(args.warmup):
-        d.damping_sweep("particle_split", eta_t, dt)
-    barrier(ws)
-    cuda_sync()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        elapsed = d.damping_sweep("particle_split", eta_t, dt, count=args.steps)  # CUDA events on the stream
-    cuda_sync()
-    barrier(ws)
-    t_max = barrier_and_max(elapsed, ws)
-    value = dpu_per_sweep * args.steps * ws / t_max
-    phase_launches = 54
-    avg_launch = elapsed / (args.steps * phase_launches)
-    achieved = (b_sweep / phase_launches) / avg_launch / 1e9
-    peak, peak_src = load_peaks()
+def sweep_bytes(s_free, n_free, dim=3):
+    return 2 * (BYTES_SLOT * s_free + P_D[dim] * n_free)
 
-    # e2e through the C ABI with host buffers: v host->device, sweep, v device->host, every step,
-    # from / into pinned host memory
+
+def operator_loop(what, steps, warmup):
+    """The e2e legs: lib/tlsph-operator-loop (C++ against include/tlsph/*.hpp only)."""
+    out = subprocess.run([OPERATOR_LOOP, what, str(steps), str(warmup), "fast"], capture_output=True, text=True,
+                         timeout=1200)
+    if out.returncode != 0:
+        raise RuntimeError(f"tlsph-operator-loop {what} failed: {out.stderr.strip()[-400:]}")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+# ----------------------------------------------------------------------------- shared config (both arms)
+CFG4_WORKLOAD = ("cfg4: jittered 1 x 1 x 0.5 m block, dp 0.004 (250 x 250 x 125 lattice, +-0.4 dp jitter "
+                 "from RandomSource(3)), fp64 neo-Hookean TL-SPH + random-choice particle-split damping "
+                 "(alpha 0.1, seed 0), gravity, 5-layer clamp, stable_dt (CFL 0.6)")
+
+
+def cfg4_config(n, slots, steps, warmup):
+    return {"workload": CFG4_WORKLOAD, "particles": int(n), "slots": int(slots),
+            "window": f"loop steps {warmup}..{warmup + steps - 1} of one run (after {warmup} warm-up steps)",
+            "l2": "inputs larger than L2 (neighbour CSR ~30 GB, state ~3 GB vs 126 MB L2); no flush"}
+
+
+# ----------------------------------------------------------------------------- headline, ours (N = 1)
+def headline_cfg4(args):
     import numpy as np
-    import torch
-    v_in = torch.empty(cfg["v0"].shape, dtype=torch.float64, pin_memory=True).numpy()
-    v_out = torch.empty(cfg["v0"].shape, dtype=torch.float64, pin_memory=True).numpy()
-    v_in[...] = cfg["v0"]
-    h2d = d2h = v_in.nbytes
-    d.set("v", v_in)
-    d.damping_sweep("particle_split", eta_t, dt)
-    d.get("v", out=v_out)
-    barrier(ws)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        d.set("v", v_in)
-        d.damping_sweep("particle_split", eta_t, dt)
-        d.get("v", out=v_out)
-    t_e2e = barrier_and_max(time.perf_counter() - t0, ws)
-    e2e = dpu_per_sweep * args.steps * ws / t_e2e
 
-    out = {
-        "metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
-        "value": value,
-        "unit": "DPU/s",
-        "n_gpus": ws,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": t_max / args.steps * 1e3,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (seeded 64^3 lattice, v ~ N(0,1) Box-Muller from RandomSource(1))",
-        "config": {"workload": "cfg2: 3D damping-only sweep, 64^3 lattice, 27-colour particle-split, alpha=1",
-                   "particles": int(d.n), "slots": int(offsets[-1]), "dpu_per_step": dpu_per_sweep,
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (CSR 200 MB + 20 MB state > 126 MB L2); no flush",
-                   "reduction": "fast (warp-shuffle)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": load_traffic(), "kernel": "k_sweep_fast (one colour phase)",
-                     "bytes_per_launch": b_sweep / phase_launches, "avg_launch_s": avg_launch,
-                     "peak_source": peak_src},
-        "e2e": {"value": e2e, "unit": "DPU/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "tlsph_dev_set_field(V) + tlsph_dev_damping_sweep + tlsph_dev_get_field(V), host buffers"},
-        "gpu_launches": phase_launches * args.steps,
-        "clocks": clk.summary(),
-    }
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        from oracle import oracle as O
-        threads = min(threads, O.openmp_threads())
-        times, _ = cpu_sweep_sample(cfg, threads, budget_s=args.cpu_budget)
-        t_cpu = statistics.median(times)
-        times1, _ = cpu_sweep_sample(cfg, 1, budget_s=min(args.cpu_budget, 5.0))
-        out["cpu_baseline"] = {"value": dpu_per_sweep / t_cpu, "unit": "DPU/s", "cores": threads, "kind": "port",
-                               "sample": f"{len(times)} full cfg2 sweeps (median), oracle OpenMP over same-colour cells",
-                               "value_1_thread": dpu_per_sweep / statistics.median(times1),
-                               "sample_1_thread": f"{len(times1)} full cfg2 sweeps (median), 1 thread"}
-        if args.parity_sweeps > 0:
-            out["parity"] = cfg2_parity(cfg, d, args.parity_sweeps, threads)
-    return out
-
-
-def cfg2_parity(cfg, d, sweeps, threads):
-    """BASELINE cfg2's check: velocity-variance decay over `sweeps` sweeps from v0, GPU (FAST) against
-    the oracle (reference arithmetic), plus the relative L2 distance of the final velocity fields."""
-    import numpy as np
-    from oracle import oracle as O
-    eta_t, dt = cfg["eta"] / cfg["alpha"], cfg["fixed_dt"]
-    d.set("v", cfg["v0"])
-    d.damping_sweep("particle_split", eta_t, dt, count=sweeps)
-    vg = d.get("v")
-    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
-    o.set("v", cfg["v0"])
-    for _ in range(sweeps):
-        o.damping_sweep("particle_split", eta_t, dt, threads=threads)
-    vo = o.get("v")
-    var0 = float(np.var(cfg["v0"]))
-    return {"sweeps": sweeps, "var_v0": var0, "var_gpu": float(np.var(vg)), "var_oracle": float(np.var(vo)),
-            "rel_l2_v": float(np.linalg.norm(vg - vo) / np.linalg.norm(vo)), "tolerance": 1e-10,
-            "mode": "fast (warp-shuffle reductions) vs oracle"}
-
-
-def particle_steps(args, ws, rank):
-    """Second half of BASELINE.json's metric: particle-steps/s of the full device-resident loop
-    (TL-SPH step + random-choice splitting damping, runner.cpp:341-391) on cfg3, the 3D cantilever
-    beam (640,000 particles), FAST reductions; the reference CPU path (oracle port, OpenMP) timed on
-    a bounded sample of the same loop."""
     from paper_2103_08932_b200 import scenarios as S
-    cfg = S.cfg3()
-    steps = max(50, min(args.ps_steps, 2000))
+    cfg = S.cfg4()
+    mat = S.material()
     d = S.build_device(cfg, prepare=True)
     d.set_reduction("fast")
-    r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=steps, seed=cfg["seed"])
-    t_max = barrier_and_max(r["total_s"], ws)
-    n = int(d.n)
-    slots = int(d.slot_count)
-    # BASELINE.md §4: B_step = S*2*(4+8+8D) + N*P_s (+ B_sweep on damped steps), P_s = 1,091 B (3D)
-    b_elastic = slots * 2 * (4 + 8 + 8 * 3) + n * 1091
-    t_el = r["elastic_s"] / max(r["steps"], 1)
+    d.set_resort(True)
+    n, slots = int(d.n), int(d.slot_count)
+    W, K = args.warmup, args.steps
+    kw = dict(eta=cfg["eta"], alpha=cfg["alpha"], seed=cfg["seed"])
+    w = d.run(mat, steps=W, **kw) if W > 0 else None
+    cuda_sync()
+    with ClockSampler(0) as clk:
+        r = d.run(mat, steps=W + K, resume=W > 0, **kw)
+    cuda_sync()
+    base = w or {"total_s": 0.0, "elastic_s": 0.0, "damping_s": 0.0, "damped": 0}  # times are cumulative
+    t = r["total_s"] - base["total_s"]
+    t_el = (r["elastic_s"] - base["elastic_s"]) / K
+    damped = r["damped"] - base["damped"]
+    t_dm = (r["damping_s"] - base["damping_s"]) / max(damped, 1)
+    assert r["steps"] == W + K
+    final = {"v": d.get("v"), "u": d.get("r") - cfg["r0"], "steps": r["steps"], "damped": r["damped"], "t": r["t"]}
     peak, peak_src = load_peaks()
-    out = {"metric": "particle-steps/s (fp64 TL-SPH step + splitting damping, random choice)",
-           "value": n * r["steps"] * ws / t_max, "unit": "PS/s", "steps": r["steps"], "damped_steps": r["damped"],
-           "ms_per_step": t_max / max(r["steps"], 1) * 1e3, "elastic_ms_per_step": t_el * 1e3,
-           "damping_ms_per_damped_step": r["damping_s"] / max(r["damped"], 1) * 1e3,
-           "config": {"workload": "cfg3: 3D cantilever beam 400x40x40, neo-Hookean, gravity, 5-layer clamp, "
-                                  "alpha=0.2", "particles": n, "slots": slots, "reduction": "fast"},
-           "roofline": {"bound": "hbm", "kernel": "TL-SPH step (passes A-C + step-begin reduction)",
-                        "achieved": b_elastic / t_el / 1e9, "peak": peak, "unit": "GB/s",
-                        "frac": b_elastic / t_el / 1e9 / peak, "bytes_per_step": b_elastic, "peak_source": peak_src}}
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        from oracle import oracle as O
-        out["cpu_baseline"] = cfg3_oracle_steps(min(os.cpu_count() or 1, O.openmp_threads()), 10)
-    return out
-
-
-def sweep_at_scale(args, ws, rank):
-    """The damping sweep on a large body: BASELINE cfg5's weak-scaling share of one GPU (250 x 250 x 250
-    lattice, 15.6 M particles, 1.24 G slots, dp 0.004, 5-layer clamp), where the colours hold ~10^4
-    cells and the streamed FAST kernel (slot block from L2) runs; DPU/s against the HBM roofline on the
-    same algorithmic byte model as the headline, with the DRAM bytes per launch of the committed ncu
-    capture (profiles/traffic_scale.json)."""
-    from paper_2103_08932_b200 import scenarios as S
-    cfg = S.cfg5_weak()
-    d = S.build_device(cfg, prepare=False)
-    d.set_reduction("fast")
-    offsets = d.row_offsets()
-    s_free, n_free = free_slots(offsets, cfg["constrained"])
-    b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_free)
-    eta_t, dt = cfg["eta"] / cfg["alpha"], 1e-5
-    d.damping_sweep("particle_split", eta_t, dt, count=2)
-    sweeps = max(3, min(args.scale_sweeps, 50))
-    elapsed = d.damping_sweep("particle_split", eta_t, dt, count=sweeps)
-    t_max = barrier_and_max(elapsed, ws)
-    t_sweep = t_max / sweeps
-    peak, peak_src = load_peaks()
-    achieved = b_sweep / t_sweep / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic_scale.json")) as fh:
-            traffic = json.load(fh)
-    except Exception:
-        pass
-    del d
-    return {"metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
-            "value": 2 * s_free * sweeps * ws / t_max, "unit": "DPU/s", "sweeps": sweeps,
-            "ms_per_sweep": t_sweep * 1e3,
-            "config": {"workload": "cfg5 weak-scaling share of one GPU: 250^3 lattice dp 0.004, 5-layer clamp",
-                       "particles": len(cfg["r0"]), "slots": int(offsets[-1]), "reduction": "fast",
-                       "sweep_tiling": "auto (streamed: colours of ~9,700 cells)"},
-            "roofline": {"bound": "hbm", "kernel": "k_sweep_fast<streamed> (one colour phase)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "bytes_per_launch": b_sweep / 54, "avg_launch_s": t_sweep / 54,
-                         "traffic": traffic, "peak_source": peak_src}}
-
-
-def sweep_sharded(args, ws, rank):
-    """N > 1: BASELINE cfg5's weak-scaling run. A body of ws x `--scale-layers` x-layers of 250 x 250
-    (dp 0.004; 15.6 M particles per GPU at the default 250) is x-slab decomposed, one slab per rank,
-    with the fused exchange across processes (slabs.IpcSlabSweep: CUDA IPC mappings of the
-    neighbours' velocity arrays, phase kernels storing shared columns into them over NVLink, the
-    per-phase barrier as stream waits on the neighbours' IPC phase events). Device time per rank
-    (events on the slab's stream), max over ranks; DPU over the whole body. Compare with
-    `sweep_at_scale` of the N = 1 line for the weak-scaling efficiency of the decomposed sweep."""
-    import numpy as np
-    import torch.distributed as dist
-
-    from paper_2103_08932_b200 import scenarios as S
-    from paper_2103_08932_b200 import slabs
-
-    from paper_2103_08932_b200 import dev
-
-    layers, dp = args.scale_layers, 0.004
-    h = 1.3 * dp
-    # this rank's held particles only (slabs.lattice_slab == decompose on the whole lattice)
-    grid, ranges, part, r0 = slabs.lattice_slab([0.0, 0.0, 0.0], [layers * ws * dp, 1.0, 1.0], dp, h, ws, rank)
-    parts = [slabs.Slab(r, x0, x1, None) for r, (x0, x1) in enumerate(ranges)]
-    cons_local = (r0[:, 0] < 5 * dp).astype(np.uint8)
-    d = dev.DeviceSystem(r0, dp ** 3, S.RHO0, h, cons_local, grid=grid[:2])
-    d.set_task_range(part.x0, part.x1)
-    cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
-    own = (cols >= part.x0) & (cols < part.x1)
-    del r0
-    d.set_reduction("fast")
+    b_el = step_bytes(n, slots)
     off = d.row_offsets()
-    rows = off[1:] - off[:-1]
-    s_free_local = int(rows[own & (cons_local == 0)].sum())
-    gloo = dist.new_group(backend="gloo")
-    sweep = slabs.IpcSlabSweep(d, rank, ws, group=gloo)
-    eta_t, dt = S.eta_for(h), 1e-5
-    sweep.sweep("particle_split", eta_t, dt, count=2)
-    sweeps = max(3, min(args.scale_sweeps, 50))
-    dist.barrier(group=gloo)
-    d.timer_start()
-    sweep.sweep("particle_split", eta_t, dt, count=sweeps)
-    t = d.timer_stop()
-    t_max = barrier_and_max(t, ws)
-    tot = [None] * ws
-    dist.all_gather_object(tot, (s_free_local, int(own.sum())), group=gloo)
-    s_free = sum(x[0] for x in tot)
-    n_owned = sum(x[1] for x in tot)
-    # the full loop over the slabs (cfg5: TL-SPH step + random-choice damping, alpha 0.2): halo
-    # pushes and sweeps through the IPC links, dt from an all-reduce of the step scalars
-    loop = None
-    if args.scale_steps > 0:
-        mat = S.material()
-        g = np.zeros((d.n, 3))
-        g[:, 1] = -S.GRAVITY
-        d.set("body", g)
-        d.prepare(mat)
-        group = slabs.IpcGroup(slabs.DeviceSlabEngine(d, 3), [(p.x0, p.x1) for p in parts], rank, sweep)
-        spec = slabs.LoopSpec(mat, h, S.eta_for(h), 0.2, args.scale_steps, seed=0)
-        dist.barrier(group=gloo)
-        d.timer_start()
-        res = slabs.run_loop(group, spec, 3, sweeper=lambda scheme, et, dt_: sweep.sweep(scheme, et, dt_))
-        t_loop = barrier_and_max(d.timer_stop(), ws)
-        loop = {"metric": "particle-steps/s (fp64 TL-SPH step + splitting damping, random choice)",
-                "value": n_owned * res["steps"] / t_loop, "unit": "PS/s", "steps": res["steps"],
-                "damped_steps": res["damped"], "ms_per_step": t_loop / res["steps"] * 1e3,
-                "exchange": "halo pushes and sweeps through CUDA IPC; dt from an all-reduce per step"}
-    sweep.close()
+    s_free, n_free = free_slots(off, cfg["constrained"])
+    b_sw = sweep_bytes(s_free, n_free)
+    traffic = load_json("profiles/traffic_cfg4.json")
+    out = {
+        "metric": METRIC_PS,
+        "value": n * K / t, "unit": "PS/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": t / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded jittered lattice, BASELINE.md §3)",
+        "config": cfg4_config(n, slots, K, W),
+        "mode": {"reduction": "fast (lane-parallel sums; <= 1e-10 of the reference order)",
+                 "resort": "current-cell list rebuilt every step inside the loop's graph"},
+        "damped_steps": damped, "elastic_ms_per_step": t_el * 1e3, "damping_ms_per_damped_step": t_dm * 1e3,
+        "roofline": {"bound": "hbm", "kernel": "TL-SPH step: k_step_begin + passes A, B, C (+ current-cell rebuild)",
+                     "achieved": b_el / t_el / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": b_el / t_el / 1e9 / peak, "bytes_per_launch": b_el, "avg_launch_s": t_el,
+                     "traffic": traffic.get("dram_bytes_per_step") if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None, "peak_source": peak_src,
+                     "timing": "CUDA events on the library's stream around each step's kernels, timed steps only"},
+        "roofline_damping": {"bound": "hbm", "kernel": "k_sweep_folds + 54 colour phases (k_sweep_fast, streamed)",
+                             "achieved": b_sw / t_dm / 1e9, "peak": peak, "unit": "GB/s",
+                             "frac": b_sw / t_dm / 1e9 / peak, "bytes_per_sweep": b_sw},
+        "gpu_launches": r["kernel_launches"],  # this call's launches (the timed K steps)
+        "clocks": clk.summary(),
+    }
     del d
-    peak, peak_src = load_peaks()
-    b_sweep = 2 * (BYTES_SLOT * s_free + P_D[3] * n_owned)  # whole body; per GPU divide by ws
-    return {"metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
-            "value": 2 * s_free * sweeps / t_max, "unit": "DPU/s", "sweeps": sweeps, "ms_per_sweep": t_max / sweeps * 1e3,
-            "scaling": "weak",
-            "config": {"workload": f"cfg5 weak scaling: {layers * ws} x 250 x 250 lattice (dp 0.004), "
-                                   f"{ws} x-slabs, one per GPU", "particles": n_owned, "slots_free": s_free,
-                       "exchange": "fused: CUDA IPC peer stores of shared columns + IPC phase events (no host sync)"},
-            "roofline": {"bound": "hbm", "achieved_per_gpu": b_sweep / ws / (t_max / sweeps) / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": b_sweep / ws / (t_max / sweeps) / 1e9 / peak,
-                         "peak_source": peak_src},
-            "timing": "CUDA events on each slab's stream between a barrier and the last phase, max over ranks",
-            "loop": loop}
+    return out, cfg, final
 
 
-def cfg3_oracle_steps(threads, steps):
-    """Reference CPU path (oracle port, OpenMP) over the first `steps` cfg3 loop steps."""
+def oracle_loop(cfg, W, K, threads):
+    """The reference CPU path (oracle port of runner.cpp:341-391) on a scenario: W warm-up steps,
+    then K timed steps of the same run."""
     from oracle import oracle as O
     from paper_2103_08932_b200 import scenarios as S
-    cfg = S.cfg3()
+    t0 = time.perf_counter()
     o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
     o.set_material(S.E_MOD, S.NU, S.RHO0)
     o.set("v", cfg["v0"])
     o.set("body", cfg["body"])
     o.prepare(threads=threads)
-    ro = o.run(eta=cfg["eta"], alpha=cfg["alpha"], steps=steps, seed=cfg["seed"], threads=threads)
-    n = len(cfg["r0"])
-    return {"value": n * ro["steps"] / ro["total_s"], "unit": "PS/s", "cores": threads, "kind": "port",
-            "sample": f"first {ro['steps']} cfg3 loop steps, oracle OpenMP"}
+    init_s = time.perf_counter() - t0
+    kw = dict(eta=cfg["eta"], alpha=cfg["alpha"], seed=cfg["seed"], threads=threads)
+    if W > 0:
+        o.run(steps=W, **kw)
+    r = o.run(steps=W + K, resume=W > 0, **kw)
+    return o, r, init_s
 
 
-def reference_particle_steps():
+# ----------------------------------------------------------------------------- legs (N = 1)
+def leg_cfg2(args):
+    """cfg2: 64^3 damping-only sweep, DPU/s; e2e through tlsph::strang_damping_sweep<3>; parity."""
+    import numpy as np
+
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg2()
+    d = S.build_device(cfg, prepare=False)
+    d.set_reduction("fast")
+    off = d.row_offsets()
+    s_free, n_free = free_slots(off, cfg["constrained"])
+    eta_t, dt = cfg["eta"] / cfg["alpha"], cfg["fixed_dt"]
+    sweeps = max(20, args.steps)
+    d.damping_sweep("particle_split", eta_t, dt, count=3)
+    el = d.damping_sweep("particle_split", eta_t, dt, count=sweeps)
+    peak, _ = load_peaks()
+    b = sweep_bytes(s_free, n_free)
+    out = {"metric": METRIC_DPU, "value": 2 * s_free * sweeps / el, "unit": "DPU/s", "sweeps": sweeps,
+           "ms_per_sweep": el / sweeps * 1e3,
+           "config": {"workload": "cfg2: 64^3 lattice, v ~ N(0,1) (seed 1), particle-split, alpha 1, dt 0.6 h / c",
+                      "particles": int(d.n), "slots": int(off[-1])},
+           "roofline": {"bound": "hbm", "kernel": "k_sweep_fast (staged) x 54 + k_sweep_folds",
+                        "achieved": b / (el / sweeps) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": b / (el / sweeps) / 1e9 / peak, "bytes_per_sweep": b,
+                        "traffic": (load_json("profiles/traffic.json") or {}).get("dram_bytes_per_launch"),
+                        "note": "latency-bound by construction: 27-particle Gauss-Seidel chains, ~580 cells per colour"}}
+    pw = d.damping_sweep("pairwise_split", eta_t, dt, count=max(5, sweeps // 4))
+    npw = max(5, sweeps // 4)
+    out["pairwise_split"] = {"value": 2 * s_free * npw / pw, "unit": "DPU/s", "ms_per_sweep": pw / npw * 1e3,
+                             "roofline_frac": b / (pw / npw) / 1e9 / peak,
+                             "kernel": "k_pair_factors + k_sweep_pairwise (FAST: affine warp scans)"}
+    if args.parity_sweeps > 0 and not args.no_cpu:
+        from oracle import oracle as O
+        threads = cpu_threads()
+        d.set("v", cfg["v0"])
+        d.damping_sweep("particle_split", eta_t, dt, count=args.parity_sweeps)
+        vg = d.get("v")
+        o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+        o.set("v", cfg["v0"])
+        times = []
+        for _ in range(args.parity_sweeps):
+            t0 = time.perf_counter()
+            o.damping_sweep("particle_split", eta_t, dt, threads=threads)
+            times.append(time.perf_counter() - t0)
+        vo = o.get("v")
+        out["parity"] = {"sweeps": args.parity_sweeps, "var_v0": float(np.var(cfg["v0"])),
+                         "var_gpu": float(np.var(vg)), "var_oracle": float(np.var(vo)),
+                         "rel_l2_v": rel_l2(vg, vo), "tolerance": 1e-10, "mode": "fast vs oracle"}
+        out["cpu_baseline"] = {"value": 2 * s_free / statistics.median(times), "unit": "DPU/s", "cores": threads,
+                               "kind": "port", "sample": f"{len(times)} full cfg2 sweeps (median)"}
+    del d
+    try:
+        e = operator_loop("sweep", max(50, args.steps), 3)
+        out["e2e"] = {"value": e["value"], "unit": "DPU/s", "h2d_bytes_per_step": e["h2d_bytes_per_step"],
+                      "d2h_bytes_per_step": e["d2h_bytes_per_step"], "path": e["api"], "steps": e["steps"]}
+    except Exception as exc:  # reported, never silently replaced
+        out["e2e"] = {"error": str(exc)}
+    return out
+
+
+def leg_cfg1(args):
+    """cfg1 in full: 2D plate, 16,000 particles, 2,000 steps (latency-bound; reported, not the headline)."""
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg1()
+    d = S.build_device(cfg, prepare=True)
+    d.set_reduction("fast")
+    r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=cfg["steps"], seed=cfg["seed"])
+    n = int(d.n)
+    return {"metric": METRIC_PS, "value": n * r["steps"] / r["total_s"], "unit": "PS/s", "steps": r["steps"],
+            "damped_steps": r["damped"], "ms_total": r["total_s"] * 1e3,
+            "config": {"workload": "cfg1: 2D plate 400 x 40, neo-Hookean, gravity, 4-column clamp, alpha 0.2",
+                       "particles": n, "slots": int(d.slot_count)}}
+
+
+def leg_cfg3(args):
+    """cfg3: 3D beam (640,000 particles), 300 loop steps; CPU sample of the same loop."""
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg3()
+    d = S.build_device(cfg, prepare=True)
+    d.set_reduction("fast")
+    steps = 300
+    r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=steps, seed=cfg["seed"])
+    n, slots = int(d.n), int(d.slot_count)
+    t_el = r["elastic_s"] / r["steps"]
+    peak, _ = load_peaks()
+    out = {"metric": METRIC_PS, "value": n * r["steps"] / r["total_s"], "unit": "PS/s", "steps": r["steps"],
+           "damped_steps": r["damped"], "ms_per_step": r["total_s"] / r["steps"] * 1e3,
+           "elastic_ms_per_step": t_el * 1e3, "damping_ms_per_damped_step": r["damping_s"] / max(r["damped"], 1) * 1e3,
+           "config": {"workload": "cfg3: 3D cantilever beam 400 x 40 x 40, neo-Hookean, gravity, 5-layer clamp, "
+                                  "alpha 0.2", "particles": n, "slots": slots},
+           "roofline": {"bound": "hbm", "kernel": "TL-SPH step: k_step_begin + passes A, B, C",
+                        "achieved": step_bytes(n, slots) / t_el / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": step_bytes(n, slots) / t_el / 1e9 / peak}}
+    del d
+    if not args.no_cpu:
+        threads = cpu_threads()
+        o, ro, _ = oracle_loop(cfg, 0, 10, threads)
+        out["cpu_baseline"] = {"value": n * ro["steps"] / ro["total_s"], "unit": "PS/s", "cores": threads,
+                               "kind": "port", "sample": "first 10 cfg3 loop steps"}
+    return out
+
+
+def leg_cfg5_weak(args):
+    """cfg5's weak-scaling share of one GPU (250^3 lattice, 15.6 M particles, 1.24 G slots): the
+    damping sweep (DPU/s) and the full loop (PS/s, alpha 0.2) -- the N = 1 base of the N > 1 line."""
+    from paper_2103_08932_b200 import scenarios as S
+    cfg = S.cfg5_weak()
+    d = S.build_device(cfg, prepare=True)
+    d.set_reduction("fast")
+    off = d.row_offsets()
+    s_free, n_free = free_slots(off, cfg["constrained"])
+    n, slots = int(d.n), int(off[-1])
+    peak, _ = load_peaks()
+    eta_t, dt = cfg["eta"] / cfg["alpha"], 1e-5
+    d.damping_sweep("particle_split", eta_t, dt, count=2)
+    sweeps = max(3, min(args.scale_sweeps, 50))
+    el = d.damping_sweep("particle_split", eta_t, dt, count=sweeps)
+    b = sweep_bytes(s_free, n_free)
+    out = {"sweep": {"metric": METRIC_DPU, "value": 2 * s_free * sweeps / el, "unit": "DPU/s", "sweeps": sweeps,
+                     "ms_per_sweep": el / sweeps * 1e3,
+                     "roofline": {"bound": "hbm", "kernel": "k_sweep_fast (streamed) x 54 + k_sweep_folds",
+                                  "achieved": b / (el / sweeps) / 1e9, "peak": peak, "unit": "GB/s",
+                                  "frac": b / (el / sweeps) / 1e9 / peak, "bytes_per_sweep": b,
+                                  "traffic": load_json("profiles/traffic_scale.json")}},
+           "config": {"workload": "cfg5 weak-scaling share of one GPU: 250^3 lattice dp 0.004, 5-layer clamp, "
+                                  "gravity, alpha 0.2", "particles": n, "slots": slots}}
+    d.set("v", cfg["v0"])
+    steps = max(5, args.scale_steps)
+    r = d.run(S.material(), eta=cfg["eta"], alpha=cfg["alpha"], steps=steps, seed=cfg["seed"])
+    t_el = r["elastic_s"] / r["steps"]
+    out["loop"] = {"metric": METRIC_PS, "value": n * r["steps"] / r["total_s"], "unit": "PS/s", "steps": r["steps"],
+                   "damped_steps": r["damped"], "ms_per_step": r["total_s"] / r["steps"] * 1e3,
+                   "roofline": {"bound": "hbm", "kernel": "TL-SPH step: k_step_begin + passes A, B, C",
+                                "achieved": step_bytes(n, slots) / t_el / 1e9, "peak": peak, "unit": "GB/s",
+                                "frac": step_bytes(n, slots) / t_el / 1e9 / peak}}
+    del d
+    return out
+
+
+# ----------------------------------------------------------------------------- N > 1
+def sharded_cfg5(args, ws, rank):
+    """BASELINE cfg5's weak scaling: a body of ws x `--scale-layers` x-layers of 250 x 250 (dp 0.004;
+    15.6 M particles per GPU at 250), x-slab decomposed, one slab per rank, fused cross-process
+    exchange (CUDA IPC peer stores + IPC events); loop PS/s and sweep DPU/s over the whole body,
+    device time per rank (events on the slab's stream), max over ranks."""
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2103_08932_b200 import dev
+    from paper_2103_08932_b200 import scenarios as S
+    from paper_2103_08932_b200 import slabs
+
+    layers, dp = args.scale_layers, 0.004
+    h = 1.3 * dp
+    grid, ranges, part, r0 = slabs.lattice_slab([0.0, 0.0, 0.0], [layers * ws * dp, 1.0, 1.0], dp, h, ws, rank)
+    parts = [slabs.Slab(r, x0, x1, None) for r, (x0, x1) in enumerate(ranges)]
+    cons = (r0[:, 0] < 5 * dp).astype(np.uint8)
+    d = dev.DeviceSystem(r0, dp ** 3, S.RHO0, h, cons, grid=grid[:2])
+    d.set_task_range(part.x0, part.x1)
+    cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
+    own = (cols >= part.x0) & (cols < part.x1)
+    d.set_reduction("fast")
+    off = d.row_offsets()
+    rows = off[1:] - off[:-1]
+    s_free_local = int(rows[own & (cons == 0)].sum())
+    slots_local = int(rows[own].sum())
+    gloo = dist.new_group(backend="gloo")
+    sweep = slabs.IpcSlabSweep(d, rank, ws, group=gloo)
+    mat = S.material()
+    g = np.zeros((d.n, 3))
+    g[:, 1] = -S.GRAVITY
+    d.set("body", g)
+    d.prepare(mat)
+    group = slabs.IpcGroup(slabs.DeviceSlabEngine(d, 3), [(p.x0, p.x1) for p in parts], rank, sweep)
+    W, K = args.warmup, args.steps
+    spec_w = slabs.LoopSpec(mat, h, S.eta_for(h), 0.2, W, seed=0)
+    if W > 0:
+        slabs.run_loop(group, spec_w, 3, sweeper=lambda scheme, et, dt_: sweep.sweep(scheme, et, dt_))
+    dist.barrier(group=gloo)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        d.timer_start()
+        spec = slabs.LoopSpec(mat, h, S.eta_for(h), 0.2, K, seed=0)
+        res = slabs.run_loop(group, spec, 3, sweeper=lambda scheme, et, dt_: sweep.sweep(scheme, et, dt_))
+        t_loop = barrier_and_max(d.timer_stop(), ws)
+    tot = [None] * ws
+    dist.all_gather_object(tot, (s_free_local, int(own.sum()), slots_local), group=gloo)
+    n_owned = sum(x[1] for x in tot)
+    slots = sum(x[2] for x in tot)
+    eta_t, dt = S.eta_for(h) / 0.2, 1e-5
+    dist.barrier(group=gloo)
+    d.timer_start()
+    sweep.sweep("particle_split", eta_t, dt, count=max(3, min(args.scale_sweeps, 50)))
+    t_sw = barrier_and_max(d.timer_stop(), ws)
+    sweep.close()
+    peak, peak_src = load_peaks()
+    s_free = sum(x[0] for x in tot)
+    nsw = max(3, min(args.scale_sweeps, 50))
+    b_step = step_bytes(n_owned, slots) / ws
+    return {"metric": METRIC_PS, "value": n_owned * res["steps"] / t_loop, "unit": "PS/s", "n_gpus": ws,
+            "steps": K, "warmup": W, "ms_per_step": t_loop / K * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded lattice, BASELINE.md §3)",
+            "config": {"workload": f"cfg5 weak scaling: {layers * ws} x 250 x 250 lattice (dp 0.004), {ws} x-slabs, "
+                                   "one per GPU, alpha 0.2", "particles": n_owned, "slots": slots,
+                       "parallelism": f"x-slabs x{ws}",
+                       "exchange": "fused: CUDA IPC peer stores of shared columns + IPC phase events"},
+            "roofline": {"bound": "hbm", "kernel": "whole step per GPU (elastic + damping share)",
+                         "achieved": b_step / (t_loop / K) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": b_step / (t_loop / K) / 1e9 / peak, "peak_source": peak_src},
+            "damped_steps": res["damped"],
+            "sweep": {"metric": METRIC_DPU, "value": 2 * s_free * nsw / t_sw, "unit": "DPU/s",
+                      "ms_per_sweep": t_sw / nsw * 1e3},
+            "gpu_launches": None, "clocks": clk.summary(),
+            "timing": "CUDA events on each slab's stream between a barrier and the last step, max over ranks"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def reference_cfg4_inputs():
+    """cfg4's inputs built with the oracle's own lattice and RandomSource (no product library)."""
+    import numpy as np
     from oracle import oracle as O
-    threads = min(os.cpu_count() or 1, O.openmp_threads())
-    b = cfg3_oracle_steps(threads, 10)
-    return {"metric": "particle-steps/s (fp64 TL-SPH step + splitting damping, random choice)",
-            "value": b["value"], "unit": "PS/s", "impl": "reference", "cpu_baseline": b}
+    dp = 0.004
+    r0 = O.box_lattice([0.0, 0.0, 0.0], [1.0, 1.0, 0.5], dp)
+    n = len(r0)
+    u = O.random_uniforms(3, n * 6)
+    r0 = np.ascontiguousarray(r0 + (2.0 * u[: n * 3].reshape(n, 3) - 1.0) * (0.4 * dp))
+    v0 = -0.01 + 0.02 * u[n * 3:].reshape(n, 3)
+    mat = O.material(2.0e6, 0.3, 1000.0)
+    h = 1.3 * dp
+    body = np.tile([0.0, -9.81, 0.0], (n, 1))
+    return dict(r0=r0, V0=dp ** 3, rho0=1000.0, h=h, constrained=(r0[:, 0] < 5 * dp).astype(np.uint8), v0=v0,
+                body=body, eta=0.2 * 1000.0 * mat["c"] * h, alpha=0.1, seed=0)
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the reference CPU path (oracle port; the reference itself cannot be built here)."""
+    """--impl reference: the reference CPU path (oracle port of runner.cpp:341-391 and the operators it
+    calls; the reference itself cannot be built here) on every host core, same config and window."""
     if rank != 0:
         return None
     from oracle import oracle as O
-    from paper_2103_08932_b200 import scenarios as S
-    cfg = S.cfg2()
-    threads = min(os.cpu_count() or 1, O.openmp_threads())
-    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"])
+    threads = cpu_threads()
+    cfg = reference_cfg4_inputs()
+    W, K = args.warmup, args.steps
+    t0 = time.perf_counter()
+    o = O.OracleSystem(cfg["r0"], cfg["V0"], cfg["rho0"], cfg["h"], constrained=cfg["constrained"])
+    o.set_material(2.0e6, 0.3, 1000.0)
     o.set("v", cfg["v0"])
-    nb = o.neighborhood()
-    s_free = int(nb["offsets"][-1])
-    dpu = 2 * s_free
-    eta_t = cfg["eta"] / cfg["alpha"]
-    for _ in range(max(0, min(args.warmup, 3))):
-        o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)
-    budget = args.cpu_budget * 4
-    times = []
-    t_start = time.perf_counter()
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        o.damping_sweep("particle_split", eta_t, cfg["fixed_dt"], threads=threads)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > budget:
-            break
-    total = sum(times)
-    value = dpu * len(times) / total
+    o.set("body", cfg["body"])
+    o.prepare(threads=threads)
+    init_s = time.perf_counter() - t0
+    n = len(cfg["r0"])
+    slots = int(o.neighborhood([])["offsets"][-1])
+    kw = dict(eta=cfg["eta"], alpha=cfg["alpha"], seed=cfg["seed"], threads=threads)
+    if W > 0:
+        o.run(steps=W, **kw)
+    r = o.run(steps=W + K, resume=W > 0, **kw)
+    value = n * K / r["total_s"]
     return {
-        "impl": "reference",
-        "metric": "damping pair-updates/s (fp64 particle-split Strang sweep)",
-        "value": value, "unit": "DPU/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total / len(times) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded 64^3 lattice, v ~ N(0,1))",
-        "config": {"workload": "cfg2: 3D damping-only sweep, 64^3 lattice, 27-colour particle-split, alpha=1",
-                   "particles": len(cfg["r0"]), "slots": s_free},
-        "cpu_baseline": {"value": value, "unit": "DPU/s", "cores": threads, "kind": "port",
-                         "sample": f"{len(times)} of {args.steps} requested full sweeps (time budget {budget:.0f} s)"},
-        "e2e": {"value": value, "unit": "DPU/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC_PS, "value": value, "unit": "PS/s", "n_gpus": ws, "steps": K,
+        "warmup": W, "ms_per_step": r["total_s"] / K * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered lattice, BASELINE.md §3)",
+        "config": cfg4_config(n, slots, K, W),
+        "cpu_baseline": {"value": value, "unit": "PS/s", "cores": threads, "kind": "port",
+                         "sample": f"cfg4 loop steps {W}..{W + K - 1} (oracle restatement of runner.cpp:341-391, "
+                                   f"OpenMP on {threads} threads); init {init_s:.1f} s untimed"},
+        "e2e": {"value": value, "unit": "PS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "damped_steps": int(r["damped"]),
     }
 
 
+# ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg2"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sampling")
-    ap.add_argument("--ps-steps", type=int, default=300, help="loop steps of the particle-steps/s leg (cfg3)")
-    ap.add_argument("--no-ps", action="store_true", help="skip the particle-steps/s leg")
-    ap.add_argument("--scale-sweeps", type=int, default=10, help="sweeps of the large-body (cfg5-weak) leg")
-    ap.add_argument("--no-scale", action="store_true", help="skip the large-body sweep leg")
-    ap.add_argument("--scale-steps", type=int, default=20, help="loop steps of the N > 1 sharded leg (0: sweep only)")
-    ap.add_argument("--scale-layers", type=int, default=250,
-                    help="x-layers of 250 x 250 per GPU of the N > 1 sharded leg (cfg5 weak scaling)")
-    ap.add_argument("--parity-sweeps", type=int, default=500, help="cfg2 sweeps of the GPU-vs-oracle check (0: skip)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle legs (cpu_baseline, parity)")
+    ap.add_argument("--no-legs", action="store_true", help="headline only")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the operator-API e2e leg of the headline")
+    ap.add_argument("--parity-sweeps", type=int, default=500, help="cfg2 sweeps of the GPU-vs-oracle check")
+    ap.add_argument("--scale-sweeps", type=int, default=10, help="sweeps of the cfg5-weak legs")
+    ap.add_argument("--scale-steps", type=int, default=20, help="loop steps of the cfg5-weak leg (N = 1)")
+    ap.add_argument("--scale-layers", type=int, default=250, help="x-layers of 250 x 250 per GPU (N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    args.steps = max(args.steps, 1)
     ws, rank, local = dist_env()
-    # TLSPH_BENCH_ONE_DEVICE=1: every rank on GPU 0 over gloo (protocol tests of the N > 1 path on a
-    # one-GPU box; small --scale-layers)
-    one_device = os.environ.get("TLSPH_BENCH_ONE_DEVICE") == "1"
+    one_device = os.environ.get("TLSPH_BENCH_ONE_DEVICE") == "1"  # N > 1 protocol on one GPU (tests)
     if one_device:
         local = 0
     if ws > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("gloo" if one_device else "nccl")
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group("gloo" if (one_device or args.impl == "reference") else "nccl")
     if args.impl == "reference":
         out = run_reference(args, ws, rank)
-        if out is not None and not args.no_ps:
-            out["particle_steps"] = reference_particle_steps()
     else:
         from paper_2103_08932_b200 import dev
         dev.select_device(local)
-        out = run_cfg2(args, ws, rank)
-        if not args.no_ps:
-            out["particle_steps"] = particle_steps(args, ws, rank)
-        if not args.no_scale:
-            if ws == 1:
-                out["sweep_at_scale"] = sweep_at_scale(args, ws, rank)
-            else:
-                sh = sweep_sharded(args, ws, rank)
-                if out is not None:
-                    out["sweep_sharded"] = sh
+        if ws > 1:
+            out = sharded_cfg5(args, ws, rank)
+        else:
+            out, cfg, final = headline_cfg4(args)
+            if not args.no_e2e:
+                try:
+                    e = operator_loop("loop", args.steps, args.warmup)
+                    out["e2e"] = {"value": e["value"], "unit": "PS/s", "h2d_bytes_per_step": e["h2d_bytes_per_step"],
+                                  "d2h_bytes_per_step": e["d2h_bytes_per_step"], "path": e["api"],
+                                  "window": f"steps {args.warmup}..{args.warmup + args.steps - 1}",
+                                  "damped_steps": e["damped_steps"]}
+                except Exception as exc:
+                    out["e2e"] = {"error": str(exc)}
+            if not args.no_cpu:
+                threads = cpu_threads()
+                o, ro, init_s = oracle_loop(cfg, args.warmup, args.steps, threads)
+                out["cpu_baseline"] = {"value": len(cfg["r0"]) * args.steps / ro["total_s"], "unit": "PS/s",
+                                       "cores": threads, "kind": "port",
+                                       "sample": f"cfg4 loop steps {args.warmup}..{args.warmup + args.steps - 1}, "
+                                                 f"oracle OpenMP on {threads} threads (init {init_s:.1f} s untimed)"}
+                out["parity"] = {"steps": int(ro["steps"]), "steps_gpu": int(final["steps"]),
+                                 "damped_oracle": int(ro["damped"]), "damped_gpu": int(final["damped"]),
+                                 "t_rel_diff": abs(final["t"] - ro["t"]) / ro["t"],
+                                 "rel_l2_v": rel_l2(final["v"], o.get("v")),
+                                 "rel_l2_displacement": rel_l2(final["u"], o.get("r") - cfg["r0"]),
+                                 "tolerance": 1e-10, "mode": "fast + re-sort (GPU) vs oracle, same W+K steps"}
+                del o
+            if not args.no_legs:
+                for name, fn in (("sweep_cfg2", leg_cfg2), ("cfg1", leg_cfg1), ("particle_steps_cfg3", leg_cfg3),
+                                 ("cfg5_weak", leg_cfg5_weak)):
+                    try:
+                        out[name] = fn(args)
+                    except Exception as exc:
+                        out[name] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0 and out is not None:
         print(json.dumps(out))
     if ws > 1:

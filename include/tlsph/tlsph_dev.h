@@ -350,6 +350,7 @@ typedef struct tlsph_dev_loop_result {
   int stopped_on_ke;
   size_t probe_samples;  /* samples written to probe_out (cumulative across resumes) */
   int paused;            /* 1: stopped at an output mark with pause_on_mark set */
+  uint64_t kernel_launches; /* kernels this call launched (graph kernel nodes per step kind) */
 } tlsph_dev_loop_result;
 
 /* Runs the loop with all state resident on the device; the eta~ sequence is

@@ -187,6 +187,22 @@ void capture(cudaStream_t st, Graph& out, Fn&& fn) {
   CK(cudaGraphInstantiate(&out.e, out.g, 0));
 }
 
+// kernel nodes of a captured graph (the launches one replay issues)
+uint64_t kernel_nodes(const Graph& g) {
+  if (!g.g) return 0;
+  size_t count = 0;
+  CK(cudaGraphGetNodes(g.g, nullptr, &count));
+  std::vector<cudaGraphNode_t> nodes(count);
+  if (count) CK(cudaGraphGetNodes(g.g, nodes.data(), &count));
+  uint64_t k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    CK(cudaGraphNodeGetType(nd, &t));
+    if (t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
 }  // namespace
 
 void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) {
@@ -286,6 +302,9 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
     return loop_flags[step] != 0;
   };
 
+  const uint64_t per_begin = kernel_nodes(g_begin), per_elastic = p.elastic ? kernel_nodes(g_elastic) : 0;
+  const uint64_t per_damp = damping_active ? kernel_nodes(g_damp) : 0;
+  uint64_t launches = 0;
   const uint64_t chunk = 64;
   std::vector<cudaEvent_t> ev(3 * chunk + 2);
   for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -301,13 +320,20 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
       CK(cudaEventRecord(ev[3 * k], stream));
       CK(cudaGraphLaunch(g_begin.e, stream));  // the elastic window includes step_begin (stable_dt, checks)
       if (p.elastic) CK(cudaGraphLaunch(g_elastic.e, stream));
+      launches += per_begin + per_elastic;
       CK(cudaEventRecord(ev[3 * k + 1], stream));
-      if (damping_active && outcome(enq + k)) CK(cudaGraphLaunch(g_damp.e, stream));
+      if (damping_active && outcome(enq + k)) {
+        CK(cudaGraphLaunch(g_damp.e, stream));
+        launches += per_damp;
+      }
       CK(cudaEventRecord(ev[3 * k + 2], stream));
     }
     enq += todo;
     const bool last_chunk = p.max_steps && enq >= p.max_steps;
-    if (last_chunk) begin_launch(1);  // accounting of the final step
+    if (last_chunk) {
+      begin_launch(1);  // accounting of the final step
+      launches += 1;
+    }
     CK_LAUNCH("k_step_begin");
     CK(cudaEventRecord(ev[3 * chunk + 1], stream));
     CK(cudaMemcpyAsync(&hs, scal.p, sizeof(DScalars), cudaMemcpyDeviceToHost, stream));
@@ -340,6 +366,7 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   res.stopped_on_ke = hs.stopped_on_ke;
   res.paused = hs.paused;
   res.probe_samples = static_cast<size_t>(hs.probe_count);
+  res.kernel_launches = launches;
   if (want_probe && hs.probe_count > 0 && p.probe_out) {
     const size_t ncopy = std::min<size_t>(static_cast<size_t>(hs.probe_count), p.probe_capacity);
     CK(cudaMemcpy(p.probe_out, probe_dev.p, ncopy * 4 * sizeof(double), cudaMemcpyDeviceToHost));

@@ -82,7 +82,7 @@ class LoopResult(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("damped_steps", C.c_uint64), ("t", C.c_double), ("last_dt", C.c_double),
                 ("elastic_seconds", C.c_double), ("damping_seconds", C.c_double), ("total_seconds", C.c_double),
                 ("peak_ke", C.c_double), ("final_ke", C.c_double), ("stopped_on_ke", C.c_int),
-                ("probe_samples", C.c_size_t), ("paused", C.c_int)]
+                ("probe_samples", C.c_size_t), ("paused", C.c_int), ("kernel_launches", C.c_uint64)]
 
 
 _lib = None
@@ -522,7 +522,8 @@ class DeviceSystem:
         _check(lib().tlsph_dev_run(self._h, C.byref(p), C.byref(r)))
         return {"steps": r.steps, "damped": r.damped_steps, "t": r.t, "last_dt": r.last_dt,
                 "elastic_s": r.elastic_seconds, "damping_s": r.damping_seconds, "total_s": r.total_seconds,
-                "peak_ke": r.peak_ke, "final_ke": r.final_ke, "stopped_on_ke": bool(r.stopped_on_ke)}
+                "peak_ke": r.peak_ke, "final_ke": r.final_ke, "stopped_on_ke": bool(r.stopped_on_ke),
+                "kernel_launches": int(r.kernel_launches)}
 
     def last_run(self):
         """(completed steps, t) of the last run, also when it stopped on an error."""
