@@ -22,3 +22,12 @@ def test_cpp_suite(binary):
     out = subprocess.run([os.path.join(ROOT, "build", "tests", binary)], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_config_and_output_writers_host_only():
+    """tests/cpp/test_config.cpp: parse_config messages and kinds, probe CSV / report.json bytes (no device)."""
+    _build()
+    out = subprocess.run([os.path.join(ROOT, "build", "tests", "test_config")], capture_output=True, text=True,
+                         timeout=120)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
