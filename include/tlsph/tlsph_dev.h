@@ -254,6 +254,16 @@ typedef enum tlsph_dev_sweep_tiling {
 } tlsph_dev_sweep_tiling;
 tlsph_status tlsph_dev_set_sweep_tiling(tlsph_dev* dev, tlsph_dev_sweep_tiling mode);
 
+/* Temporal blocking of the colour-phase schedule over x-column chunks: phases are run k at a time,
+ * each chunk of `columns` cell columns through an upright trapezoid (narrowing by 2 columns per
+ * phase) and each chunk boundary through the inverted one, so a chunk's velocities stay in L2
+ * across k phases. Every cell task sees the inputs of the phase-by-phase order: results are
+ * bitwise identical. FAST particle split runs it as one persistent dataflow launch (per-column
+ * completion counters), other schemes/modes as column-range launches. columns = -1: automatic
+ * (the phase-by-phase order: blocking measured slower on this B200); columns = 0:
+ * off; phases <= 0 with columns > 0: columns / 4. Ignored for x-slabs (task range or peers). */
+tlsph_status tlsph_dev_set_sweep_blocking(tlsph_dev* dev, int columns, int phases);
+
 /* Penalty contact plane of ExternalAccel<D> (forces.hpp:13-39): a_i +=
  * stiffness * max(0, -(r_i - point).normal) / m_i * normal, evaluated at the
  * current position inside the momentum RHS. stiffness <= 0 removes it. */

@@ -402,6 +402,14 @@ tlsph_status tlsph_dev_set_sweep_tiling(tlsph_dev* dev, tlsph_dev_sweep_tiling m
   });
 }
 
+tlsph_status tlsph_dev_set_sweep_blocking(tlsph_dev* dev, int columns, int phases) {
+  return guarded([&] {
+    if (columns < -1) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "sweep blocking: columns must be >= -1");
+    sys(dev).sweep_block_w = columns;
+    sys(dev).sweep_block_k = phases;
+  });
+}
+
 tlsph_status tlsph_dev_grid_info(const tlsph_dev* dev, int* dims, double* origin, double* cell_size,
                                  int64_t* n_cells) {
   return guarded([&] {

@@ -284,6 +284,7 @@ void DevSystem::run(const tlsph_dev_loop_params& p, tlsph_dev_loop_result& res) 
   });
   if (p.elastic) capture(stream, g_elastic, [&] { enqueue_verlet(*this, mat, 0.0, 1); });
   if (damping_active) {
+    if (p.scheme != TLSPH_SCHEME_EXPLICIT) prepare_sweep_schedule(p.scheme);  // no allocation under capture
     capture(stream, g_damp, [&] {
       if (p.scheme == TLSPH_SCHEME_EXPLICIT) enqueue_explicit(*this, eta_tilde, visc.p);
       else enqueue_sweep(p.scheme, eta_tilde, 0.0, true);

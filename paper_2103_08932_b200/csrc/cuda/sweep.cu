@@ -52,8 +52,13 @@
 //   FAST:    x * y (<= 1 ulp), within the 1e-10 north_star class.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
+#include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "stencil_tile.cuh"
 #include "sweep_chain.cuh"
@@ -84,8 +89,9 @@ void launch_pdl_phase(void (*kernel)(KArgs...), unsigned grid, unsigned block, s
 }
 
 struct Phase {
-  const int* cells;  // this colour's task cells (linear index), fuller first; blockIdx -> cell
-  long long ncol;    // cells in the colour
+  const int* cells;  // this launch's task cells (linear index), fuller first; blockIdx -> cell
+  long long ncol;    // cells in this launch
+  long long ncol_colour;  // cells in the whole colour (the staged/streamed choice follows it)
   int forward;
   int S;           // padded stencil tile length, multiple of 8
   int SC;          // max slots per cell, multiple of 8
@@ -339,9 +345,9 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
 #define TLSPH_STREAM_L2PF 1
 #endif
   if (!SLOTS && TLSPH_STREAM_L2PF) {  // streamed slot block: bring it into L2 ahead of the chain's register loads
-    if (lane == 1) tma_prefetch_l2(f.pf + cs.f0(), static_cast<uint32_t>((cs.f1() - cs.f0()) * 8));
+    if (lane == 1) tma_prefetch_l2_stream(f.pf + cs.f0(), static_cast<uint32_t>((cs.f1() - cs.f0()) * 8));
     else if (lane == 2)
-      tma_prefetch_l2((nl_src ? nl_src : f.nloc) + cs.n0(), static_cast<uint32_t>((cs.n1() - cs.n0()) * 2));
+      tma_prefetch_l2_stream((nl_src ? nl_src : f.nloc) + cs.n0(), static_cast<uint32_t>((cs.n1() - cs.n0()) * 2));
   }
   stamp(blockIdx.x, 3);
   const RowPairs rp = row_pairs(sstart, lane < kSegs ? slen : 0, sbase, lane);
@@ -666,28 +672,19 @@ k_sweep_phase(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 // more cells share an SM -- the form for colours with more cells than one
 // wave of staged tiles holds (large bodies).
 // UNI (with STREAM, uniform masses): no stencil 1/m staged (fast_chain_stream).
-template <int D, int K, bool STREAM, bool UNI>
-__global__ void __launch_bounds__(kWarp)
-k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
-  if (ph.dt_from_scalars && sc->halt) return;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x;
-  stamp(blockIdx.x, 0);
-  stamp(blockIdx.x, 1);
-  grid_launch_dependents();  // the next phase may stage its static data while this one runs
-  int c[3];
-  const long long lin = phase_cell<D>(ph, f, blockIdx.x, c);
-  Tile<D> t = carve<D>(smem, ph);
-  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
-  const double kb = ph.eta * (0.5 * dt);  // b = kb * pair_factor
-
+// One cell task of a FAST particle-split phase, executed by one warp: staging, chain, write-back.
+// PDL: the phase was launched with programmatic dependent launch (wait for the previous phase
+// before the velocity copies).
+template <int D, int K, bool STREAM, bool UNI, bool PDL>
+__device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, long long lin, const int c[3],
+                                          const Tile<D>& t, double kb, int lane) {
   const CellSpan cs{f.cell_start[lin], f.cell_start[lin + 1], f.cell_slot[lin], f.cell_slot[lin + 1]};
   long long sstart, send;
   locate_row<D>(f, c, lane, sstart, send);
   if (cs.p0 == cs.p1) return;
   stamp(blockIdx.x, 2);
-  issue_staging<D, true, false, true, !STREAM || UNI, !STREAM, UNI>(f, t, cs, sstart, send, lane,
-                                                                     UNI ? f.nlocf : f.nloc);
+  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI>(f, t, cs, sstart, send, lane,
+                                                                    UNI ? f.nlocf : f.nloc);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
@@ -726,6 +723,112 @@ k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
 #ifdef TLSPH_SWEEP_TIMING
   if (lane == 0 && blockIdx.x < (1 << 16)) g_sweep_stamp[blockIdx.x][8] = static_cast<unsigned long long>(cs.p1 - cs.p0);
 #endif
+}
+
+template <int D>
+__device__ __forceinline__ void cell_coords(const DFields& f, long long lin, int c[3]) {
+  c[0] = static_cast<int>(lin % f.dims[0]);
+  c[1] = static_cast<int>((lin / f.dims[0]) % f.dims[1]);
+  c[2] = D == 3 ? static_cast<int>(lin / (static_cast<long long>(f.dims[0]) * f.dims[1])) : 0;
+}
+
+// The whole chain of a cell in one warp (sweep_chain.cuh): every slot's
+// metadata is read once for all D components and the D residuals share one
+// shuffle tree.
+// STREAM: the slot block is not staged; the chain reads pair factors, mass
+// factors and stencil indices from global memory (L2), a particle ahead. The
+// tile shrinks to the stencil velocities and per-particle constants, so many
+// more cells share an SM -- the form for colours with more cells than one
+// wave of staged tiles holds (large bodies).
+// UNI (with STREAM, uniform masses): no stencil 1/m staged (fast_chain_stream).
+template <int D, int K, bool STREAM, bool UNI>
+__global__ void __launch_bounds__(kWarp)
+k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
+  if (ph.dt_from_scalars && sc->halt) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  stamp(blockIdx.x, 0);
+  stamp(blockIdx.x, 1);
+  grid_launch_dependents();  // the next phase may stage its static data while this one runs
+  int c[3];
+  const long long lin = phase_cell<D>(ph, f, blockIdx.x, c);
+  Tile<D> t = carve<D>(smem, ph);
+  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
+  fast_task<D, K, STREAM, UNI, true>(f, ph, lin, c, t, ph.eta * (0.5 * dt), lane);  // b = kb * pair_factor
+}
+
+// ------------------------------------------------------------------ the dataflow sweep
+// A whole FAST particle-split sweep in one persistent launch (sweep_flow below): warps dequeue
+// cell tasks (cell, global phase) in the temporally blocked order and run each once the tasks it
+// depends on are complete. A task touches its cell's 3^D stencil, x-1..x+1, so it depends exactly
+// on the earlier-phase tasks in columns x-2..x+2; per column a counter of completed tasks, and
+// pref[p][x] = the number of tasks of phases < p in column x. A column's counter reaches pref[p][x]
+// only once all of those tasks are done (a task never completes before the earlier-phase tasks of
+// its own column), so waiting for counter >= pref on the five columns orders every pair of
+// overlapping tasks as the phase-by-phase sweep does: bitwise the same result, with no launch
+// boundaries and each chunk's velocities reused from L2 across its k phases. The queue order is a
+// topological order of these dependencies and every dequeued task is held by a resident warp,
+// so the waits always end.
+struct Flow {
+  const int2* queue;  // (cell, phase) in schedule order
+  long long ntask;
+  const int* pref;    // (2 nb + 1) x dims[0]
+  int* done;          // per column, zeroed per sweep
+  unsigned long long* head;  // dequeue counter, zeroed per sweep
+  int nb;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifndef TLSPH_FLOW_MINB
+#define TLSPH_FLOW_MINB 15
+#endif
+template <int D, int K, bool STREAM, bool UNI>
+__global__ void __launch_bounds__(kWarp, TLSPH_FLOW_MINB)
+k_sweep_flow(DFields f, Phase ph, Flow fl, const DScalars* __restrict__ sc) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  grid_dependency_wait();  // fold constants, dt, the preceding step
+  if (ph.dt_from_scalars && sc->halt) return;
+  Tile<D> t = carve<D>(smem, ph);
+  const double dt = ph.dt_from_scalars ? sc->dt : ph.dt;
+  const double kb = ph.eta * (0.5 * dt);
+  const int nx = f.dims[0];
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(fl.head, 1ull);
+    k = __shfl_sync(kFull, k, 0);
+    if (static_cast<long long>(k) >= fl.ntask) break;
+    const int2 task = fl.queue[k];
+    int c[3];
+    cell_coords<D>(f, task.x, c);
+    if (lane < 5) {
+      const int x = c[0] - 2 + lane;
+      if (x >= 0 && x < nx) {
+        const int need = fl.pref[static_cast<size_t>(task.y) * nx + x];
+        // bounded: a schedule fault aborts the launch (~10 s) instead of hanging the device
+        for (long long spin = 0; ld_acquire(fl.done + x) < need; ++spin) {
+          if (spin > (1ll << 27)) __trap();
+          __nanosleep(64);
+        }
+      }
+    }
+    __syncwarp();
+    Phase pt = ph;
+    pt.forward = task.y < fl.nb;
+    fast_task<D, K, STREAM, UNI, false>(f, pt, task.x, c, t, kb, lane);
+    if (lane == 0) mbar_inval(t.bar);
+    bulk_wait_all();  // this lane's bulk stores performed, not only read from shared memory
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(fl.done + c[0], 1);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ pairwise split, one warp per cell
@@ -966,7 +1069,7 @@ inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_byte
   // measured crossover: staged still wins at ~1.6 waves (cfg3: 1.133 vs 1.188 ms per sweep) and
   // loses from ~11 waves on (cfg4 12.5 vs 10.4, cfg5-weak 24.2 vs 18.0)
   const long long per_sm = std::max<long long>(1, static_cast<long long>((228 * 1024) / (staged_bytes + 1024)));
-  return ph.ncol > 2 * per_sm * sms;
+  return std::max(ph.ncol, ph.ncol_colour) > 2 * per_sm * sms;
 }
 
 inline bool uniform_disabled() {  // TLSPH_SWEEP_UNIFORM=0: the stencil-1/m form even for uniform masses (A/B)
@@ -1036,6 +1139,41 @@ void launch_fast(const DevSystem& s, const DFields& f, const Phase& ph) {
     else launch_fast_impl<D, K, false, false>(s, f, ph);
   } else if (f.nlocf && !uniform_disabled()) launch_fast_impl<D, K, true, true>(s, f, ph);
   else launch_fast_impl<D, K, true, false>(s, f, ph);
+}
+
+// The dataflow sweep (k_sweep_flow): one persistent launch of as many one-warp CTAs as fit.
+template <int D, int K, bool STREAM, bool UNI>
+void launch_flow_impl(const DevSystem& s, const DFields& f, Phase ph, const Flow& fl) {
+  if (STREAM) {
+    ph.SC = 0;
+    ph.fast = UNI ? 1 : 2;
+  } else if (UNI) {
+    ph.fast = 3;
+  }
+  const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
+  auto kern = k_sweep_flow<D, K, STREAM, UNI>;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = smem;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarp, smem));
+  const long long grid = std::min<long long>(static_cast<long long>(std::max(per_sm, 1)) * sms, fl.ntask);
+  launch_pdl_phase(kern, static_cast<unsigned>(std::max<long long>(grid, 1)), kWarp, smem, s.stream, f, ph, fl,
+                   static_cast<const DScalars*>(s.scal.p));
+}
+
+template <int D, int K>
+void launch_flow(const DevSystem& s, const DFields& f, const Phase& ph, const Flow& fl) {
+  const bool uni = f.nlocf && !uniform_disabled();
+  if (!stream_slots(s, ph, tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, uni ? 3 : ph.fast))) {
+    if (uni) launch_flow_impl<D, K, false, true>(s, f, ph, fl);
+    else launch_flow_impl<D, K, false, false>(s, f, ph, fl);
+  } else if (uni) launch_flow_impl<D, K, true, true>(s, f, ph, fl);
+  else launch_flow_impl<D, K, true, false>(s, f, ph, fl);
 }
 
 // ------------------------------------------------------------------ ORDERED particle split, one warp per cell
@@ -1308,13 +1446,8 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
 // reverse, damping.cpp:112-121); tasks are the colour's cells whose x lies in
 // the task range [task_x0, task_x1) (the whole grid unless a slab is set).
 template <int D>
-void enqueue_phase(DevSystem& s, int scheme, Phase ph, int pass, int index) {
-  constexpr int nb = colour_count<D>();
-  const int b = pass == 0 ? index : nb - 1 - index;
-  ph.forward = pass == 0;
-  ph.cells = s.colour_cells.p + s.colour_start[b];
-  ph.ncol = s.colour_start[b + 1] - s.colour_start[b];
-  if (ph.ncol == 0) return;  // empty colour (neighbors.cpp:152)
+void launch_tasks(DevSystem& s, int scheme, Phase ph) {
+  if (ph.ncol == 0) return;  // empty colour (neighbors.cpp:152) or an empty column range
   const DFields f = s.fields();
   if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT) {
     if (s.reduction == TLSPH_REDUCTION_ORDERED) launch_particle_split<D, true>(s, f, ph);
@@ -1325,10 +1458,174 @@ void enqueue_phase(DevSystem& s, int scheme, Phase ph, int pass, int index) {
 }
 
 template <int D>
+int phase_colour(int pass, int index) {
+  return pass == 0 ? index : colour_count<D>() - 1 - index;
+}
+
+template <int D>
+void enqueue_phase(DevSystem& s, int scheme, Phase ph, int pass, int index) {
+  const int b = phase_colour<D>(pass, index);
+  ph.forward = pass == 0;
+  ph.cells = s.colour_cells.p + s.colour_start[b];
+  ph.ncol = ph.ncol_colour = s.colour_start[b + 1] - s.colour_start[b];
+  launch_tasks<D>(s, scheme, ph);
+}
+
+// Global phase p (0 .. 2 nb - 1) restricted to the tasks whose cell x lies in [xa, xb).
+template <int D>
+void enqueue_phase_columns(DevSystem& s, int scheme, Phase ph, int p, int xa, int xb) {
+  constexpr int nb = colour_count<D>();
+  const int nx = s.dims[0];
+  xa = std::max(xa, 0);
+  xb = std::min(xb, nx);
+  if (xa >= xb) return;
+  const int pass = p / nb, b = phase_colour<D>(pass, p % nb);
+  const long long* st = s.xcol_start.data() + static_cast<size_t>(b) * (nx + 1);
+  ph.forward = pass == 0;
+  ph.cells = s.xcol_cells.p + st[xa];
+  ph.ncol = st[xb] - st[xa];
+  ph.ncol_colour = s.colour_start[b + 1] - s.colour_start[b];
+  launch_tasks<D>(s, scheme, ph);
+}
+
+// Blocking parameters (W columns per chunk, k phases per block); {0, 0}: phase-by-phase order.
+// Set by tlsph_dev_set_sweep_blocking or TLSPH_SWEEP_BLOCK="W,k" (W = 0: off). AUTO keeps the
+// phase-by-phase order: measured on cfg4 / cfg5-weak the blocked schedule cuts DRAM bytes per phase
+// by ~45 % (chunk velocities reused from L2) but is slower -- 14-17 ms vs 10.4 ms per cfg4 sweep
+// as column-range launches (launch gaps, partial waves), 16.6 ms as the dataflow kernel (per-task
+// dequeue / completion latency) -- because the phase kernel is bound by L1 traffic and chain
+// latency, not by DRAM (ncu: DRAM 37 %, L1 74 % of peak; profiles/r2_sweep_blocking.md).
+template <int D>
+std::pair<int, int> sweep_blocking(const DevSystem& s, int scheme) {
+  const int nx = s.dims[0];
+  static const std::pair<int, int> forced = [] {
+    const char* e = std::getenv("TLSPH_SWEEP_BLOCK");
+    if (!e || !*e) return std::pair<int, int>{-1, -1};
+    int w = 0, k = 0;
+    if (std::sscanf(e, "%d,%d", &w, &k) < 1) return std::pair<int, int>{-1, -1};
+    return std::pair<int, int>{w, k};
+  }();
+  if (s.task_x0 > 0 || (s.task_x1 >= 0 && s.task_x1 < nx) || s.peer_x[0] >= 0 || s.peer_x[1] >= 0 ||
+      s.xcol_start.empty())
+    return {0, 0};  // slabs keep the phase-by-phase order (the cross-slab protocol is per phase)
+  int w = 0, k = 0;
+  if (s.sweep_block_w >= 0 || forced.first >= 0) {
+    w = s.sweep_block_w >= 0 ? s.sweep_block_w : forced.first;
+    k = s.sweep_block_w >= 0 ? s.sweep_block_k : forced.second;
+    if (k <= 0) k = w / 4;
+  } else {
+    return {0, 0};
+  }
+  if (w <= 0 || k <= 1 || w >= nx || w < 4 * k) return {0, 0};  // chunks are >= w wide (blocked_order)
+  return {w, k};
+}
+
+// The temporally blocked order of one sweep's cell tasks over x-column chunks. The 2 nb phases
+// are taken k at a time; within a block every chunk [lo, hi) runs its upright trapezoid (phase j
+// of the block on tasks with x in [lo + 2j, hi - 2j), the sides at the body's ends not narrowed)
+// and, once the chunk to its right is done, each internal chunk boundary B its inverted trapezoid
+// (phase j on [B - 2j, B + 2j)). A task touches x-1..x+1, so a phase-(j+1) task depends only on
+// phase-j tasks within 2 columns: every task comes after all the earlier-phase tasks it overlaps
+// and before the later-phase tasks that overlap it, i.e. it sees exactly the inputs of the
+// phase-by-phase order. `emit(p, xa, xb)` receives the ranges in that order.
+template <int D, typename Emit>
+void blocked_order(int nx, int w, int k, Emit&& emit) {
+  constexpr int nphase = 2 * colour_count<D>();
+  const int nchunk = std::max(1, nx / w);  // chunks of w .. 2w-1 columns: the trapezoids never invert
+  std::vector<int> lo(static_cast<size_t>(nchunk) + 1);
+  for (int c = 0; c <= nchunk; ++c) lo[static_cast<size_t>(c)] = static_cast<int>(static_cast<long long>(c) * nx / nchunk);
+  for (int p0 = 0; p0 < nphase; p0 += k) {
+    const int kk = std::min(k, nphase - p0);
+    for (int c = 0; c < nchunk; ++c) {
+      const int a = lo[static_cast<size_t>(c)], b = lo[static_cast<size_t>(c) + 1];
+      for (int j = 0; j < kk; ++j) emit(p0 + j, a + (c > 0 ? 2 * j : 0), b - (c + 1 < nchunk ? 2 * j : 0));
+      if (c > 0)
+        for (int j = 1; j < kk; ++j) emit(p0 + j, a - 2 * j, a + 2 * j);
+    }
+  }
+}
+
+// Task queue and per-column prefix counts of the dataflow sweep for (w, k); rebuilt when they change.
+template <int D>
+Flow flow_schedule(DevSystem& s, int w, int k) {
+  constexpr int nb = colour_count<D>();
+  const int nx = s.dims[0];
+  if (s.flow_w != w || s.flow_k != k || s.flow_ntask == 0) {
+    std::vector<int2> q;
+    q.reserve(static_cast<size_t>(s.colour_start[nb]));
+    blocked_order<D>(nx, w, k, [&](int p, int xa, int xb) {
+      xa = std::max(xa, 0);
+      xb = std::min(xb, nx);
+      if (xa >= xb) return;
+      const int b = phase_colour<D>(p / nb, p % nb);
+      const long long* st = s.xcol_start.data() + static_cast<size_t>(b) * (nx + 1);
+      for (long long e = st[xa]; e < st[xb]; ++e) q.push_back(make_int2(s.xcol_cells_h[static_cast<size_t>(e)], p));
+    });
+    std::vector<int> pref(static_cast<size_t>(2 * nb + 1) * nx, 0);
+    for (int p = 0; p < 2 * nb; ++p) {
+      const int b = phase_colour<D>(p / nb, p % nb);
+      const long long* st = s.xcol_start.data() + static_cast<size_t>(b) * (nx + 1);
+      for (int x = 0; x < nx; ++x)
+        pref[static_cast<size_t>(p + 1) * nx + x] =
+            pref[static_cast<size_t>(p) * nx + x] + static_cast<int>(st[x + 1] - st[x]);
+    }
+    if (q.size() != static_cast<size_t>(2 * s.colour_start[nb]))
+      throw DevError(TLSPH_ERR_INTERNAL, "blocked sweep schedule does not cover every cell task twice");
+    s.flow_queue.alloc(q.size());
+    s.flow_pref.alloc(pref.size());
+    s.flow_done.alloc(static_cast<size_t>(nx));
+    s.flow_head.alloc(1);
+    CK(cudaMemcpyAsync(s.flow_queue.p, q.data(), q.size() * sizeof(int2), cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemcpyAsync(s.flow_pref.p, pref.data(), pref.size() * sizeof(int), cudaMemcpyHostToDevice, s.stream));
+    s.sync();
+    s.flow_w = w;
+    s.flow_k = k;
+    s.flow_ntask = static_cast<long long>(q.size());
+  }
+  Flow fl{};
+  fl.queue = s.flow_queue.p;
+  fl.ntask = s.flow_ntask;
+  fl.pref = s.flow_pref.p;
+  fl.done = s.flow_done.p;
+  fl.head = s.flow_head.p;
+  fl.nb = nb;
+  return fl;
+}
+
+template <int D>
+void enqueue_sweep_blocked(DevSystem& s, int scheme, const Phase& ph, int w, int k) {
+  const int K = (s.max_row + kWarp - 1) / kWarp;
+  if (scheme == TLSPH_SCHEME_PARTICLE_SPLIT && s.reduction != TLSPH_REDUCTION_ORDERED && K <= 4) {
+    const Flow fl = flow_schedule<D>(s, w, k);
+    CK(cudaMemsetAsync(s.flow_done.p, 0, static_cast<size_t>(s.dims[0]) * sizeof(int), s.stream));
+    CK(cudaMemsetAsync(s.flow_head.p, 0, sizeof(unsigned long long), s.stream));
+    const DFields f = s.fields();
+    Phase pf = ph;
+    pf.ncol = pf.ncol_colour = s.colour_start[1] - s.colour_start[0];  // the staged/streamed choice
+    for (int b = 1; b < colour_count<D>(); ++b)
+      pf.ncol_colour = std::max(pf.ncol_colour, s.colour_start[b + 1] - s.colour_start[b]);
+    pf.ncol = pf.ncol_colour;
+    if (K <= 1) launch_flow<D, 1>(s, f, pf, fl);
+    else if (K == 2) launch_flow<D, 2>(s, f, pf, fl);
+    else if (K == 3) launch_flow<D, 3>(s, f, pf, fl);
+    else launch_flow<D, 4>(s, f, pf, fl);
+    return;
+  }
+  // other schemes and modes: the same order as a sequence of column-range launches
+  blocked_order<D>(s.dims[0], w, k,
+                   [&](int p, int xa, int xb) { enqueue_phase_columns<D>(s, scheme, ph, p, xa, xb); });
+}
+
+template <int D>
 void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_scal) {
   const Phase ph = prepare_sweep<D>(s, scheme, eta, dt, from_scal);
-  for (int pass = 0; pass < 2; ++pass)
-    for (int bb = 0; bb < colour_count<D>(); ++bb) enqueue_phase<D>(s, scheme, ph, pass, bb);
+  const auto [w, k] = sweep_blocking<D>(s, scheme);
+  if (w > 0) {
+    enqueue_sweep_blocked<D>(s, scheme, ph, w, k);
+  } else {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int bb = 0; bb < colour_count<D>(); ++bb) enqueue_phase<D>(s, scheme, ph, pass, bb);
+  }
   CK_LAUNCH("k_sweep_phase");
 }
 
@@ -1384,6 +1681,18 @@ __global__ void k_selftest_division(unsigned long long seed, long long n, unsign
 }
 
 }  // namespace
+
+void DevSystem::prepare_sweep_schedule(int scheme) {
+  auto build = [&](auto dim) {
+    constexpr int DD = decltype(dim)::value;
+    const auto [w, k] = sweep_blocking<DD>(*this, scheme);
+    const int K = (max_row + kWarp - 1) / kWarp;
+    if (w > 0 && scheme == TLSPH_SCHEME_PARTICLE_SPLIT && reduction != TLSPH_REDUCTION_ORDERED && K <= 4)
+      flow_schedule<DD>(*this, w, k);
+  };
+  if (D == 2) build(std::integral_constant<int, 2>{});
+  else build(std::integral_constant<int, 3>{});
+}
 
 void DevSystem::enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars) {
   if (D == 2) enqueue_sweep_d<2>(*this, scheme, eta_tilde, dt_fixed, dt_from_scalars);
@@ -1528,28 +1837,47 @@ void DevSystem::build_colour_lists() {
   sync();
   const int x0 = task_x0, x1 = task_x1 < 0 ? dims[0] : std::min(task_x1, dims[0]);
   const int nb = D == 2 ? 9 : 27;
-  std::vector<int> cells;
+  const int nx = dims[0];
+  std::vector<int> cells, xcells;
   colour_start.assign(static_cast<size_t>(nb + 1), 0);
+  xcol_start.assign(static_cast<size_t>(nb) * (nx + 1), 0);
   std::vector<std::pair<long long, int>> col;  // (-count, cell)
+  std::vector<std::tuple<int, long long, int>> bycol;  // (x, -count, cell)
   for (int b = 0; b < nb; ++b) {
     const int r0 = b % 3, r1 = (b / 3) % 3, r2 = D == 3 ? b / 9 : 0;
     col.clear();
+    bycol.clear();
     for (int z = r2; z < (D == 3 ? dims[2] : 1); z += 3)
       for (int y = r1; y < dims[1]; y += 3)
         for (int x = r0; x < dims[0]; x += 3) {
           if (x < x0 || x >= x1) continue;
           const long long lin = (static_cast<long long>(z) * dims[1] + y) * dims[0] + x;
           const long long cnt = cst[lin + 1] - cst[lin];
-          if (cnt > 0) col.emplace_back(-cnt, static_cast<int>(lin));
+          if (cnt > 0) {
+            col.emplace_back(-cnt, static_cast<int>(lin));
+            bycol.emplace_back(x, -cnt, static_cast<int>(lin));
+          }
         }
     std::stable_sort(col.begin(), col.end());
     colour_start[b] = static_cast<long long>(cells.size());
     for (const auto& c : col) cells.push_back(c.second);
+    std::stable_sort(bycol.begin(), bycol.end());
+    long long* xs = xcol_start.data() + static_cast<size_t>(b) * (nx + 1);
+    size_t k = 0;
+    for (int x = 0; x <= nx; ++x) {
+      while (k < bycol.size() && std::get<0>(bycol[k]) < x) xcells.push_back(std::get<2>(bycol[k++]));
+      xs[x] = static_cast<long long>(xcells.size());
+    }
   }
   colour_start[nb] = static_cast<long long>(cells.size());
   colour_cells.alloc(std::max<size_t>(cells.size(), 1));
-  if (!cells.empty())
+  xcol_cells.alloc(std::max<size_t>(xcells.size(), 1));
+  xcol_cells_h = xcells;
+  flow_ntask = 0;  // the dataflow schedule is rebuilt from the new lists
+  if (!cells.empty()) {
     CK(cudaMemcpyAsync(colour_cells.p, cells.data(), cells.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(xcol_cells.p, xcells.data(), xcells.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+  }
   sync();
 }
 

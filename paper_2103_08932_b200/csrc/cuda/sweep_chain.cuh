@@ -242,6 +242,9 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
 // (state.cu k_qf), so the arithmetic is that of fast_chain. UNI (uniform
 // masses): no stencil 1/m either; the factor is pair_factor * RN(1/m) unless
 // bit 15 of the slot's stencil index marks a clamped j.
+#ifndef TLSPH_SWEEP_STREAM_HINT
+#define TLSPH_SWEEP_STREAM_HINT 0
+#endif
 template <int D, int K, bool UNI>
 __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lane) {
   const int np = t.np;
@@ -257,8 +260,10 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     for (int u = 0; u < K; ++u) {
       const int s = lane + u * 32;
       const bool v = s < cnt;
-      j[u] = v ? static_cast<int>(t.nl[lo + s]) : li;  // invalid lanes read i itself with b = 0
-      pf[u] = v ? t.pf[lo + s] : 0.0;
+      // streaming loads: the slot block is read once per sweep (evict-first; the stencil
+      // velocities keep L2)
+      j[u] = v ? static_cast<int>(TLSPH_SWEEP_STREAM_HINT ? __ldcs(t.nl + lo + s) : t.nl[lo + s]) : li;
+      pf[u] = v ? (TLSPH_SWEEP_STREAM_HINT ? __ldcs(t.pf + lo + s) : t.pf[lo + s]) : 0.0;
     }
   };
   auto mass_factors = [&](const int (&j)[K], const double (&pf)[K], double (&q)[K]) {

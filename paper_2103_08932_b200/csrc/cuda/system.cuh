@@ -104,6 +104,19 @@ class DevSystem {
   int peer_x[2] = {-1, -1};
   DBuf<int> colour_cells;
   std::vector<long long> colour_start;
+  // the same task cells ordered by x column (fuller first within a column), for the temporally
+  // blocked sweep (sweep.cu, enqueue_sweep_blocked): colour b's cells of column x are
+  // xcol_cells[xcol_start[b * (dims[0] + 1) + x] .. xcol_start[b * (dims[0] + 1) + x + 1])
+  DBuf<int> xcol_cells;
+  std::vector<long long> xcol_start;
+  int sweep_block_w = -1, sweep_block_k = 0;  // tlsph_dev_set_sweep_blocking (-1: automatic)
+  std::vector<int> xcol_cells_h;
+  // the dataflow sweep's task queue (cell, phase), per-column prefix counts, counters (sweep.cu)
+  DBuf<int2> flow_queue;
+  DBuf<int> flow_pref, flow_done;
+  DBuf<unsigned long long> flow_head;
+  int flow_w = 0, flow_k = 0;
+  long long flow_ntask = 0;
 
   // fields (sorted order)
   DBuf<double> r0[3], r[3], v[3], a[3], body[3];
@@ -219,6 +232,8 @@ class DevSystem {
   // damping (damping.cu)
   void damping_sweep(int scheme, double eta_tilde, double dt, int count);
   void enqueue_sweep(int scheme, double eta_tilde, double dt_fixed, bool dt_from_scalars);
+  // builds what enqueue_sweep allocates on first use (the dataflow schedule), before a graph capture
+  void prepare_sweep_schedule(int scheme);
   // one colour phase (pass 0 forward / 1 reverse, index-th colour of the pass)
   void enqueue_sweep_phase(int scheme, double eta_tilde, double dt_fixed, int pass, int index);
   std::vector<cudaEvent_t> phase_events;  // tlsph_dev_sweep_linked: one per colour phase (this device)

@@ -104,6 +104,14 @@ constexpr int kGB3 = TLSPH_TL_GB3, kGC3 = TLSPH_TL_GC3;  // lanes per particle i
 #define TLSPH_TL_SORTED 1
 #endif
 template <int D, int G, bool OI = false>
+// slots whose metadata and neighbour records a thread of the slot-order (OI) passes loads ahead of
+// their (still strictly slot-ordered) accumulation
+#ifndef TLSPH_TL_OU
+#define TLSPH_TL_OU 1
+#endif
+#ifndef TLSPH_TL_STREAM_HINT
+#define TLSPH_TL_STREAM_HINT 0
+#endif
 struct SlotView {
   const int* nbr;
   const double* dw;
@@ -124,6 +132,13 @@ struct SlotView {
   __device__ __forceinline__ long long at(const DFields& f, long long ob, long long lo, long long s) const {
     if (OI) return ob + 32 * (s - lo);
     return s;
+  }
+  // Slot fields are read once per pass: streaming loads (evict-first in L1 and L2), so they do
+  // not displace the neighbour records the gathers reuse (TLSPH_TL_STREAM_HINT=0: plain loads).
+  __device__ __forceinline__ int nb(long long su) const { return TLSPH_TL_STREAM_HINT ? __ldcs(nbr + su) : nbr[su]; }
+  __device__ __forceinline__ double w(long long su) const { return TLSPH_TL_STREAM_HINT ? __ldcs(dw + su) : dw[su]; }
+  __device__ __forceinline__ double e(int d, long long su) const {
+    return TLSPH_TL_STREAM_HINT ? __ldcs(e0[d] + su) : e0[d][su];
   }
 };
 
@@ -162,10 +177,10 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
       for (int u = 0; u < U; ++u) {
         const bool ok = s + u * G < hi;
         const long long su = sv.at(f, ob_i, lo_i, ok ? s + u * G : s);
-        j[u] = sv.nbr[su];
-        dw[u] = sv.dw[su];
+        j[u] = sv.nb(su);
+        dw[u] = sv.w(su);
 #pragma unroll
-        for (int d = 0; d < D; ++d) e[u][d] = sv.e0[d][su];
+        for (int d = 0; d < D; ++d) e[u][d] = sv.e(d, su);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -229,7 +244,7 @@ __global__ void TL_BOUNDS_C k_deformation_rate(DFields f, DScalars* sc, double d
 }
 template <int D, bool POST, bool OI = false>
 __global__ void k_deformation_rate_ordered(DFields f, DScalars* sc, double dt, int loop) {
-  deformation_rate_body<D, 1, 1, POST, false, OI>(f, sc, dt, loop);
+  deformation_rate_body<D, 1, OI ? TLSPH_TL_OU : 1, POST, false, OI>(f, sc, dt, loop);
 }
 
 // ------------------------------------------------------------------ density (integrator.cpp:60-78)
@@ -340,28 +355,32 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long su = sv.at(f, ob_i, lo_i, s + u * G < hi ? s + u * G : s);
-        j[u] = sv.nbr[su];
-        dw[u] = sv.dw[su];
+        j[u] = sv.nb(su);
+        dw[u] = sv.w(su);
 #pragma unroll
-        for (int d = 0; d < D; ++d) e[u][d] = sv.e0[d][su];
+        for (int d = 0; d < D; ++d) e[u][d] = sv.e(d, su);
+      }
+      // P B0 and V0 of each j in W/2 16-byte loads from one packed record; all U records are
+      // requested before the first is used (slots past the row end re-read a valid record)
+      double pbj[U][W];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int k = 0; k < W / 2; ++k) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(f.pbv + pbv_at<D>(f.n, j[u], 2 * k)));
+          pbj[u][2 * k] = x.x;
+          pbj[u][2 * k + 1] = x.y;
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (u > 0 && s + u * G >= hi) break;
-        // P B0 and V0 of j in W/2 16-byte loads from one packed record
-        double pbj[W];
-#pragma unroll
-        for (int k = 0; k < W / 2; ++k) {
-          const double2 x = __ldg(reinterpret_cast<const double2*>(f.pbv + pbv_at<D>(f.n, j[u], 2 * k)));
-          pbj[2 * k] = x.x;
-          pbj[2 * k + 1] = x.y;
-        }
-        const double k = V0i * pbj[D * D] * dw[u];
+        const double k = V0i * pbj[u][D * D] * dw[u];
 #pragma unroll
         for (int r = 0; r < D; ++r) {
-          double t = (k * (pbi[r * D] + pbj[r * D])) * e[u][0];
+          double t = (k * (pbi[r * D] + pbj[u][r * D])) * e[u][0];
 #pragma unroll
-          for (int q = 1; q < D; ++q) t = t + (k * (pbi[r * D + q] + pbj[r * D + q])) * e[u][q];
+          for (int q = 1; q < D; ++q) t = t + (k * (pbi[r * D + q] + pbj[u][r * D + q])) * e[u][q];
           acc[r] = acc[r] + t;
         }
       }
@@ -411,7 +430,7 @@ __global__ void TL_BOUNDS_B k_momentum(DFields f, DScalars* sc, double dt_arg, i
 }
 template <int D, bool KICK, bool OI = false>
 __global__ void k_momentum_ordered(DFields f, DScalars* sc, double dt_arg, int loop) {
-  momentum_body<D, 1, 1, KICK, OI>(f, sc, dt_arg, loop);
+  momentum_body<D, 1, OI ? TLSPH_TL_OU : 1, KICK, OI>(f, sc, dt_arg, loop);
 }
 
 template <int D>

@@ -128,6 +128,7 @@ def lib():
     L.tlsph_dev_set_reduction.argtypes = [P, I]
     L.tlsph_dev_sweep_linked.argtypes = [C.POINTER(P), I, I, C.c_double, C.c_double, I]
     L.tlsph_dev_set_sweep_tiling.argtypes = [P, I]
+    L.tlsph_dev_set_sweep_blocking.argtypes = [P, I, I]
     L.tlsph_dev_set_resort.argtypes = [P, I]
     L.tlsph_dev_last_run_steps.argtypes = [P]
     L.tlsph_dev_last_run_steps.restype = C.c_int64
@@ -285,6 +286,11 @@ class DeviceSystem:
     def set_sweep_tiling(self, mode):
         """FAST sweep slot-block placement: "auto", "staged" (shared memory) or "streamed" (L2)."""
         _check(lib().tlsph_dev_set_sweep_tiling(self._h, {"auto": 0, "staged": 1, "streamed": 2}[mode]))
+
+    def set_sweep_blocking(self, columns=-1, phases=0):
+        """Temporal blocking of the sweep's phase schedule over x-column chunks (-1: automatic,
+        0: off); results are bitwise those of the phase-by-phase order."""
+        _check(lib().tlsph_dev_set_sweep_blocking(self._h, int(columns), int(phases)))
 
     # ---- fields
     def _shape(self, name):

@@ -489,6 +489,58 @@ def test_sweep_tiling_staged_equals_streamed(case):
     assert np.array_equal(out["staged"], out["streamed"])
 
 
+def blocking_bodies():
+    rng = np.random.RandomState(11)
+    base3 = lattice_r0([100, 8, 7], 0.01)
+    yield "jitter3d", base3 + rng.uniform(-0.004, 0.004, base3.shape), 0.01 ** 3, 1000.0, 0.013
+    base2 = lattice_r0([160, 12], 0.01)
+    yield "lattice2d", base2, 0.01 ** 2, 1000.0, 0.013
+
+
+@pytest.mark.parametrize("case", list(blocking_bodies()), ids=lambda c: c[0])
+@pytest.mark.parametrize("mode", ["fast", "ordered"])
+@pytest.mark.parametrize("scheme", ["particle_split", "pairwise_split"])
+def test_temporally_blocked_sweep_is_bitwise_phase_by_phase(case, mode, scheme):
+    """The x-chunked trapezoid schedule of the colour phases (tlsph_dev_set_sweep_blocking) gives the
+    phase-by-phase result bit for bit: several chunk widths and depths (uneven chunks, blocks that
+    straddle the forward/reverse pass boundary), both tilings, clamped particles; and in the device
+    loop (graph-captured sweeps with the device dt)."""
+    name, r0, V0, rho0, h = case
+    cons = (r0[:, 0] < np.quantile(r0[:, 0], 0.05)).astype(np.uint8)
+    v = random_velocities(len(r0), r0.shape[1], 1.0, 29)
+    v[cons == 1] = 0.0
+    ref = None
+    for blocking in ((0, 0), (8, 2), (13, 3), (24, 5)):
+        for tiling in (("staged", "streamed") if mode == "fast" and scheme == "particle_split" else ("auto",)):
+            d = dev.DeviceSystem(r0, V0, rho0, h, constrained=cons)
+            d.set_reduction(mode)
+            d.set_sweep_tiling(tiling)
+            d.set_sweep_blocking(*blocking)
+            d.set("v", v)
+            d.damping_sweep(scheme, 400.0, 1e-4, count=2)
+            got = d.get("v")
+            if ref is None:
+                ref = got
+                assert d.grid()["dims"][0] >= 30, "body too short to exercise several chunks"
+            assert np.array_equal(got, ref), (blocking, tiling)
+    if r0.shape[1] == 3 and scheme == "particle_split":
+        mat = S.material()
+        g = np.zeros_like(r0)
+        g[:, 1] = -9.81
+        loop = []
+        for blocking in ((0, 0), (10, 2)):
+            d = dev.DeviceSystem(r0, V0, rho0, h, constrained=cons)
+            d.set_reduction(mode)
+            d.set_sweep_blocking(*blocking)
+            d.set("body", g)
+            d.set("v", v * 0.01)
+            d.prepare(mat)
+            r = d.run(mat, eta=S.eta_for(h), alpha=0.5, steps=6, seed=0)
+            loop.append((d.get("v"), d.get("r"), r["damped"]))
+        assert loop[0][2] > 0
+        assert np.array_equal(loop[0][0], loop[1][0]) and np.array_equal(loop[0][1], loop[1][1])
+
+
 def test_per_step_resort_is_a_pure_storage_permutation():
     """BASELINE cfg4's per-step re-sort: the device loop rebuilds a current-position cell list every
     step; it matches a host binning of the final positions (bit-exact cells, ascending storage order
