@@ -11,6 +11,7 @@ matrices (n, D, D) row-major.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -91,6 +92,8 @@ def lib():
         L.orc_box_lattice.argtypes = [I, D, D, C.c_double, D]
         L.orc_box_lattice.restype = C.c_longlong
         L.orc_run.argtypes = [P, D, D]
+        L.orc_run_probed.argtypes = [P, D, D, D, C.c_longlong, C.POINTER(C.c_longlong)]
+        L.orc_set_contact.argtypes = [P, D, D, C.c_double]
         L.orc_openmp_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -257,17 +260,135 @@ class OracleSystem:
         _check(lib().orc_explicit_damping_accel(self._h, eta, _dp(out), threads))
         return out
 
+    def set_contact(self, point, normal, stiffness):
+        """ExternalAccel's penalty contact plane (forces.hpp:13-24); stiffness <= 0 removes it."""
+        pt = np.zeros(3)
+        nm = np.zeros(3)
+        pt[: self.dim] = point
+        nm[: self.dim] = normal
+        _check(lib().orc_set_contact(self._h, _dp(pt), _dp(nm), float(stiffness)))
+
     def run(self, *, eta, alpha, scheme="particle_split", steps, fixed_dt=0.0, end_time=0.0,
-            elastic=True, seed=0, threads=1, resume=False):
+            elastic=True, seed=0, threads=1, resume=False, probe=-1, interval=0.0):
         """runner.cpp:341-391. resume=True continues the previous run (same damping stream, t and
         step count; `steps` is then the cumulative cap; the returned counts are cumulative, the
-        times are those of this call)."""
+        times are those of this call). probe >= 0: also the probe series of runner.cpp:328,378-395
+        (t, u) at the output marks every `interval` -- returned as "probe" (k x (1 + dim))."""
         params = np.array([self.h, eta, alpha, SCHEMES[scheme], steps, fixed_dt, end_time,
-                           1.0 if elastic else 0.0, seed, threads, 1.0 if resume else 0.0], dtype=np.float64)
+                           1.0 if elastic else 0.0, seed, threads, 1.0 if resume else 0.0,
+                           float(probe), float(interval)], dtype=np.float64)
         out = np.zeros(8)
-        _check(lib().orc_run(self._h, _dp(params), _dp(out)))
-        return {"steps": int(out[0]), "damped": int(out[1]), "t": out[2], "elastic_s": out[3],
-                "damping_s": out[4], "total_s": out[5], "last_dt": out[6]}
+        cap = int(end_time / interval) + 8 if probe >= 0 and interval > 0 else (2 if probe >= 0 else 0)
+        samples = np.zeros((max(cap, 1), 4))
+        ns = C.c_longlong(0)
+        _check(lib().orc_run_probed(self._h, _dp(params), _dp(out), _dp(samples), cap, C.byref(ns)))
+        r = {"steps": int(out[0]), "damped": int(out[1]), "t": out[2], "elastic_s": out[3],
+             "damping_s": out[4], "total_s": out[5], "last_dt": out[6]}
+        if probe >= 0:
+            r["probe"] = samples[: ns.value, : 1 + self.dim].copy()
+        return r
+
+
+# ---- the built-in cases (reference: proj/src/tlsph/cases.cpp:15-231)
+GRAVITY_CASES = 9.8  # cases.cpp:15 (kGravity)
+CLAMP_LAYERS = 3     # cases.cpp:18
+
+
+def case_spec(name, resolution=0):
+    """builtin_cases + make_case (cases.cpp:72-144): the case constants, dp from the resolution."""
+    if name in ("bending_cantilever", "twisting_cantilever"):
+        spec = dict(name=name, dim=3, resolution=6, length=0.04, thickness=0.016, E=5.0e4, nu=0.45, rho0=1265.0,
+                    model="neo_hookean", gravity=GRAVITY_CASES, L=0.04, beta=0.4, end_time=2.0, interval=0.005,
+                    probe_target=(0.04, 0.0, 0.0), rotational=False)
+        if name == "twisting_cantilever":  # cases.cpp:96-105
+            spec.update(resolution=12, gravity=0.0, rotational=True, probe_target=(0.04, 0.008, 0.008))
+    elif name == "falling_ball":  # cases.cpp:107-127
+        spec = dict(name=name, dim=2, resolution=50, diameter=1.0, clearance=0.25, E=5.0e5, nu=0.45, rho0=1000.0,
+                    model="linear_kirchhoff", gravity=GRAVITY_CASES, L=1.0, beta=1.0, end_time=6.0, interval=0.005,
+                    probe_target=(0.0, 0.75, 0.0), contact_stiffness=0.0)
+    else:
+        raise OracleError(2, f"unknown case '{name}'")
+    if resolution > 0:
+        spec["resolution"] = resolution
+    ref = spec["diameter"] if name == "falling_ball" else spec["thickness"]
+    spec["dp"] = ref / spec["resolution"]  # cases.cpp:137-141
+    return spec
+
+
+def disk(center, diameter, dp):
+    """generate_disk (cases.cpp:48-64): lattice offsets (i dp, j dp), |offset| <= radius, j outer."""
+    radius = 0.5 * diameter
+    n = int(np.floor(radius / dp))
+    pts = []
+    for j in range(-n, n + 1):
+        for i in range(-n, n + 1):
+            ox, oy = i * dp, j * dp
+            if np.sqrt(ox * ox + oy * oy) <= radius:
+                pts.append((center[0] + ox, center[1] + oy))
+    return np.array(pts, dtype=np.float64)
+
+
+def nearest_particle(r0, target):
+    """cases.cpp:146-158: the first particle at the smallest |r0 - target|."""
+    d = r0 - np.asarray(target[: r0.shape[1]])
+    dist = np.sqrt(np.sum(d * d, axis=1)) if r0.shape[1] == 2 else np.sqrt((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
+    return int(np.argmin(dist))
+
+
+def case_setup(name, resolution=0):
+    """build_case (cases.cpp:160-231) plus the damping the runner derives from the config
+    (runner.cpp:146-168: eta from beta = artificial_viscosity, alpha 0.2, seed 0, particle split)."""
+    spec = case_spec(name, resolution)
+    dp, dim = spec["dp"], spec["dim"]
+    mat = material(spec["E"], spec["nu"], spec["rho0"], spec["model"])
+    if dim == 3:
+        half = 0.5 * spec["thickness"]
+        r0 = box_lattice([-CLAMP_LAYERS * dp, -half, -half], [spec["length"], half, half], dp)
+        cons = (r0[:, 0] < 0.0).astype(np.uint8)
+        body = np.tile([0.0, -spec["gravity"], 0.0], (len(r0), 1))
+        if spec["rotational"]:  # rotational_body_force, cases.cpp:66-70,180-186
+            # libm sin per particle (math.sin), as std::sin in the reference
+            gamma = np.array([(20.0 * GRAVITY_CASES / spec["thickness"]) * math.sin(math.pi * x / (2.0 * spec["length"]))
+                              for x in r0[:, 0]])
+            body = np.stack([np.zeros(len(r0)), r0[:, 1] * gamma, r0[:, 2] * gamma], axis=1)
+            body[cons == 1] = 0.0
+        contact = None
+    else:
+        center = (0.0, spec["clearance"] + 0.5 * spec["diameter"])
+        r0 = disk(center, spec["diameter"], dp)
+        cons = np.zeros(len(r0), dtype=np.uint8)
+        body = np.tile([0.0, -spec["gravity"]], (len(r0), 1))
+        k = spec["contact_stiffness"] if spec["contact_stiffness"] > 0 else mat["K"]
+        contact = ((0.0, 0.0), (0.0, 1.0), k)
+    probe = nearest_particle(r0, spec["probe_target"] if dim == 3 else (0.0, spec["clearance"] + 0.5 * spec["diameter"]))
+    eta = artificial_viscosity(spec["beta"], spec["rho0"], spec["E"], spec["L"]) if spec["beta"] > 0 else 0.0
+    return dict(spec=spec, r0=r0, V0=dp ** dim, rho0=spec["rho0"], h=1.3 * dp, constrained=cons, body=body,
+                material=mat, contact=contact, probe=probe, eta=eta, alpha=0.2, seed=0)
+
+
+def run_case(name, resolution=0, end_time=None, interval=None, threads=1):
+    """The oracle's tlsph_sim_run: case_setup, runner.cpp:299-313 initialisation, the loop of
+    :341-391 with the probe series; returns (probe samples, loop result)."""
+    c = case_setup(name, resolution)
+    spec = c["spec"]
+    o = OracleSystem(c["r0"], c["V0"], c["rho0"], c["h"], constrained=c["constrained"])
+    o.set_material(spec["E"], spec["nu"], spec["rho0"], spec["model"])
+    o.set("body", c["body"])
+    if c["contact"] is not None:
+        o.set_contact(*c["contact"])
+    o.prepare(threads=threads)
+    end = spec["end_time"] if end_time is None else end_time
+    r = o.run(eta=c["eta"], alpha=c["alpha"], seed=c["seed"], steps=1 << 62, end_time=end, threads=threads,
+              probe=c["probe"], interval=spec["interval"] if interval is None else interval)
+    return r["probe"], r, o
+
+
+def probe_csv(samples, dim):
+    """write_probe_csv (runner.cpp:422-439): header, then t,u... as %.17g, LF line ends."""
+    lines = ["t,ux,uy" if dim == 2 else "t,ux,uy,uz"]
+    for row in samples:
+        lines.append(",".join("%.17g" % x for x in row[: 1 + dim]))
+    return "\n".join(lines) + "\n"
 
 
 # ---- stateless helpers

@@ -395,7 +395,11 @@ long long orc_box_lattice(int dim, const double* lo, const double* hi, double dp
 //         [6]=end_time (<=0: unbounded) [7]=elastic (1: verlet_step each step; 0: damping only)
 //         [8]=seed [9]=threads
 // out: [0]=steps [1]=damped [2]=t [3]=elastic_s [4]=damping_s [5]=total_s [6]=last_dt
-int orc_run(void* hv, const double* params, double* out) {
+// params[11]: probe particle (-1: none), params[12]: output interval; probe samples (t, u_0..u_2)
+// as runner.cpp:328,378-383,393-395 records them: the initial one, one at each output mark, the
+// end state if it is later than the last mark.
+int orc_run_probed(void* hv, const double* params, double* out, double* samples, long long capacity,
+                   long long* nsamples) {
   return guarded([&] {
     with_sim(hv, [&](auto& s) {
       const auto t0 = Clock::now();
@@ -415,6 +419,19 @@ int orc_run(void* hv, const double* params, double* out) {
         s.loop_steps = s.loop_damped = 0;
       }
       orc::RandomSource& rng = *s.loop_rng;
+      constexpr int DD = std::remove_reference_t<decltype(s)>::dim;
+      const long long probe = params[11] >= 0.0 ? static_cast<long long>(params[11]) : -1;
+      const double interval = params[12];
+      long long ns = 0;
+      auto record = [&](double tt) {
+        if (probe < 0 || !samples || ns >= capacity) return;
+        double* o = samples + 4 * ns++;
+        o[0] = tt;
+        o[1] = o[2] = o[3] = 0.0;
+        for (int d = 0; d < DD; ++d) o[1 + d] = s.sys.r[static_cast<std::size_t>(probe)][d] - s.sys.r0[static_cast<std::size_t>(probe)][d];
+      };
+      if (!resume) record(0.0);
+      double next_mark = interval > 0.0 ? interval : 0.0;
       const bool damping_active = eta > 0.0;
       orc::ViscousBounds vb{};
       if (damping_active) vb = orc::viscous_dt_bounds(h, eta / (alpha * s.mat.rho0), std::remove_reference_t<decltype(s)>::dim);
@@ -453,7 +470,13 @@ int orc_run(void* hv, const double* params, double* out) {
         t += dt;
         ++steps;
         orc::check_finite(s.sys, static_cast<std::uint64_t>(steps));
+        if (probe >= 0 && interval > 0.0 && t >= next_mark - 1e-12 * end_time) {
+          record(t);
+          while (next_mark <= t + 1e-12 * end_time) next_mark += interval;
+        }
       }
+      if (probe >= 0 && (ns == 0 || samples[4 * (ns - 1)] < t)) record(t);
+      if (nsamples) *nsamples = ns;
       s.loop_t = t;
       s.loop_steps = steps;
       s.loop_damped = damped;
@@ -464,6 +487,29 @@ int orc_run(void* hv, const double* params, double* out) {
       out[4] = dm;
       out[5] = since(t0);
       out[6] = last_dt;
+    });
+  });
+}
+
+int orc_run(void* hv, const double* params, double* out) {
+  double p[13];
+  for (int k = 0; k < 11; ++k) p[k] = params[k];
+  p[11] = -1.0;
+  p[12] = 0.0;
+  return orc_run_probed(hv, p, out, nullptr, 0, nullptr);
+}
+
+// ExternalAccel's contact plane (forces.hpp:13-24); stiffness <= 0 removes it.
+int orc_set_contact(void* hv, const double* point, const double* normal, double stiffness) {
+  return guarded([&] {
+    with_sim(hv, [&](auto& s) {
+      constexpr int DD = std::remove_reference_t<decltype(s)>::dim;
+      s.ext.contact = stiffness > 0.0;
+      s.ext.cp_k = stiffness;
+      for (int d = 0; d < DD; ++d) {
+        s.ext.cp_point[d] = point[d];
+        s.ext.cp_normal[d] = normal[d];
+      }
     });
   });
 }

@@ -704,11 +704,25 @@ inline void update_density(ParticleSystem<D>& sys, int threads) {
             "inverted element: det(F) <= 0 for particle " + std::to_string(i));
 }
 
-// reference: forces.hpp:34-38 (body term only; the contact plane is out of scope)
+// reference: forces.hpp:13-39 -- the per-particle body term plus the optional penalty contact
+// plane of the falling-ball case, evaluated at the current position:
+// gap = (r - point).normal; gap < 0 adds (stiffness * (-gap) / m) * normal.
 template <int D>
 struct ExternalAccel {
   std::vector<Vec<D>> body;  // empty = zero
-  Vec<D> eval(std::size_t i) const { return body.empty() ? Vec<D>::zero() : body[i]; }
+  bool contact = false;
+  Vec<D> cp_point = Vec<D>::zero(), cp_normal = Vec<D>::zero();
+  double cp_k = 0.0;
+  Vec<D> eval(std::size_t i, const Vec<D>& r, double m) const {
+    Vec<D> acc = body.empty() ? Vec<D>::zero() : body[i];
+    if (!contact) return acc;
+    double gap = (r[0] - cp_point[0]) * cp_normal[0];
+    for (int d = 1; d < D; ++d) gap = gap + (r[d] - cp_point[d]) * cp_normal[d];
+    if (gap >= 0.0) return acc;
+    const double k = cp_k * (-gap) / m;
+    for (int d = 0; d < D; ++d) acc[d] = acc[d] + k * cp_normal[d];
+    return acc;
+  }
 };
 
 // reference: integrator.cpp:80-116
@@ -742,7 +756,7 @@ inline void compute_momentum_rhs(ParticleSystem<D>& sys, const Neighborhood<D>& 
           acc[r] = acc[r] + t;
         }
       }
-      const Vec<D> g = ext.eval(i);
+      const Vec<D> g = ext.eval(i, sys.r[i], sys.m[i]);
       for (int d = 0; d < D; ++d) sys.a[i][d] = acc[d] / sys.m[i] + g[d];
     }
   });
