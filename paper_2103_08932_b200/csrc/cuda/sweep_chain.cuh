@@ -5,9 +5,12 @@
 //
 // Lane l owns slots l, l+32, ... (K per lane) of the current particle for all
 // D velocity components. Reassociated update (FAST tolerance class): with
-// Y = (1 + bm) v_j - bm v_i and C = -bm (diag + b),
+// w = v_j - v_i, Y = v_j + bm w and C = -bm (diag + b),
 //   v_j' = v_j - bm (v_i + diag rate - (v_j - b rate)) = Y + C rate,
-// so one FMA per slot follows the residual reduction on the chain.
+// so one FMA per slot follows the residual reduction on the chain. Y is formed from w (not as
+// (1 + bm) v_j - bm v_i): a uniform velocity field (w = 0, rate = 0) is left exactly unchanged, as
+// in the reference's order -- the sweep amplifies any non-uniformity when eta~ dt is large (the
+// falling-ball case), so FAST must not create one.
 //
 // Software pipeline. Everything but the stencil velocities is static during
 // the chain, so the slot metadata of the next particle is loaded while the
@@ -118,7 +121,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
   // current particle: coefficients
   int pk = pidx(0);
   int jq[K];
-  double bq[K], bmq[K], c1[K], cq[K];
+  double bq[K], bmq[K], cq[K];
   unsigned upm;
   bool skip;
   double diag, y;
@@ -143,7 +146,6 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       jq[u] = j;
       bq[u] = v ? t.kb * t.pf[lo + s] : 0.0;
       bmq[u] = t.kb * q;
-      c1[u] = 1.0 + bmq[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
       upm |= up ? (1u << u) : 0u;
     }
@@ -182,15 +184,19 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
 
     double P[D], Y[K][D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      P[d] = bq[0] * (vq[0][d] - vi[d]);
+    for (int u = 0; u < K; ++u)
 #pragma unroll
-      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], vq[u][d] - vi[d], P[d]);
+      for (int d = 0; d < D; ++d) Y[u][d] = vq[u][d] - vi[d];  // w = v_j - v_i
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      P[d] = bq[0] * Y[0][d];
+#pragma unroll
+      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], Y[u][d], P[d]);
     }
 #pragma unroll
     for (int u = 0; u < K; ++u)
 #pragma unroll
-      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(c1[u], vq[u][d], -bmq[u] * vi[d]);
+      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(bmq[u], Y[u][d], vq[u][d]);  // v_j + bm w
     if (SHUF) chain_sum<D>(P, lane);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -223,7 +229,6 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       jq[u] = jn[u];
       bq[u] = t.kb * pfn[u];
       bmq[u] = t.kb * qfn[u];
-      c1[u] = 1.0 + bmq[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
       upm |= up ? (1u << u) : 0u;
     }
@@ -279,7 +284,7 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
   };
 
   int jq[K];
-  double bq[K], bmq[K], c1[K], cq[K];
+  double bq[K], bmq[K], cq[K];
   unsigned upm;
   bool skip;
   double diag, y;
@@ -291,7 +296,6 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
       jq[u] = UNI ? (j[u] & 0x7fff) : j[u];
       bq[u] = t.kb * pf[u];
       bmq[u] = t.kb * q[u];
-      c1[u] = 1.0 + bmq[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
       upm |= q[u] != 0.0 ? (1u << u) : 0u;
     }
@@ -341,15 +345,19 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
 
     double P[D], Y[K][D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      P[d] = bq[0] * (vq[0][d] - vi[d]);
+    for (int u = 0; u < K; ++u)
 #pragma unroll
-      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], vq[u][d] - vi[d], P[d]);
+      for (int d = 0; d < D; ++d) Y[u][d] = vq[u][d] - vi[d];  // w = v_j - v_i
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      P[d] = bq[0] * Y[0][d];
+#pragma unroll
+      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], Y[u][d], P[d]);
     }
 #pragma unroll
     for (int u = 0; u < K; ++u)
 #pragma unroll
-      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(c1[u], vq[u][d], -bmq[u] * vi[d]);
+      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(bmq[u], Y[u][d], vq[u][d]);  // v_j + bm w
     chain_sum<D>(P, lane);
     double qfn[K];
     mass_factors(jn, pfn, qfn);  // particle kk+1 (loaded an iteration ago)

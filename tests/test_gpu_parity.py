@@ -628,3 +628,20 @@ def test_large_body_loop_matches_oracle(mode):
     assert r["steps"] == ro["steps"] == 6 and r["damped"] == ro["damped"] > 0
     for name in ("v", "r"):
         assert rel_l2(d.get(name), o.get(name)) <= TOL, name
+
+
+@pytest.mark.parametrize("mode", ["fast", "ordered"])
+@pytest.mark.parametrize("tiling", ["staged", "streamed"])
+def test_uniform_field_is_exactly_invariant_under_a_stiff_sweep(mode, tiling):
+    """tests/test_damping.cpp:336-346 (uniform-field invariance), at the falling-ball's eta~ dt where
+    the split sweep amplifies any non-uniformity by ~1e20 per sweep: both modes must leave a uniform
+    field bit-for-bit unchanged (FAST forms v_j + bm (v_j - v_i), not (1 + bm) v_j - bm v_i)."""
+    c = O.case_setup("falling_ball")
+    n = len(c["r0"])
+    v = np.tile([0.0, -0.0037], (n, 1))
+    d = dev.DeviceSystem(c["r0"], c["V0"], c["rho0"], c["h"], constrained=np.zeros(n, np.uint8))
+    d.set_reduction(mode)
+    d.set_sweep_tiling(tiling)
+    d.set("v", v)
+    d.damping_sweep("particle_split", 27950.0, 3.8e-4, count=3)
+    assert np.array_equal(d.get("v"), v)
