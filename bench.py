@@ -14,8 +14,9 @@ untimed warm-up steps of the same run); the reference arm times the same window.
 Keys of the line:
   value      PS/s from CUDA events on the library's stream around the K steps (inputs resident);
   e2e        the same metric through the reference's C++ operator API (stable_dt / verlet_step /
-             strang_damping_sweep<3> on a host ParticleSystem<3>, fields moved every call from and
-             into pageable host vectors; lib/tlsph-operator-loop);
+             strang_damping_sweep<3> on a host ParticleSystem<3> whose storage the caller page-locks
+             once (tlsph::pin_host_memory); every call moves the fields the reference operator reads
+             host -> device and the ones it writes device -> host; lib/tlsph-operator-loop);
   roofline   the TL-SPH step kernels (k_step_begin + passes A-C + current-cell rebuild) against
              the measured HBM copy bandwidth on BASELINE.md §4's algorithmic byte model;
   cpu_baseline / parity   the oracle (reference arithmetic, OpenMP on every host core) over the
@@ -256,9 +257,11 @@ def headline_cfg4(args):
         "dtype": "f64", "data": "synthetic (seeded jittered lattice, BASELINE.md §3)",
         "config": cfg4_config(n, slots, K, W),
         "mode": {"reduction": "fast (lane-parallel sums; <= 1e-10 of the reference order)",
-                 "resort": "current-cell list rebuilt every step inside the loop's graph"},
+                 "resort": ("per-step current-position cell binning (keys, counting sort, in-cell order) inside "
+                            "the loop's graph, its time included; not a storage permutation: the CSR, colouring "
+                            "and sweep order are r0-based (SURVEY.md §7 item 7), storage keeps r0-cell order")},
         "damped_steps": damped, "elastic_ms_per_step": t_el * 1e3, "damping_ms_per_damped_step": t_dm * 1e3,
-        "roofline": {"bound": "hbm", "kernel": "TL-SPH step: k_step_begin + passes A, B, C (+ current-cell rebuild)",
+        "roofline": {"bound": "hbm", "kernel": "TL-SPH step: k_step_begin + passes A, B, C (+ current-cell binning)",
                      "achieved": b_el / t_el / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": b_el / t_el / 1e9 / peak, "bytes_per_launch": b_el, "avg_launch_s": t_el,
                      "traffic": traffic.get("dram_bytes_per_step") if traffic else None,
@@ -347,7 +350,8 @@ def leg_cfg2(args):
     try:
         e = operator_loop("sweep", max(50, args.steps), 3)
         out["e2e"] = {"value": e["value"], "unit": "DPU/s", "h2d_bytes_per_step": e["h2d_bytes_per_step"],
-                      "d2h_bytes_per_step": e["d2h_bytes_per_step"], "path": e["api"], "steps": e["steps"]}
+                      "d2h_bytes_per_step": e["d2h_bytes_per_step"], "path": e["api"], "steps": e["steps"],
+                      "host_memory": e.get("host_memory")}
     except Exception as exc:  # reported, never silently replaced
         out["e2e"] = {"error": str(exc)}
     return out
@@ -603,6 +607,7 @@ def main():
                     e = operator_loop("loop", args.steps, args.warmup)
                     out["e2e"] = {"value": e["value"], "unit": "PS/s", "h2d_bytes_per_step": e["h2d_bytes_per_step"],
                                   "d2h_bytes_per_step": e["d2h_bytes_per_step"], "path": e["api"],
+                                  "host_memory": e.get("host_memory"),
                                   "window": f"steps {args.warmup}..{args.warmup + args.steps - 1}",
                                   "damped_steps": e["damped_steps"]}
                 except Exception as exc:

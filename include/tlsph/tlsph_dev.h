@@ -224,6 +224,10 @@ tlsph_status tlsph_dev_take(const tlsph_dev* dev, tlsph_dev_field field, void* h
 /* Cumulative bytes moved between host memory and the device by the field
  * transfers of all handles of this process (set/get_field, put/refresh/take). */
 void tlsph_dev_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+/* Page-locks (cudaHostRegister) a caller-owned host range so field transfers from and into it run
+ * as direct DMA; idempotent per range. Unregister before the memory is freed. */
+tlsph_status tlsph_dev_host_register(void* host, size_t bytes);
+tlsph_status tlsph_dev_host_unregister(void* host);
 
 
 /* Per-step re-sort (BASELINE cfg4): with `on`, every step of tlsph_dev_run

@@ -8,8 +8,10 @@
 // device -> host, inside the timed region; the neighbourhood stays resident on the device
 // (csrc/host/resident.hpp).
 //
-//   tlsph-operator-loop sweep <steps> <warmup> [fast|ordered]   cfg2: strang_damping_sweep<3>
-//   tlsph-operator-loop loop  <steps> <warmup> [fast|ordered]   cfg4: the runner loop
+//   tlsph-operator-loop sweep <steps> <warmup> [fast|ordered] [pinned|pageable]   cfg2: strang_damping_sweep<3>
+//   tlsph-operator-loop loop  <steps> <warmup> [fast|ordered] [pinned|pageable]   cfg4: the runner loop
+// pinned (default): the caller page-locks its ParticleSystem once (tlsph::pin_host_memory) before
+// the loop, as a GPU-aware caller does; pageable: plain std::vector storage (staging ring).
 //
 // Inputs follow BASELINE.md §3 (generate_box_lattice, RandomSource streams). Prints one JSON line.
 #include <chrono>
@@ -35,6 +37,8 @@ using Clock = std::chrono::steady_clock;
 namespace {
 
 constexpr double kRho0 = 1000.0, kE = 2.0e6, kNu = 0.3, kGravity = 9.81;
+
+bool g_pinned = true;  // the caller page-locks its ParticleSystem (tlsph/device.hpp); "pageable" arg: off
 
 double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
 
@@ -83,6 +87,7 @@ int sweep_bench(int steps, int warmup) {
   const auto nbh = build_reference_neighborhoods<3>(std::span<const Vec3>(sys.r0), std::span<const double>(sys.V0),
                                                     kernel, grid);
   const double init_s = since(t_init);
+  if (g_pinned) pin_host_memory<3>(sys);
   for (int k = 0; k < warmup; ++k)
     strang_damping_sweep<3>(sys, nbh, grid, blocks, DampingScheme::ParticleSplit, eta, dt, 1);
   const Bytes b0 = Bytes::now();
@@ -91,12 +96,13 @@ int sweep_bench(int steps, int warmup) {
     strang_damping_sweep<3>(sys, nbh, grid, blocks, DampingScheme::ParticleSplit, eta, dt, 1);
   const double secs = since(t0);
   const Bytes b1 = Bytes::now();
+  if (g_pinned) unpin_host_memory<3>(sys);
   std::int64_t s_free = nbh.offsets.back();
   const double dpu = 2.0 * static_cast<double>(s_free) * steps;
   std::printf("{\"workload\": \"cfg2\", \"api\": \"tlsph::strang_damping_sweep<3> on a host ParticleSystem<3>\", "
               "\"particles\": %zu, \"slots\": %lld, \"steps\": %d, \"warmup\": %d, \"seconds\": %.9g, "
               "\"value\": %.9g, \"unit\": \"DPU/s\", \"h2d_bytes_per_step\": %llu, \"d2h_bytes_per_step\": %llu, "
-              "\"init_seconds\": %.6g, \"var_v\": %.17g}\n",
+              "\"init_seconds\": %.6g, \"var_v\": %.17g, \"host_memory\": \"%s\"}\n",
               n, static_cast<long long>(s_free), steps, warmup, secs, dpu / secs,
               static_cast<unsigned long long>((b1.h2d - b0.h2d) / std::max(steps, 1)),
               static_cast<unsigned long long>((b1.d2h - b0.d2h) / std::max(steps, 1)), init_s,
@@ -108,7 +114,8 @@ int sweep_bench(int steps, int warmup) {
                 for (auto& x : sys.v)
                   for (int d = 0; d < 3; ++d) q += (x[d] - m) * (x[d] - m);
                 return q / (3.0 * n);
-              }());
+              }(),
+              g_pinned ? "pinned" : "pageable");
   return 0;
 }
 
@@ -150,6 +157,7 @@ int loop_bench(int steps, int warmup) {
   const double init_s = since(t_init);
   RandomSource rng(damping.seed);
   const ViscousBounds viscous = viscous_dt_bounds(h, damping.nu_kin_applied(kRho0), 3);
+  if (g_pinned) pin_host_memory<3>(sys, &ext.body);
 
   std::uint64_t step = 0, damped = 0, damped_timed = 0;
   double t = 0.0;
@@ -177,17 +185,19 @@ int loop_bench(int steps, int warmup) {
   for (int k = 0; k < steps; ++k) damped_timed += one_step() ? 1 : 0;
   const double secs = since(t0);
   const Bytes b1 = Bytes::now();
+  if (g_pinned) unpin_host_memory<3>(sys, &ext.body);
   double disp = 0.0;
   for (std::size_t i = 0; i < n; ++i) disp += (sys.r[i] - sys.r0[i]).squaredNorm();
   std::printf("{\"workload\": \"cfg4\", \"api\": \"runner.cpp:341-391 loop over tlsph::stable_dt / verlet_step / "
               "strang_damping_sweep<3> on a host ParticleSystem<3>\", \"particles\": %zu, \"slots\": %lld, "
               "\"steps\": %d, \"warmup\": %d, \"damped_steps\": %llu, \"seconds\": %.9g, \"value\": %.9g, "
               "\"unit\": \"PS/s\", \"h2d_bytes_per_step\": %llu, \"d2h_bytes_per_step\": %llu, "
-              "\"init_seconds\": %.6g, \"t\": %.17g, \"displacement_l2\": %.17g}\n",
+              "\"init_seconds\": %.6g, \"t\": %.17g, \"displacement_l2\": %.17g, \"host_memory\": \"%s\"}\n",
               n, static_cast<long long>(nbh.offsets.back()), steps, warmup,
               static_cast<unsigned long long>(damped_timed), secs, static_cast<double>(n) * steps / secs,
               static_cast<unsigned long long>((b1.h2d - b0.h2d) / std::max(steps, 1)),
-              static_cast<unsigned long long>((b1.d2h - b0.d2h) / std::max(steps, 1)), init_s, t, std::sqrt(disp));
+              static_cast<unsigned long long>((b1.d2h - b0.d2h) / std::max(steps, 1)), init_s, t, std::sqrt(disp),
+              g_pinned ? "pinned" : "pageable");
   return 0;
 }
 
@@ -201,6 +211,7 @@ int main(int argc, char** argv) {
   const std::string what = argv[1];
   const int steps = std::atoi(argv[2]), warmup = std::atoi(argv[3]);
   const std::string mode = argc > 4 ? argv[4] : "fast";
+  g_pinned = !(argc > 5 && std::string(argv[5]) == "pageable");
   set_operator_reduction(mode == "ordered" ? Reduction::Ordered : Reduction::Fast);
   try {
     if (what == "sweep") return sweep_bench(steps, warmup);

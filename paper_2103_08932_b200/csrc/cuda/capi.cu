@@ -362,6 +362,30 @@ tlsph_status tlsph_dev_refresh(tlsph_dev* dev, tlsph_dev_field field, const void
   return guarded([&] { sys(dev).put_record(field, host, layout, true, changed); });
 }
 
+tlsph_status tlsph_dev_host_register(void* host, size_t bytes) {
+  return guarded([&] {
+    if (!host || bytes == 0) return;
+    const cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+      return;
+    }
+    CK(e);
+  });
+}
+
+tlsph_status tlsph_dev_host_unregister(void* host) {
+  return guarded([&] {
+    if (!host) return;
+    const cudaError_t e = cudaHostUnregister(host);
+    if (e == cudaErrorHostMemoryNotRegistered) {
+      cudaGetLastError();
+      return;
+    }
+    CK(e);
+  });
+}
+
 void tlsph_dev_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
   if (h2d) *h2d = tlsph_cuda::g_h2d_bytes.load();
   if (d2h) *d2h = tlsph_cuda::g_d2h_bytes.load();

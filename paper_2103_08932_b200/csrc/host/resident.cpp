@@ -20,6 +20,44 @@ void set_operator_reduction(Reduction mode) { g_reduction.store(static_cast<int>
 Reduction operator_reduction() { return static_cast<Reduction>(g_reduction.load()); }
 void release_device_state() { host::release_resident(); }
 
+namespace {
+template <typename V>
+void pin_vector(V& v, bool on) {
+  if (v.empty()) return;
+  if (on) host::check(tlsph_dev_host_register(v.data(), v.size() * sizeof(v[0])));
+  else host::check(tlsph_dev_host_unregister(v.data()));
+}
+template <int D>
+void pin_all(ParticleSystem<D>& s, std::vector<Vec<D>>* body, bool on) {
+  pin_vector(s.r0, on);
+  pin_vector(s.r, on);
+  pin_vector(s.v, on);
+  pin_vector(s.a, on);
+  pin_vector(s.F, on);
+  pin_vector(s.dFdt, on);
+  pin_vector(s.B0, on);
+  pin_vector(s.V0, on);
+  pin_vector(s.m, on);
+  pin_vector(s.rho0, on);
+  pin_vector(s.rho, on);
+  pin_vector(s.constrained, on);
+  if (body) pin_vector(*body, on);
+}
+}  // namespace
+
+template <int D>
+void pin_host_memory(ParticleSystem<D>& system, std::vector<Vec<D>>* body) {
+  pin_all<D>(system, body, true);
+}
+template <int D>
+void unpin_host_memory(ParticleSystem<D>& system, std::vector<Vec<D>>* body) {
+  pin_all<D>(system, body, false);
+}
+template void pin_host_memory<2>(ParticleSystem<2>&, std::vector<Vec<2>>*);
+template void pin_host_memory<3>(ParticleSystem<3>&, std::vector<Vec<3>>*);
+template void unpin_host_memory<2>(ParticleSystem<2>&, std::vector<Vec<2>>*);
+template void unpin_host_memory<3>(ParticleSystem<3>&, std::vector<Vec<3>>*);
+
 namespace host {
 
 static_assert(sizeof(Vec<3>) == 3 * sizeof(double) && sizeof(Mat<3>) == 9 * sizeof(double),
