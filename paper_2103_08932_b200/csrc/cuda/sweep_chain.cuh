@@ -22,6 +22,19 @@
 // diagonal) or one without neighbours (damping.cpp:54, :151) runs the same
 // code with its writes disabled, so the loop has no data-dependent branch.
 #pragma once
+// Y of the FAST update (see below): v_j + bm (v_j - v_i) (default), or the former
+// (1 + bm) v_j - bm v_i (TLSPH_Y_FORM=2: not exact for uniform fields; A/B only)
+// streamed chain: Y formed at the scatter (1) or before the reduction (0)
+#ifndef TLSPH_Y_LATE
+#define TLSPH_Y_LATE 1
+#endif
+#if defined(TLSPH_Y_FORM) && TLSPH_Y_FORM == 2
+#define TLSPH_Y(u, d) __fma_rn(1.0 + bmq[u], vq[u][d], -bmq[u] * vi[d])
+#elif defined(TLSPH_Y_FORM) && TLSPH_Y_FORM == 3
+#define TLSPH_Y(u, d) __dadd_rn(vq[u][d], __dmul_rn(bmq[u], vq[u][d] - vi[d]))
+#else
+#define TLSPH_Y(u, d) __fma_rn(bmq[u], vq[u][d] - vi[d], vq[u][d])
+#endif
 #include <cstdint>
 
 namespace tlsph_cuda {
@@ -184,19 +197,15 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
 
     double P[D], Y[K][D];
 #pragma unroll
-    for (int u = 0; u < K; ++u)
-#pragma unroll
-      for (int d = 0; d < D; ++d) Y[u][d] = vq[u][d] - vi[d];  // w = v_j - v_i
-#pragma unroll
     for (int d = 0; d < D; ++d) {
-      P[d] = bq[0] * Y[0][d];
+      P[d] = bq[0] * (vq[0][d] - vi[d]);
 #pragma unroll
-      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], Y[u][d], P[d]);
+      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], vq[u][d] - vi[d], P[d]);
     }
 #pragma unroll
     for (int u = 0; u < K; ++u)
 #pragma unroll
-      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(bmq[u], Y[u][d], vq[u][d]);  // v_j + bm w
+      for (int d = 0; d < D; ++d) Y[u][d] = TLSPH_Y(u, d);  // v_j + bm (v_j - v_i)
     if (SHUF) chain_sum<D>(P, lane);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -343,21 +352,20 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
       for (int d = 0; d < D; ++d) vq[u][d] = t.sv[d][jq[u]];
     const double diag1 = t.diag[pk1], y1 = t.y[pk1];
 
-    double P[D], Y[K][D];
-#pragma unroll
-    for (int u = 0; u < K; ++u)
-#pragma unroll
-      for (int d = 0; d < D; ++d) Y[u][d] = vq[u][d] - vi[d];  // w = v_j - v_i
+    double P[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      P[d] = bq[0] * Y[0][d];
+      P[d] = bq[0] * (vq[0][d] - vi[d]);
 #pragma unroll
-      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], Y[u][d], P[d]);
+      for (int u = 1; u < K; ++u) P[d] = __fma_rn(bq[u], vq[u][d] - vi[d], P[d]);
     }
+#if !TLSPH_Y_LATE
+    double Y[K][D];
 #pragma unroll
     for (int u = 0; u < K; ++u)
 #pragma unroll
-      for (int d = 0; d < D; ++d) Y[u][d] = __fma_rn(bmq[u], Y[u][d], vq[u][d]);  // v_j + bm w
+      for (int d = 0; d < D; ++d) Y[u][d] = TLSPH_Y(u, d);  // v_j + bm (v_j - v_i)
+#endif
     chain_sum<D>(P, lane);
     double qfn[K];
     mass_factors(jn, pfn, qfn);  // particle kk+1 (loaded an iteration ago)
@@ -366,7 +374,11 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
       const double rate = P[d] * y;
 #pragma unroll
       for (int u = 0; u < K; ++u)
+#if TLSPH_Y_LATE
+        if (upm & (1u << u)) t.sv[d][jq[u]] = __fma_rn(cq[u], rate, TLSPH_Y(u, d));
+#else
         if (upm & (1u << u)) t.sv[d][jq[u]] = __fma_rn(cq[u], rate, Y[u][d]);
+#endif
       // i is not its own neighbour, so this store cannot race the scatter above
       if (lane == 0 && !skip) t.sv[d][li] = __fma_rn(diag, rate, vi[d]);
     }
