@@ -452,7 +452,6 @@ def sharded_cfg5(args, ws, rank):
     layers, dp = args.scale_layers, 0.004
     h = 1.3 * dp
     grid, ranges, part, r0 = slabs.lattice_slab([0.0, 0.0, 0.0], [layers * ws * dp, 1.0, 1.0], dp, h, ws, rank)
-    parts = [slabs.Slab(r, x0, x1, None) for r, (x0, x1) in enumerate(ranges)]
     cons = (r0[:, 0] < 5 * dp).astype(np.uint8)
     d = dev.DeviceSystem(r0, dp ** 3, S.RHO0, h, cons, grid=grid[:2])
     d.set_task_range(part.x0, part.x1)
@@ -464,36 +463,34 @@ def sharded_cfg5(args, ws, rank):
     s_free_local = int(rows[own & (cons == 0)].sum())
     slots_local = int(rows[own].sum())
     gloo = dist.new_group(backend="gloo")
-    sweep = slabs.IpcSlabSweep(d, rank, ws, group=gloo)
     mat = S.material()
     g = np.zeros((d.n, 3))
     g[:, 1] = -S.GRAVITY
     d.set("body", g)
     d.prepare(mat)
-    group = slabs.IpcGroup(slabs.DeviceSlabEngine(d, 3), [(p.x0, p.x1) for p in parts], rank, sweep)
+    # the C entry point: tlsph_dev_group_* (csrc/cuda/group.cu) over a gloo communicator
+    group = slabs.CGroup(d, slabs.TorchComm(gloo))
     W, K = args.warmup, args.steps
-    spec_w = slabs.LoopSpec(mat, h, S.eta_for(h), 0.2, W, seed=0)
+    kw = dict(h=h, eta=S.eta_for(h), alpha=0.2, seed=0)
     if W > 0:
-        slabs.run_loop(group, spec_w, 3, sweeper=lambda scheme, et, dt_: sweep.sweep(scheme, et, dt_))
+        group.run(mat, steps=W, **kw)
     dist.barrier(group=gloo)
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        d.timer_start()
-        spec = slabs.LoopSpec(mat, h, S.eta_for(h), 0.2, K, seed=0)
-        res = slabs.run_loop(group, spec, 3, sweeper=lambda scheme, et, dt_: sweep.sweep(scheme, et, dt_))
-        t_loop = barrier_and_max(d.timer_stop(), ws)
+        res = group.run(mat, steps=K, **kw)
+        t_loop = barrier_and_max(res["device_s"], ws)
     tot = [None] * ws
     dist.all_gather_object(tot, (s_free_local, int(own.sum()), slots_local), group=gloo)
     n_owned = sum(x[1] for x in tot)
     slots = sum(x[2] for x in tot)
     eta_t, dt = S.eta_for(h) / 0.2, 1e-5
+    nsw = max(3, min(args.scale_sweeps, 50))
     dist.barrier(group=gloo)
     d.timer_start()
-    sweep.sweep("particle_split", eta_t, dt, count=max(3, min(args.scale_sweeps, 50)))
+    group.sweep("particle_split", eta_t, dt, count=nsw)
     t_sw = barrier_and_max(d.timer_stop(), ws)
-    sweep.close()
+    group.close()
     peak, peak_src = load_peaks()
     s_free = sum(x[0] for x in tot)
-    nsw = max(3, min(args.scale_sweeps, 50))
     b_step = step_bytes(n_owned, slots) / ws
     return {"metric": METRIC_PS, "value": n_owned * res["steps"] / t_loop, "unit": "PS/s", "n_gpus": ws,
             "steps": K, "warmup": W, "ms_per_step": t_loop / K * 1e3, "higher_is_better": True, "scaling": "weak",
@@ -501,7 +498,8 @@ def sharded_cfg5(args, ws, rank):
             "config": {"workload": f"cfg5 weak scaling: {layers * ws} x 250 x 250 lattice (dp 0.004), {ws} x-slabs, "
                                    "one per GPU, alpha 0.2", "particles": n_owned, "slots": slots,
                        "parallelism": f"x-slabs x{ws}",
-                       "exchange": "fused: CUDA IPC peer stores of shared columns + IPC phase events"},
+                       "exchange": "fused: CUDA IPC peer stores of shared columns + IPC phase events",
+                       "driver": "C ABI tlsph_dev_group_run / tlsph_dev_group_sweep (csrc/cuda/group.cu)"},
             "roofline": {"bound": "hbm", "kernel": "whole step per GPU (elastic + damping share)",
                          "achieved": b_step / (t_loop / K) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": b_step / (t_loop / K) / 1e9 / peak, "peak_source": peak_src},

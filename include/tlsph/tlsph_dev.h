@@ -374,6 +374,49 @@ typedef struct tlsph_dev_loop_result {
  * runner.cpp:306-312 does before its loop. */
 tlsph_status tlsph_dev_run(tlsph_dev* dev, const tlsph_dev_loop_params* params, tlsph_dev_loop_result* result);
 
+/* ---- x-slab groups across processes (one process per GPU; csrc/cuda/group.cu) ----
+ * A body decomposed along x over the GLOBAL cell grid: each process creates its slab with
+ * tlsph_dev_create_in_grid (the particles of its columns [x0 - 1, x1 + 1), ascending reference id)
+ * and tlsph_dev_set_task_range(x0, x1), prepares it (runner.cpp:306-312) and joins a group. The
+ * group links every slab to its x neighbours through CUDA IPC (colour-phase and halo stores go
+ * straight into the neighbour's arrays; the barriers are stream waits on IPC events) and combines
+ * the step scalars through the caller's communicator, so the owned particles follow the
+ * undivided body's device loop bit for bit. */
+typedef enum tlsph_group_op { TLSPH_GROUP_MAX = 0, TLSPH_GROUP_SUM = 1 } tlsph_group_op;
+/* The caller's collective transport (MPI, torch.distributed, ...). Every call is made by all
+ * ranks in the same order; return 0 on success. allgather: `bytes` from each rank into `recv`
+ * (size x bytes, rank order). allreduce_f64: in place over `count` doubles. */
+typedef struct tlsph_group_comm {
+  void* ctx;
+  int rank;
+  int size;
+  int (*allgather)(void* ctx, const void* send, size_t bytes, void* recv);
+  int (*allreduce_f64)(void* ctx, double* values, int count, int op);
+} tlsph_group_comm;
+typedef struct tlsph_dev_group tlsph_dev_group;
+/* Collective: exchanges the IPC exports and cell tables, creates the shared enqueue counters and
+ * links the neighbours. The slab must outlive the group. */
+tlsph_status tlsph_dev_group_create(tlsph_dev* slab, const tlsph_group_comm* comm, tlsph_dev_group** out);
+/* Collective: `count` strang_damping_sweeps (damping.cpp:125-182) of the whole body. */
+tlsph_status tlsph_dev_group_sweep(tlsph_dev_group* group, tlsph_dev_scheme scheme, double eta_tilde, double dt,
+                                   int count);
+/* Collective: the loop of runner.cpp:341-391 for params->max_steps steps (fixed step count: no
+ * end_time, KE stop, probe or resume). result: steps, damped_steps, t, last_dt and, in
+ * total_seconds, this rank's device time of the loop (the caller takes the max over ranks). */
+tlsph_status tlsph_dev_group_run(tlsph_dev_group* group, const tlsph_dev_loop_params* params,
+                                 tlsph_dev_loop_result* result);
+/* Collective (a final barrier); frees the group, not the slab. */
+void tlsph_dev_group_destroy(tlsph_dev_group* group);
+/* Message of the last failed tlsph_dev_group_* / tlsph_group_* call on this thread. */
+const char* tlsph_group_last_error(void);
+/* Host-only pieces (no device): the slab planner (column ranges balanced by particle count, each
+ * at least min_width wide; ranges[2r], ranges[2r+1] = x0, x1 of rank r; -1 if impossible), the
+ * per-step dt the group loop forms from the combined |v|max, |a|max (k_step_begin's formula),
+ * and a check of a communicator's allgather / allreduce. */
+int tlsph_group_plan(const int64_t* column_counts, int ncol, int world, int min_width, int* ranges);
+double tlsph_group_step_dt(const tlsph_dev_loop_params* params, int dim, double vmax, double amax);
+tlsph_status tlsph_group_comm_selftest(const tlsph_group_comm* comm);
+
 /* Host RNG helpers (damping.hpp:41-50, damping.cpp:29-34). */
 tlsph_status tlsph_random_uniforms(uint64_t seed, size_t n, double* out);
 tlsph_status tlsph_random_choice(double eta, double alpha, uint64_t seed, size_t n, double* out);

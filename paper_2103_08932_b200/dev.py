@@ -78,6 +78,16 @@ class LoopParams(C.Structure):
                 ("probe_capacity", C.c_size_t), ("pause_on_mark", C.c_int), ("resume", C.c_int)]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int)
+
+
+class GroupComm(C.Structure):
+    """tlsph_group_comm: the caller's collectives for a tlsph_dev_group (tlsph_dev.h)."""
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int), ("size", C.c_int), ("allgather", ALLGATHER_FN),
+                ("allreduce_f64", ALLREDUCE_FN)]
+
+
 class LoopResult(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("damped_steps", C.c_uint64), ("t", C.c_double), ("last_dt", C.c_double),
                 ("elastic_seconds", C.c_double), ("damping_seconds", C.c_double), ("total_seconds", C.c_double),
@@ -166,6 +176,16 @@ def lib():
     L.tlsph_dev_pairwise_split_update.argtypes = [P, S, C.c_int64, C.c_double, C.c_double]
     L.tlsph_dev_explicit_damping_accel.argtypes = [P, C.c_double, D]
     L.tlsph_dev_run.argtypes = [P, C.POINTER(LoopParams), C.POINTER(LoopResult)]
+    L.tlsph_dev_group_create.argtypes = [P, C.POINTER(GroupComm), C.POINTER(C.c_void_p)]
+    L.tlsph_dev_group_sweep.argtypes = [P, I, C.c_double, C.c_double, I]
+    L.tlsph_dev_group_run.argtypes = [P, C.POINTER(LoopParams), C.POINTER(LoopResult)]
+    L.tlsph_dev_group_destroy.argtypes = [P]
+    L.tlsph_dev_group_destroy.restype = None
+    L.tlsph_group_last_error.restype = C.c_char_p
+    L.tlsph_group_plan.argtypes = [C.POINTER(C.c_int64), I, I, I, C.POINTER(C.c_int)]
+    L.tlsph_group_step_dt.argtypes = [C.POINTER(LoopParams), I, C.c_double, C.c_double]
+    L.tlsph_group_step_dt.restype = C.c_double
+    L.tlsph_group_comm_selftest.argtypes = [C.POINTER(GroupComm)]
     L.tlsph_random_uniforms.argtypes = [C.c_uint64, S, D]
     L.tlsph_random_choice.argtypes = [C.c_double, C.c_double, C.c_uint64, S, D]
     L.tlsph_dev_last_elapsed.argtypes = [P]

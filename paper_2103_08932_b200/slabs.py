@@ -598,3 +598,112 @@ def run_loop(group, spec, dim, sweeper=None):
         t = t + dt
     group.reduce(False, spec.steps)  # check_finite of the last step
     return {"steps": spec.steps, "damped": int(flags.sum()), "t": t, "last_dt": dt}
+
+
+# ---------------------------------------------------------------- the C entry point (csrc/cuda/group.cu)
+class TorchComm:
+    """tlsph_group_comm over torch.distributed (a gloo group: the collectives carry host bytes and
+    scalars); keep the object alive while the C group uses it."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        from . import dev
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        self._ag = dev.ALLGATHER_FN(self._allgather)
+        self._ar = dev.ALLREDUCE_FN(self._allreduce)
+        self.struct = dev.GroupComm(None, self.rank, self.size, self._ag, self._ar)
+
+    def _allgather(self, ctx, send, nbytes, recv):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        try:
+            mine = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8) if nbytes else \
+                torch.empty(0, dtype=torch.uint8)
+            out = torch.empty(self.size * nbytes, dtype=torch.uint8)
+            dist.all_gather_into_tensor(out, mine, group=self.group)
+            if nbytes:
+                C.memmove(recv, out.numpy().ctypes.data, self.size * nbytes)
+            return 0
+        except Exception:  # reported to the library as a failed collective
+            return 1
+
+    def _allreduce(self, ctx, values, count, op):
+        import ctypes as C
+
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        try:
+            arr = np.ctypeslib.as_array(values, shape=(count,))
+            t = torch.from_numpy(arr.copy())
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 0 else dist.ReduceOp.SUM, group=self.group)
+            arr[:] = t.numpy()
+            return 0
+        except Exception:
+            return 1
+
+
+class CGroup:
+    """tlsph_dev_group_* (C ABI) over this process's slab: the IPC-fused group loop and sweeps."""
+
+    def __init__(self, system, comm):
+        import ctypes as C
+
+        from . import dev
+
+        self.d, self.comm = system, comm
+        self._h = C.c_void_p()
+        st = dev.lib().tlsph_dev_group_create(system._h, C.byref(comm.struct), C.byref(self._h))
+        if st != 0:
+            raise dev.TlsphError(st, dev.lib().tlsph_group_last_error().decode())
+
+    def _check(self, st):
+        from . import dev
+
+        if st != 0:
+            raise dev.TlsphError(st, dev.lib().tlsph_group_last_error().decode())
+
+    def sweep(self, scheme, eta_tilde, dt, count=1):
+        from . import dev
+
+        self._check(dev.lib().tlsph_dev_group_sweep(self._h, dev.SCHEMES[scheme], eta_tilde, dt, count))
+
+    def run(self, material, *, h, eta, alpha, steps, seed=0, scheme="particle_split", fixed_dt=0.0, elastic=True):
+        import ctypes as C
+
+        from . import dev
+
+        p = dev.LoopParams(material, h, eta, alpha, dev.SCHEMES[scheme], seed, 0.0, steps, fixed_dt,
+                           1 if elastic else 0, 0, 1e-8, -1, 0.0, None, 0, 0, 0)
+        r = dev.LoopResult()
+        self._check(dev.lib().tlsph_dev_group_run(self._h, C.byref(p), C.byref(r)))
+        return {"steps": r.steps, "damped": r.damped_steps, "t": r.t, "last_dt": r.last_dt,
+                "device_s": r.total_seconds}
+
+    def close(self):
+        from . import dev
+
+        if self._h:
+            dev.lib().tlsph_dev_group_destroy(self._h)
+            self._h = None
+
+
+def plan_c(column_counts, world, min_width=2):
+    """slabs.plan through the C ABI (tlsph_group_plan)."""
+    import ctypes as C
+
+    from . import dev
+
+    counts = np.ascontiguousarray(column_counts, dtype=np.int64)
+    out = (C.c_int * (2 * world))()
+    if dev.lib().tlsph_group_plan(counts.ctypes.data_as(C.POINTER(C.c_int64)), len(counts), world, min_width, out) != 0:
+        raise ValueError("no plan")
+    return [(out[2 * r], out[2 * r + 1]) for r in range(world)]

@@ -782,3 +782,141 @@ def test_ipc_sweep_ordering_points(tmp_path, world):
             for g, p in enumerate(phases[1:], start=1):
                 assert p == ("phase", g % nphase, (g - 1) % nphase)
             assert c[-2:] == [("wait_phase", nphase - 1), ("sync",)]
+
+
+# ---------------------------------------------------------------- the C entry point (tlsph_dev_group_*)
+def test_c_plan_equals_python_plan():
+    """tlsph_group_plan (csrc/cuda/group.cu) is slabs.plan: random column populations, 1-8 ranks."""
+    rng = np.random.RandomState(17)
+    for _ in range(200):
+        ncol = int(rng.randint(2, 120))
+        world = int(rng.randint(1, max(2, min(8, ncol // 2) + 1)))
+        counts = rng.randint(0, 5000, ncol)
+        if rng.rand() < 0.3:
+            counts[rng.rand(ncol) < 0.5] = 0
+        assert slabs.plan_c(counts, world) == slabs.plan(counts, world), (counts.tolist(), world)
+    with pytest.raises(ValueError):
+        slabs.plan_c(np.ones(3), 2)
+
+
+def test_c_step_dt_equals_python_step_dt_bitwise():
+    """The group loop's dt (tlsph_group_step_dt, k_step_begin's formula) equals slabs.step_dt bit for
+    bit: with and without |a|max, fixed dt, each scheme's viscous bound."""
+    import ctypes as C
+
+    from paper_2103_08932_b200 import dev, scenarios as S
+
+    mat = S.material()
+    rng = np.random.RandomState(5)
+    for scheme in ("particle_split", "pairwise_split", "explicit"):
+        for _ in range(300):
+            h = float(rng.uniform(1e-3, 5e-2))
+            eta = float(rng.choice([0.0, rng.uniform(1.0, 500.0)]))
+            alpha = float(rng.uniform(0.05, 1.0))
+            fixed = float(rng.choice([0.0, 0.0, 1e-4]))
+            vmax, amax = float(rng.exponential(0.5)), float(rng.choice([0.0, rng.exponential(50.0)]))
+            dim = int(rng.choice([2, 3]))
+            spec = slabs.LoopSpec(mat, h, eta, alpha, 1, scheme=scheme, fixed_dt=fixed)
+            p = dev.LoopParams(mat, h, eta, alpha, dev.SCHEMES[scheme], 0, 0.0, 1, fixed, 1, 0, 1e-8, -1, 0.0, None,
+                               0, 0, 0)
+            got = dev.lib().tlsph_group_step_dt(C.byref(p), dim, vmax, amax)
+            assert got == slabs.step_dt(spec, vmax, amax, dim), (scheme, h, eta, alpha, fixed, vmax, amax, dim)
+
+
+def _comm_selftest_rank(rank, world, port, result_dir):
+    import torch.distributed as dist
+
+    from paper_2103_08932_b200 import dev
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes as C
+
+        comm = slabs.TorchComm()
+        st = dev.lib().tlsph_group_comm_selftest(C.byref(comm.struct))
+        msg = dev.lib().tlsph_group_last_error().decode()
+        np.save(os.path.join(result_dir, f"st{rank}.npy"), np.array([st]))
+        assert st == 0, msg
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c_group_communicator_over_gloo(tmp_path, world):
+    """The C group's collectives (tlsph_group_comm) carried by torch.distributed gloo across
+    processes on the CPU: allgather in rank order, max / sum all-reduces (tlsph_group_comm_selftest)."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_comm_selftest_rank, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert int(np.load(os.path.join(tmp_path, f"st{r}.npy"))[0]) == 0
+
+
+def _c_group_loop_rank(rank, world, port, dim, mode, result_dir):
+    import torch.distributed as dist
+
+    from paper_2103_08932_b200 import dev, scenarios as S
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev.select_device(0)
+        mat = S.material()
+        r0, cons, v = body(dim, [40, 9] if dim == 2 else [24, 6, 5])
+        v = 0.05 * v
+        g = np.zeros_like(r0)
+        g[:, 1] = -9.81
+        grid, parts = slabs.decompose(r0, H, world)
+        s = parts[rank]
+        d = slabs.make_device_slab(grid, s, r0, DP ** dim, RHO, H, cons)
+        d.set_reduction(mode)
+        d.set("v", v[s.ids])
+        d.set("body", g[s.ids])
+        d.prepare(mat)
+        grp = slabs.CGroup(d, slabs.TorchComm())
+        out = grp.run(mat, h=H, eta=0.2 * RHO * mat.c * H, alpha=0.5, steps=14, seed=3)
+        grp.sweep("particle_split", 160.0, 1e-4, count=2)
+        d.synchronize()
+        np.savez(os.path.join(result_dir, f"r{rank}.npz"), ids=s.ids, x0=s.x0, x1=s.x1, t=out["t"],
+                 damped=out["damped"], **{k: d.get(k) for k in ("v", "r", "F", "dFdt", "rho", "a")})
+        grp.close()
+        del d
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,world,mode", [(3, 2, "fast"), (3, 3, "ordered"), (2, 2, "ordered")])
+def test_c_group_loop_equals_undivided_device_loop(tmp_path, dim, world, mode):
+    """tlsph_dev_group_run + tlsph_dev_group_sweep (the C entry point; one process per slab, gloo
+    carrying the set-up and dt scalars, CUDA IPC the halo and colour-phase stores): every owned
+    particle equals the undivided device loop followed by two sweeps, bit for bit."""
+    import torch.multiprocessing as mp
+
+    from paper_2103_08932_b200 import dev, scenarios as S
+
+    mp.spawn(_c_group_loop_rank, args=(world, _free_port(), dim, mode, str(tmp_path)), nprocs=world, join=True)
+    mat = S.material()
+    r0, cons, v = body(dim, [40, 9] if dim == 2 else [24, 6, 5])
+    v = 0.05 * v
+    g = np.zeros_like(r0)
+    g[:, 1] = -9.81
+    whole = dev.DeviceSystem(r0, DP ** dim, RHO, H, cons)
+    whole.set_reduction(mode)
+    whole.set("v", v)
+    whole.set("body", g)
+    whole.prepare(mat)
+    ref = whole.run(mat, eta=0.2 * RHO * mat.c * H, alpha=0.5, steps=14, seed=3)
+    whole.damping_sweep("particle_split", 160.0, 1e-4, count=2)
+    grid, parts = slabs.decompose(r0, H, world)
+    cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
+    for r in range(world):
+        z = np.load(os.path.join(tmp_path, f"r{r}.npz"))
+        assert float(z["t"]) == ref["t"] and int(z["damped"]) == ref["damped"] > 0
+        ids = z["ids"]
+        own = (cols[ids] >= int(z["x0"])) & (cols[ids] < int(z["x1"]))
+        for name in ("v", "r", "F", "dFdt", "rho", "a"):
+            assert np.array_equal(z[name][own], whole.get(name)[ids[own]]), (r, name)
