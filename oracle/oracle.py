@@ -94,6 +94,7 @@ def lib():
         L.orc_run.argtypes = [P, D, D]
         L.orc_run_probed.argtypes = [P, D, D, D, C.c_longlong, C.POINTER(C.c_longlong)]
         L.orc_set_contact.argtypes = [P, D, D, C.c_double]
+        L.orc_last_run.argtypes = [P, D]
         L.orc_openmp_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -259,6 +260,12 @@ class OracleSystem:
         out = np.empty((self.n, self.dim))
         _check(lib().orc_explicit_damping_accel(self._h, eta, _dp(out), threads))
         return out
+
+    def last_run(self):
+        """(completed steps, t) of the last run, also when it stopped on an error."""
+        out = np.zeros(2)
+        _check(lib().orc_last_run(self._h, _dp(out)))
+        return int(out[0]), float(out[1])
 
     def set_contact(self, point, normal, stiffness):
         """ExternalAccel's penalty contact plane (forces.hpp:13-24); stiffness <= 0 removes it."""

@@ -438,6 +438,21 @@ int orc_run_probed(void* hv, const double* params, double* out, double* samples,
       double t = s.loop_t, el = 0.0, dm = 0.0, last_dt = 0.0;
       long long steps = s.loop_steps, damped = s.loop_damped;
       std::vector<orc::Vec<std::remove_reference_t<decltype(s)>::dim>> visc;
+      // a failing step leaves the completed-step count and t behind (orc_last_run), as
+      // tlsph_dev_last_run_steps does for the device loop
+      struct Completed {
+        decltype(s)& sim;
+        long long& steps;
+        double& t;
+        bool armed = true;
+        ~Completed() {
+          if (armed) {
+            sim.loop_steps = steps;
+            sim.loop_t = t;
+          }
+        }
+      };
+      Completed completed{s, steps, t};
       while ((end_time <= 0.0 || t < end_time) && steps < max_steps) {
         double dt = fixed_dt > 0.0 ? fixed_dt : orc::stable_dt(s.sys, s.mat, h);
         if (damping_active && fixed_dt <= 0.0) {
@@ -477,6 +492,7 @@ int orc_run_probed(void* hv, const double* params, double* out, double* samples,
       }
       if (probe >= 0 && (ns == 0 || samples[4 * (ns - 1)] < t)) record(t);
       if (nsamples) *nsamples = ns;
+      completed.armed = false;
       s.loop_t = t;
       s.loop_steps = steps;
       s.loop_damped = damped;
@@ -497,6 +513,16 @@ int orc_run(void* hv, const double* params, double* out) {
   p[11] = -1.0;
   p[12] = 0.0;
   return orc_run_probed(hv, p, out, nullptr, 0, nullptr);
+}
+
+// Completed steps and t of the last run, also when it stopped on an error.
+int orc_last_run(void* hv, double* out) {
+  return guarded([&] {
+    with_sim(hv, [&](auto& s) {
+      out[0] = static_cast<double>(s.loop_steps);
+      out[1] = s.loop_t;
+    });
+  });
 }
 
 // ExternalAccel's contact plane (forces.hpp:13-24); stiffness <= 0 removes it.
