@@ -26,8 +26,9 @@ Keys of the line:
              (sweep DPU/s and loop PS/s on one GPU: the N = 1 base of the N > 1 line).
 
 Multi-GPU (torchrun, one rank per GPU): value = BASELINE cfg5's weak-scaling loop, one x-slab of
-an N x 250-layer body (15.6 M particles) per rank with the fused cross-process exchange
-(slabs.IpcSlabSweep / IpcGroup), PS/s over the whole body, device time max over ranks.
+an N x 250-layer body (15.6 M particles) per rank, driven through the C entry point
+tlsph_dev_group_run (csrc/cuda/group.cu: CUDA IPC peer stores per colour phase and halo pushes,
+dt all-reduce over a gloo communicator), PS/s over the whole body, device time max over ranks.
 """
 from __future__ import annotations
 

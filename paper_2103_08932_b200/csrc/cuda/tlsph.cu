@@ -242,8 +242,18 @@ template <int D, int G, bool POST, bool UV0 = false>
 __global__ void TL_BOUNDS_C k_deformation_rate(DFields f, DScalars* sc, double dt, int loop) {
   deformation_rate_body<D, G, TLSPH_TL_U, POST, UV0>(f, sc, dt, loop);
 }
+// register bound of the slot-order (one thread per particle) passes: minimum resident 128-thread
+// blocks per SM (0: none; the compiler's choice, 70-72 registers = 7 blocks)
+#ifndef TLSPH_TL_OMINB
+#define TLSPH_TL_OMINB 0
+#endif
+#if TLSPH_TL_OMINB > 0
+#define TL_BOUNDS_O __launch_bounds__(128, TLSPH_TL_OMINB)
+#else
+#define TL_BOUNDS_O
+#endif
 template <int D, bool POST, bool OI = false>
-__global__ void k_deformation_rate_ordered(DFields f, DScalars* sc, double dt, int loop) {
+__global__ void TL_BOUNDS_O k_deformation_rate_ordered(DFields f, DScalars* sc, double dt, int loop) {
   deformation_rate_body<D, 1, OI ? TLSPH_TL_OU : 1, POST, false, OI>(f, sc, dt, loop);
 }
 
@@ -367,7 +377,11 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
       for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int k = 0; k < W / 2; ++k) {
+#ifdef TLSPH_PROBE_NOGATHER  // measurement probe only: the pass without its neighbour-record gather
+          const double2 x = make_double2(pbi[2 * k] + j[u], pbi[2 * k + 1]);
+#else
           const double2 x = __ldg(reinterpret_cast<const double2*>(f.pbv + pbv_at<D>(f.n, j[u], 2 * k)));
+#endif
           pbj[u][2 * k] = x.x;
           pbj[u][2 * k + 1] = x.y;
         }
@@ -429,7 +443,7 @@ __global__ void TL_BOUNDS_B k_momentum(DFields f, DScalars* sc, double dt_arg, i
   momentum_body<D, G, TLSPH_TL_UB, KICK>(f, sc, dt_arg, loop);
 }
 template <int D, bool KICK, bool OI = false>
-__global__ void k_momentum_ordered(DFields f, DScalars* sc, double dt_arg, int loop) {
+__global__ void TL_BOUNDS_O k_momentum_ordered(DFields f, DScalars* sc, double dt_arg, int loop) {
   momentum_body<D, 1, OI ? TLSPH_TL_OU : 1, KICK, OI>(f, sc, dt_arg, loop);
 }
 
