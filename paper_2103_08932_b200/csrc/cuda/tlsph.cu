@@ -17,7 +17,6 @@
 #include <cmath>
 #include <cstdlib>
 
-#include "stencil_tile.cuh"
 #include "system.cuh"
 #include "tma.cuh"
 
@@ -447,117 +446,6 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
   momentum_finish<D, KICK>(f, i, acc, dt);
 }
 
-// Cell-tiled FAST pass B: one CTA per cell. The (P B0, V0) records of the cell's 3^D stencil are
-// staged in shared memory in the damping sweep's tile layout (stencil rows one after another, each
-// starting at the parity of its first global index; stencil_tile.cuh), so each slot's u16 stencil
-// index nloc is its neighbour's tile position and the per-slot record gather reads shared memory
-// instead of going through the L1 tag stage of global loads (which bounds the global-gather pass
-// B: 16 tag requests per 16-byte warp load, profiles/r2a_cfg4_summary.md). G lanes per particle
-// over its row (lane-parallel sums: FAST class); every thread of the CTA reaches the group sum.
-// Tile: W/2 arrays of 16-byte chunks (chunk k of the record at tile position t), S positions each.
-template <int D, int G, bool KICK>
-__global__ void __launch_bounds__(256) k_momentum_tiled(DFields f, DScalars* sc, double dt_arg, int loop, int S) {
-  constexpr int W = pbv_stride<D>();
-  constexpr int kSegs = seg_count<D>();
-  extern __shared__ __align__(16) double2 tile[];
-  __shared__ long long s_start[9];
-  __shared__ int s_base[9], s_len[9];
-  if (TLSPH_TL_PDL) {
-    grid_launch_dependents();
-    grid_dependency_wait();  // pass A's records
-  }
-  if (loop && sc->halt) return;
-  const long long lin = blockIdx.x;
-  const long long p0 = f.cell_start[lin], p1 = f.cell_start[lin + 1];
-  if (p0 == p1) return;  // uniform over the CTA
-  const double dt = loop ? sc->dt : dt_arg;
-  const int tid = threadIdx.x;
-  int c[3];
-  c[0] = static_cast<int>(lin % f.dims[0]);
-  c[1] = static_cast<int>((lin / f.dims[0]) % f.dims[1]);
-  c[2] = D == 3 ? static_cast<int>(lin / (static_cast<long long>(f.dims[0]) * f.dims[1])) : 0;
-  if (tid < 32) {  // the row table, as issue_staging lays it out (tile position = nloc)
-    long long sstart, send;
-    locate_row<D>(f, c, tid, sstart, send);
-    const int slen = static_cast<int>(send - sstart);
-    const int par = static_cast<int>(sstart & 1);
-    const int plen = slen > 0 ? ((slen + par + 1) & ~1) : 0;
-    int incl = plen;
-#pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-      const int x = __shfl_up_sync(kFull, incl, o);
-      if (tid >= o) incl += x;
-    }
-    if (tid < kSegs) {
-      s_start[tid] = sstart;
-      s_len[tid] = slen;
-      s_base[tid] = incl - plen + par;
-    }
-  }
-  __syncthreads();
-  // stage: 16-byte chunk k of every stencil particle, rows one after another
-  int total = 0;
-#pragma unroll
-  for (int q = 0; q < kSegs; ++q) total += s_len[q];
-  for (int e = tid; e < total * (W / 2); e += blockDim.x) {
-    const int k = e / total;
-    int r = e - k * total, q = 0;
-    while (q < kSegs - 1 && r >= s_len[q]) r -= s_len[q++];
-    const long long j = s_start[q] + r;
-    cp_async16(tile + static_cast<size_t>(k) * S + s_base[q] + r,
-               reinterpret_cast<const double2*>(f.pbv) + (static_cast<long long>(k) * f.n + j));
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  constexpr int center = D == 2 ? 1 : 4;
-  const int lbase = s_base[center] + static_cast<int>(p0 - s_start[center]);  // the cell's own particles
-  const int np = static_cast<int>(p1 - p0);
-  for (int base = 0; base < np * G; base += blockDim.x) {  // every thread reaches the group sums
-    const int t = base + tid;
-    const int pi = t / G, l = t % G;
-    const bool active = pi < np;
-    const long long i = p0 + (active ? pi : 0);
-    double acc[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] = 0.0;
-    if (active) {
-      double pbi[W];
-#pragma unroll
-      for (int k = 0; k < W / 2; ++k) {
-        const double2 x = tile[static_cast<size_t>(k) * S + lbase + pi];
-        pbi[2 * k] = x.x;
-        pbi[2 * k + 1] = x.y;
-      }
-      const double V0i = pbi[D * D];
-      for (long long sl = f.offs[i] + l, hi = f.offs[i + 1]; sl < hi; sl += G) {
-        const int jt = f.nloc[sl];
-        const double dw = f.dwdr0[sl];
-        double e[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) e[d] = f.e0[d][sl];
-        double pbj[W];
-#pragma unroll
-        for (int k = 0; k < W / 2; ++k) {
-          const double2 x = tile[static_cast<size_t>(k) * S + jt];
-          pbj[2 * k] = x.x;
-          pbj[2 * k + 1] = x.y;
-        }
-        const double kk = V0i * pbj[D * D] * dw;
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-          double tt = (kk * (pbi[r * D] + pbj[r * D])) * e[0];
-#pragma unroll
-          for (int q = 1; q < D; ++q) tt = tt + (kk * (pbi[r * D + q] + pbj[r * D + q])) * e[q];
-          acc[r] = acc[r] + tt;
-        }
-      }
-    }
-#pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] = group_sum_fast<G>(acc[d]);
-    if (active && l == 0) momentum_finish<D, KICK>(f, i, acc, dt);
-  }
-}
-
 template <int D, int G, bool KICK>
 __global__ void TL_BOUNDS_B k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
   momentum_body<D, G, TLSPH_TL_UB, KICK>(f, sc, dt_arg, loop);
@@ -713,54 +601,9 @@ void launch_pdl(void (*kernel)(KArgs...), long long threads, cudaStream_t st, Ar
   CK(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-// Cell-tiled FAST pass B (k_momentum_tiled): TLSPH_TL_TILED=4 or 8 selects it with that many
-// lanes per particle (A/B knob; 0 / unset: off).
-int tiled_lanes() {
-  static const int g = [] {
-    const char* e = std::getenv("TLSPH_TL_TILED");
-    const int v = e && *e ? std::atoi(e) : 0;
-    return v == 4 || v == 8 ? v : 0;
-  }();
-  return g;
-}
-
-template <int D, int G>
-void launch_momentum_tiled(DevSystem& s, double dt, int loop) {
-  DFields f = s.fields();
-  const int S = (std::max(s.max_stencil, 1) + 7) & ~7;
-  const size_t smem = static_cast<size_t>(pbv_stride<D>() / 2) * S * sizeof(double2);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    CK(cudaFuncSetAttribute(k_momentum_tiled<D, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    configured = smem;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(s.ncells));
-  cfg.blockDim = dim3(G == 8 ? 256 : 128);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = TLSPH_TL_PDL ? 1 : 0;
-  CK(cudaLaunchKernelEx(&cfg, k_momentum_tiled<D, G, true>, f, s.scal.p, dt, loop, S));
-}
-
 void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop, int pass) {
   DFields f = s.fields();
   const long long n = s.n;
-  if (pass == 1 && s.reduction != TLSPH_REDUCTION_ORDERED && tiled_lanes() && f.nloc && s.stencil_ok) {
-    if (s.D == 2) {
-      if (tiled_lanes() == 8) launch_momentum_tiled<2, 8>(s, dt, loop);
-      else launch_momentum_tiled<2, 4>(s, dt, loop);
-    } else {
-      if (tiled_lanes() == 8) launch_momentum_tiled<3, 8>(s, dt, loop);
-      else launch_momentum_tiled<3, 4>(s, dt, loop);
-    }
-    return;
-  }
   // large bodies (group-interleaved slot copy present): both modes run the slot-order one-thread
   // kernels (build_ordered_rows, state.cu); TLSPH_TL_EIGHT_LANES=1 keeps FAST on eight lanes (A/B)
   static const bool eight_lanes = [] {
