@@ -23,7 +23,8 @@ Keys of the line:
              same W+K steps; its K timed steps are the baseline, its final state the parity check;
   legs       cfg2 damping sweep (DPU/s, its e2e through strang_damping_sweep<3>, 500-sweep parity),
              pairwise split sweep on cfg2, cfg1 full run, cfg3 loop, cfg5 weak-scaling share
-             (sweep DPU/s and loop PS/s on one GPU: the N = 1 base of the N > 1 line).
+             (sweep DPU/s and loop PS/s on one GPU: the N = 1 base of the N > 1 line), and the
+             paper's Table 1 damping times (bending cantilever h/dp 12, t = 2 s) through tlsph_sim_run.
 
 Multi-GPU (torchrun, one rank per GPU): value = BASELINE cfg5's weak-scaling loop, one x-slab of
 an N x 250-layer body (15.6 M particles) per rank, driven through the C entry point
@@ -437,6 +438,46 @@ def leg_cfg5_weak(args):
     return out
 
 
+PAPER_TABLE1 = {1.0: {"serial_s": 32.82, "parallel_6core_s": 11.61}, 0.2: {"serial_s": 6.66, "parallel_6core_s": 2.38}}
+
+
+def leg_paper_table1(args):
+    """The paper's Table 1 workload: the damping time of the
+    bending cantilever at h/dp = 12 to t = 2 s, particle split, alpha 1.0 and 0.2, through
+    tlsph_sim_run (the reference's built-in case: 33 x 12 x 12 = 4,752 particles, its 0.04 x 0.016 m
+    geometry, cases.cpp:81-82; the paper's runs used 0.1 x 0.04 m on a Ryzen 5 3600). A small body:
+    ~11 cells per colour phase, so the sweep is bound by the per-particle Gauss-Seidel chain latency."""
+    import ctypes as C
+
+    L = C.CDLL(os.path.join(ROOT, "paper_2103_08932_b200", "lib", "libtlsph.so.1"))
+    L.tlsph_sim_create.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), C.c_size_t, C.POINTER(C.c_void_p)]
+    L.tlsph_sim_run.argtypes = [C.c_void_p]
+    L.tlsph_sim_destroy.argtypes = [C.c_void_p]
+    L.tlsph_sim_phase_seconds.argtypes = [C.c_void_p, C.c_char_p]
+    L.tlsph_sim_phase_seconds.restype = C.c_double
+    L.tlsph_sim_step_count.argtypes = [C.c_void_p]
+    L.tlsph_sim_step_count.restype = C.c_uint64
+    L.tlsph_sim_damped_step_count.argtypes = [C.c_void_p]
+    L.tlsph_sim_damped_step_count.restype = C.c_uint64
+    out = {"workload": "bending_cantilever, resolution 12, end_time 2 s, particle split, gpu.reduction fast",
+           "metric": "damping process seconds (tlsph_sim_phase_seconds 'damping')", "runs": []}
+    for alpha in (1.0, 0.2):
+        ov = ["case=bending_cantilever", "resolution=12", "end_time=2.0", f"damping.alpha={alpha}", "output.dir=",
+              "gpu.reduction=fast"]
+        arr = (C.c_char_p * len(ov))(*[o.encode() for o in ov])
+        h = C.c_void_p()
+        if L.tlsph_sim_create(None, arr, len(ov), C.byref(h)) != 0 or L.tlsph_sim_run(h) != 0:
+            raise RuntimeError("tlsph_sim_run failed")
+        rec = {"alpha": alpha, "damping_s": L.tlsph_sim_phase_seconds(h, b"damping"),
+               "elastic_s": L.tlsph_sim_phase_seconds(h, b"elastic"), "total_s": L.tlsph_sim_phase_seconds(h, b"total"),
+               "steps": int(L.tlsph_sim_step_count(h)), "damped_steps": int(L.tlsph_sim_damped_step_count(h)),
+               "paper": PAPER_TABLE1[alpha]}
+        rec["paper_parallel_over_ours"] = PAPER_TABLE1[alpha]["parallel_6core_s"] / rec["damping_s"]
+        L.tlsph_sim_destroy(h)
+        out["runs"].append(rec)
+    return out
+
+
 # ----------------------------------------------------------------------------- N > 1
 def sharded_cfg5(args, ws, rank):
     """BASELINE cfg5's weak scaling: a body of ws x `--scale-layers` x-layers of 250 x 250 (dp 0.004;
@@ -627,7 +668,7 @@ def main():
                 del o
             if not args.no_legs:
                 for name, fn in (("sweep_cfg2", leg_cfg2), ("cfg1", leg_cfg1), ("particle_steps_cfg3", leg_cfg3),
-                                 ("cfg5_weak", leg_cfg5_weak)):
+                                 ("cfg5_weak", leg_cfg5_weak), ("paper_table1", leg_paper_table1)):
                     try:
                         out[name] = fn(args)
                     except Exception as exc:
