@@ -105,6 +105,10 @@ struct DFields {
   // uniform masses (every m equal): RN(1/m), and per slot the stencil index with bit 15 set for
   // a clamped j (the streamed FAST sweep forms qf = pf * minv_uniform from them); null otherwise
   const uint16_t* nlocf;
+  // bank-spread rows (uniform masses, TLSPH_SWEEP_SPREAD): nlocf and this copy of pf hold every row
+  // regrouped for conflict-free half-warp gathers; ghdr[i] = the row's group starts (k_spread_rows)
+  const double* pfsp;
+  const unsigned long long* ghdr;
   double minv_uniform;
   double v0_uniform;  // every V0 equal: that value (the FAST dF/dt pass skips the V0_j gather); 0 otherwise
   // x-slab peers (slabs.py): per particle of a column shared with a neighbouring slab, the
@@ -169,6 +173,11 @@ struct DFields {
 __device__ __forceinline__ bool is_owned(const DFields& f, long long i) { return !f.own || f.own[i]; }
 
 constexpr int kWarp = 32;
+// FAST particle-split chain on bank-spread slot rows (state.cu k_spread_rows, sweep_chain.cuh);
+// 0: rows in slot order (A/B)
+#ifndef TLSPH_SWEEP_SPREAD
+#define TLSPH_SWEEP_SPREAD 1
+#endif
 constexpr uint16_t kNoLocal = 0xFFFF;
 
 // ---------------------------------------------------------------- small helpers

@@ -460,6 +460,66 @@ __global__ void k_nlocf(const uint16_t* __restrict__ nloc, const int* __restrict
   nlocf[s] = static_cast<uint16_t>(nloc[s] | (flag[nbr[s]] ? 0x8000u : 0u));
 }
 
+// Bank-spread rows for the FAST particle-split chain (sweep_chain.cuh spread_slot). The chain's
+// half-warps gather stencil velocities from shared memory at t.sv[d][nloc]: 16 lanes, 16 pairs of
+// banks, one wavefront if the 16 indices differ mod 16 and one more per collision otherwise (ncu:
+// 2.3x the ideal wavefronts with rows in slot order). Each row is regrouped into `groups` (= 2 K)
+// groups of at most 16 slots, placing every slot in the group that holds the fewest slots of its
+// residue (ties: the emptiest), one thread per row; group g occupies positions
+// [start_g, start_g+1) of the row, header byte g = start_g (byte 0 is 0, unused groups start at
+// the row's end). Writes the regrouped stencil indices (bit 15: clamped j) and pair factors. The
+// regrouping changes only the order in which the FAST chain sums a row (its tolerance class).
+__global__ void k_spread_rows(const long long* __restrict__ offs, const uint16_t* __restrict__ nloc,
+                              const int* __restrict__ nbr, const uint8_t* __restrict__ flag,
+                              const double* __restrict__ pf, int groups, uint16_t* __restrict__ nlocf,
+                              double* __restrict__ pfsp, unsigned long long* __restrict__ ghdr, long long n) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long lo = offs[i];
+  const int cnt = static_cast<int>(offs[i + 1] - lo);
+  constexpr int kMaxRow = 128, kMaxGroups = 8;
+  if (cnt > kMaxRow || cnt > 16 * groups) {  // not a row of the register chain (K <= 4): keep slot order
+    for (int s = 0; s < cnt; ++s) {
+      nlocf[lo + s] = static_cast<uint16_t>(nloc[lo + s] | (flag[nbr[lo + s]] ? 0x8000u : 0u));
+      pfsp[lo + s] = pf[lo + s];
+    }
+    ghdr[i] = 0ull;
+    return;
+  }
+  uint8_t has[kMaxGroups][16];
+  uint8_t fill[kMaxGroups], grp[kMaxRow], idx[kMaxRow];
+  for (int g = 0; g < kMaxGroups; ++g) {
+    fill[g] = 0;
+    for (int r = 0; r < 16; ++r) has[g][r] = 0;
+  }
+  for (int s = 0; s < cnt; ++s) {
+    const int r = nloc[lo + s] & 15;
+    int best = -1, best_key = 1 << 30;
+    for (int g = 0; g < groups; ++g) {
+      if (fill[g] >= 16) continue;
+      const int key = has[g][r] * 32 + fill[g];
+      if (key < best_key) {
+        best_key = key;
+        best = g;
+      }
+    }
+    grp[s] = static_cast<uint8_t>(best);
+    idx[s] = fill[best]++;
+    ++has[best][r];
+  }
+  int start[kMaxGroups + 1];
+  start[0] = 0;
+  for (int g = 0; g < kMaxGroups; ++g) start[g + 1] = start[g] + (g < groups ? fill[g] : 0);
+  unsigned long long hdr = 0ull;
+  for (int g = 1; g < kMaxGroups; ++g) hdr |= static_cast<unsigned long long>(start[g]) << (8 * g);
+  ghdr[i] = hdr;
+  for (int s = 0; s < cnt; ++s) {
+    const long long dst = lo + start[grp[s]] + idx[s];
+    nlocf[dst] = static_cast<uint16_t>(nloc[lo + s] | (flag[nbr[lo + s]] ? 0x8000u : 0u));
+    pfsp[dst] = pf[lo + s];
+  }
+}
+
 // Rows re-ordered by ascending neighbour index (distinct within a row): one warp per row, each
 // slot's destination is its rank in the row.
 template <int D>
@@ -716,6 +776,8 @@ DFields DevSystem::fields() const {
   f.pfsq = pf_sq.p;
   f.nloc = nloc.p;
   f.nlocf = uniform_mass ? nlocf.p : nullptr;
+  f.pfsp = pfsp.p;
+  f.ghdr = ghdr.p;
   f.minv_uniform = minv_uniform;
   f.v0_uniform = v0_uniform;
   f.cell_start = cell_start.p;
@@ -937,12 +999,28 @@ void DevSystem::refresh_minvf() {
       uniform_mass = true;
       minv_uniform = 1.0 / m0;  // k_minvf's RN(1/m)
       nlocf.alloc(static_cast<size_t>(nslots));
+#if TLSPH_SWEEP_SPREAD
+      // rows regrouped for conflict-free gathers; the group count follows the chain's K
+      // (sweep.cu launch_particle_split), known once compute_sweep_stats has the longest row
+      if (max_row > 0) build_spread_rows();
+#else
       k_nlocf<<<grid_for(nslots, 256), 256, 0, stream>>>(nloc.p, nbr.p, flag.p, nlocf.p, nslots);
       CK_LAUNCH("k_nlocf");
+#endif
     }
   }
   fold_valid = false;  // constrained particles are marked in the fold constants
   pkf_valid = false;   // pairwise factors use the masses
+}
+
+void DevSystem::build_spread_rows() {
+  if (!uniform_mass || nslots <= 0 || !nlocf.p) return;
+  const int K = std::min(4, std::max(1, (max_row + kWarp - 1) / kWarp));
+  pfsp.alloc(static_cast<size_t>(nslots));
+  ghdr.alloc(static_cast<size_t>(n + 2));
+  k_spread_rows<<<grid_for(n, 128), 128, 0, stream>>>(offs.p, nloc.p, nbr.p, flag.p, pf.p, 2 * K, nlocf.p, pfsp.p,
+                                                      ghdr.p, n);
+  CK_LAUNCH("k_spread_rows");
 }
 
 // ------------------------------------------------------------------ per-step re-sort (BASELINE cfg4)
@@ -1081,6 +1159,9 @@ void DevSystem::compute_sweep_stats() {
   sync();
   max_cell_slots = static_cast<long long>(h[0]);
   max_row = static_cast<int>(h[1]);
+#if TLSPH_SWEEP_SPREAD
+  build_spread_rows();  // refresh_minvf above ran before the longest row was known
+#endif
   build_colour_lists();
 }
 

@@ -291,7 +291,10 @@ struct CellSpan {
 // the flattened row table, the cell's slot block, row offsets and fold
 // constants by bulk copies on the mbarrier. MASS: also stage m (ORDERED
 // divisions, pairwise).
-template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true, bool UNI = false>
+// HDR: the bank-spread rows' per-particle headers take the place of the fold denominators (unused
+// by the FAST chain).
+template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true, bool UNI = false,
+          bool HDR = false>
 __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
                                               long long sstart, long long send, int lane,
                                               const uint16_t* nl_src = nullptr, const double* pf_src = nullptr) {
@@ -336,7 +339,8 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   } else if (FOLD && lane == 3) {
     const uint32_t nb = static_cast<uint32_t>((cs.q1() - cs.q0()) * 8);
     tma_load_1d(t.sdiag, f.fdiag + cs.q0(), nb, t.bar);
-    tma_load_1d(t.sden, f.fden + cs.q0(), nb, t.bar);
+    if (HDR) tma_load_1d(t.sden, f.ghdr + cs.q0(), nb, t.bar);
+    else tma_load_1d(t.sden, f.fden + cs.q0(), nb, t.bar);
     tma_load_1d(t.sy, f.fy + cs.q0(), nb, t.bar);
   } else if (SLOTS && QF && !UNI && lane == 4) {
     tma_load_1d(t.sqf, f.qf + cs.f0(), mybytes, t.bar);
@@ -345,7 +349,8 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
 #define TLSPH_STREAM_L2PF 1
 #endif
   if (!SLOTS && TLSPH_STREAM_L2PF) {  // streamed slot block: bring it into L2 ahead of the chain's register loads
-    if (lane == 1) tma_prefetch_l2_stream(f.pf + cs.f0(), static_cast<uint32_t>((cs.f1() - cs.f0()) * 8));
+    if (lane == 1)
+      tma_prefetch_l2_stream((pf_src ? pf_src : f.pf) + cs.f0(), static_cast<uint32_t>((cs.f1() - cs.f0()) * 8));
     else if (lane == 2)
       tma_prefetch_l2_stream((nl_src ? nl_src : f.nloc) + cs.n0(), static_cast<uint32_t>((cs.n1() - cs.n0()) * 2));
   }
@@ -683,8 +688,10 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   locate_row<D>(f, c, lane, sstart, send);
   if (cs.p0 == cs.p1) return;
   stamp(blockIdx.x, 2);
-  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI>(f, t, cs, sstart, send, lane,
-                                                                    UNI ? f.nlocf : f.nloc);
+  constexpr bool SPREAD = UNI && TLSPH_SWEEP_SPREAD;  // bank-spread slot rows (state.cu k_spread_rows)
+  const double* const pf_rows = SPREAD ? f.pfsp : f.pf;
+  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI, SPREAD>(f, t, cs, sstart, send, lane,
+                                                                            UNI ? f.nlocf : f.nloc, pf_rows);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
@@ -694,7 +701,10 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   for (int d = 0; d < D; ++d) ct.sv[d] = t.sv[d];
   ct.smf = t.smf;
   if (STREAM) {
-    ct.pf = f.pf + cs.s0;
+    ct.pf = pf_rows + cs.s0;
+    ct.pfb = pf_rows;
+    ct.nlb = UNI ? f.nlocf : f.nloc;
+    ct.s0u = static_cast<unsigned>(cs.s0);
     ct.qf = nullptr;  // formed from 1/m (fast_chain_stream)
     ct.nl = (UNI ? f.nlocf : f.nloc) + cs.s0;
     ct.minv = f.minv_uniform;
@@ -705,6 +715,7 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
     ct.minv = f.minv_uniform;
   }
   ct.offs = t.soff + (cs.p0 - cs.o0());
+  ct.hdr = reinterpret_cast<const unsigned long long*>(t.sden) + (cs.p0 - cs.q0());
   ct.s0 = cs.s0;
   ct.diag = t.sdiag + (cs.p0 - cs.q0());
   ct.y = t.sy + (cs.p0 - cs.q0());
@@ -712,8 +723,8 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   ct.np = static_cast<int>(cs.p1 - cs.p0);
   ct.forward = ph.forward;
   ct.kb = kb;
-  if (STREAM) fast_chain_stream<D, K, UNI>(ct, lane);
-  else fast_chain<D, K, true, true, UNI>(ct, lane);
+  if (STREAM) fast_chain_stream<D, K, UNI, SPREAD>(ct, lane);
+  else fast_chain<D, K, true, true, UNI, SPREAD>(ct, lane);
   __syncwarp();
   stamp(blockIdx.x, 6);
 
@@ -1392,6 +1403,8 @@ Phase prepare_sweep(DevSystem& s, int scheme, double eta, double dt, bool from_s
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT,
                    "damping sweep needs every neighbour inside the 3^D cell stencil (neighbors.hpp:50-52)");
   if (s.colour_start.empty()) throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "damping sweep needs a neighbourhood");
+  if (s.nslots >= (1ll << 32))  // the streamed chain addresses slots by 32-bit index (180 GB hold < 2^32 of them)
+    throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "damping sweep: more than 2^32 - 1 neighbour slots on one device");
   const DFields f = s.fields();
   Phase ph{};
   ph.eta = eta;

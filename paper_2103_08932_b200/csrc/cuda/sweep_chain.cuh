@@ -37,7 +37,29 @@
 #endif
 #include <cstdint>
 
+// Bank-spread rows (UNI chains): the sweep's own copy of a row's slots (stencil index, pair
+// factor) is regrouped so that the 16 lanes of a half-warp gather from 16 distinct shared-memory
+// bank pairs (state.cu k_spread_rows); a per-particle header gives the group extents.
+#ifndef TLSPH_SWEEP_SPREAD
+#define TLSPH_SWEEP_SPREAD 1
+#endif
+
 namespace tlsph_cuda {
+
+// Slot of this lane in iteration u of a bank-spread row: half-warp h = lane / 16 reads group
+// g = 2u + h, positions [start_g, start_g+1) of the row. Header byte g = start_g (byte 0 = 0;
+// groups the row does not use start at cnt).
+template <int K>
+__device__ __forceinline__ void spread_slot(unsigned long long hdr, int cnt, int lane, int u, int& s, bool& v) {
+  const unsigned lo = static_cast<unsigned>(hdr), hi = static_cast<unsigned>(hdr >> 32);
+  const unsigned g = 2u * static_cast<unsigned>(u) + (static_cast<unsigned>(lane) >> 4);
+  // selector nibbles 1-3 are 0: they pick byte 0 of the header, which is zero
+  const int st = static_cast<int>(__byte_perm(lo, hi, g));
+  int en = static_cast<int>(__byte_perm(lo, hi, (g + 1) & 7));
+  if (2 * u + 2 >= 8 && (lane >> 4)) en = cnt;  // group 7 ends the row
+  s = st + (lane & 15);
+  v = s < en;
+}
 
 template <int D>
 struct ChainTile {
@@ -48,6 +70,10 @@ struct ChainTile {
   const double* smf;      // fast_chain_stream: staged stencil signed RN(1/m) (negative: clamped)
   double minv;            // fast_chain_stream<UNI>: the uniform RN(1/m); nl carries bit 15 = clamped j
   const long long* offs;  // offs[p] - s0 = cell-relative first slot of particle p
+  const unsigned long long* hdr;  // bank-spread rows: group extents per particle (spread_slot)
+  const uint16_t* nlb;    // fast_chain_stream: the body's slot arrays (index s0u + cell-relative slot)
+  const double* pfb;
+  unsigned s0u;
   long long s0;
   const double* diag;     // per-particle fold constants (NaN: constrained particle)
   const double* y;        // RN(1 / denominator)
@@ -122,9 +148,18 @@ __device__ __forceinline__ void chain_sum(double (&x)[D], int lane) {
   else warp_sum_vec<D>(x, lane);
 }
 
-template <int D, int K, bool SHUF = true, bool SCATTER = true, bool UNI = false>
+template <int D, int K, bool SHUF = true, bool SCATTER = true, bool UNI = false, bool SPREAD = false>
 __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
   const int np = t.np;
+  // slot of this lane in iteration u of row (hdr, cnt)
+  auto slot = [&](unsigned long long hdr, int cnt, int u, int& s, bool& v) {
+    if (SPREAD) {
+      spread_slot<K>(hdr, cnt, lane, u, s, v);
+    } else {
+      s = lane + u * 32;
+      v = s < cnt;
+    }
+  };
   auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
   auto row = [&](int p, int& lo, int& cnt) {
     lo = static_cast<int>(t.offs[p] - t.s0);
@@ -141,17 +176,20 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
   // next particle: raw loads
   int pk1 = np > 1 ? pidx(1) : pk, lo1, cnt1;
   row(pk1, lo1, cnt1);
+  unsigned long long hdr1 = SPREAD ? t.hdr[pk1] : 0ull;
   {
     int lo, cnt;
     row(pk, lo, cnt);
+    const unsigned long long hdr0 = SPREAD ? t.hdr[pk] : 0ull;
     diag = t.diag[pk];
     y = t.y[pk];
     skip = diag != diag || cnt == 0;
     upm = 0;
 #pragma unroll
     for (int u = 0; u < K; ++u) {
-      const int s = lane + u * 32;
-      const bool v = s < cnt;
+      int s;
+      bool v;
+      slot(hdr0, cnt, u, s, v);
       const int jr = v ? t.nl[lo + s] : t.lbase + pk;  // invalid lanes read i itself with b = 0
       const int j = UNI ? (jr & 0x7fff) : jr;
       const double q = UNI ? ((v && !(jr & 0x8000)) ? t.pf[lo + s] * t.minv : 0.0) : (v ? t.qf[lo + s] : 0.0);
@@ -173,8 +211,9 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     double pfn[K], qfn[K];
 #pragma unroll
     for (int u = 0; u < K; ++u) {
-      const int s = lane + u * 32;
-      const bool v = s < cnt1;
+      int s;
+      bool v;
+      slot(hdr1, cnt1, u, s, v);
       jn[u] = v ? t.nl[lo1 + s] : li1;
       pfn[u] = v ? t.pf[lo1 + s] : 0.0;
       if (!UNI) qfn[u] = v ? t.qf[lo1 + s] : 0.0;
@@ -183,6 +222,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     const int pk2 = kk + 2 < np ? pidx(kk + 2) : pk1;
     int lo2, cnt2;
     row(pk2, lo2, cnt2);
+    const unsigned long long hdr2 = SPREAD ? t.hdr[pk2] : 0ull;
 
     // the chain: gathers
     double vi[D], vq[K][D];
@@ -246,6 +286,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     pk1 = pk2;
     lo1 = lo2;
     cnt1 = cnt2;
+    hdr1 = hdr2;
   }
 }
 
@@ -259,7 +300,26 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
 #ifndef TLSPH_SWEEP_STREAM_HINT
 #define TLSPH_SWEEP_STREAM_HINT 0
 #endif
-template <int D, int K, bool UNI>
+// Measured alternatives of the streamed chain's pipeline (same-box A/B, profiles/r2c_sweep_spread.md;
+// cfg4 / cfg5-weak ms per sweep, default 9.64 / 17.98):
+// TLSPH_STREAM_ROTATE=0: the particle loop unrolled three times with the three raw buffers renamed
+//   statically instead of moved down the pipeline every iteration (fewer instructions, but
+//   10.11 / 19.05: three copies of the ~270-instruction body);
+// TLSPH_STREAM_U32=1: slot addresses as 32-bit indices into the body's arrays, one widening
+//   multiply-add per load instead of 64-bit pointer sums (10.15 / 18.80).
+#ifndef TLSPH_STREAM_ROTATE
+#define TLSPH_STREAM_ROTATE 1
+#endif
+#ifndef TLSPH_STREAM_U32
+#define TLSPH_STREAM_U32 0
+#endif
+template <int K>
+struct RawSlots {
+  int j[K];      // stencil index (UNI: bit 15 = clamped j)
+  double pf[K];  // pair factor
+};
+
+template <int D, int K, bool UNI, bool SPREAD = false>
 __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lane) {
   const int np = t.np;
   auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
@@ -269,15 +329,26 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     cnt = static_cast<int>(t.offs[p + 1] - t.s0) - lo;
   };
   // raw loads; UNI: j keeps bit 15 (clamped j) until mass_factors / coefficients strip it
-  auto load_raw = [&](int lo, int cnt, int li, int (&j)[K], double (&pf)[K]) {
+  auto load_raw = [&](int lo, int cnt, unsigned long long hdr, int li, RawSlots<K>& r) {
 #pragma unroll
     for (int u = 0; u < K; ++u) {
-      const int s = lane + u * 32;
-      const bool v = s < cnt;
-      // streaming loads: the slot block is read once per sweep (evict-first; the stencil
-      // velocities keep L2)
-      j[u] = v ? static_cast<int>(TLSPH_SWEEP_STREAM_HINT ? __ldcs(t.nl + lo + s) : t.nl[lo + s]) : li;
-      pf[u] = v ? (TLSPH_SWEEP_STREAM_HINT ? __ldcs(t.pf + lo + s) : t.pf[lo + s]) : 0.0;
+      int s;
+      bool v;
+      if (SPREAD) {
+        spread_slot<K>(hdr, cnt, lane, u, s, v);
+      } else {
+        s = lane + u * 32;
+        v = s < cnt;
+      }
+#if TLSPH_STREAM_U32
+      const unsigned g = t.s0u + static_cast<unsigned>(lo + s);
+      r.j[u] = v ? static_cast<int>(t.nlb[g]) : li;
+      r.pf[u] = v ? t.pfb[g] : 0.0;
+#else
+      // TLSPH_SWEEP_STREAM_HINT: streaming (evict-first) loads, A/B only
+      r.j[u] = v ? static_cast<int>(TLSPH_SWEEP_STREAM_HINT ? __ldcs(t.nl + lo + s) : t.nl[lo + s]) : li;
+      r.pf[u] = v ? (TLSPH_SWEEP_STREAM_HINT ? __ldcs(t.pf + lo + s) : t.pf[lo + s]) : 0.0;
+#endif
     }
   };
   auto mass_factors = [&](const int (&j)[K], const double (&pf)[K], double (&q)[K]) {
@@ -314,33 +385,36 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
   // particle 0: coefficients; particles 1, 2: raw loads in flight; particle 3: row extents
   int pk = pidx(0);
   int pk1 = pclamp(1), pk2 = pclamp(2), pk3 = pclamp(3);
-  int jn[K], jn2[K], lo1, cnt1, lo2, cnt2, lo3, cnt3;
-  double pfn[K], pfn2[K];
+  int lo1, cnt1, lo2, cnt2, lo3, cnt3;
+  RawSlots<K> ra, rb, rc;
   row(pk1, lo1, cnt1);
   row(pk2, lo2, cnt2);
   row(pk3, lo3, cnt3);
-  load_raw(lo1, cnt1, t.lbase + pk1, jn, pfn);
-  load_raw(lo2, cnt2, t.lbase + pk2, jn2, pfn2);
+  auto header = [&](int p) { return SPREAD ? t.hdr[p] : 0ull; };
+  unsigned long long hdr3 = header(pk3);
+  load_raw(lo1, cnt1, header(pk1), t.lbase + pk1, ra);
+  load_raw(lo2, cnt2, header(pk2), t.lbase + pk2, rb);
   {
-    int lo, cnt, j0[K];
-    double pf0[K], q0[K];
+    int lo, cnt;
+    RawSlots<K> r0;
+    double q0[K];
     row(pk, lo, cnt);
-    load_raw(lo, cnt, t.lbase + pk, j0, pf0);
+    load_raw(lo, cnt, header(pk), t.lbase + pk, r0);
     diag = t.diag[pk];
     y = t.y[pk];
-    mass_factors(j0, pf0, q0);
-    coefficients(j0, pf0, q0, cnt);
+    mass_factors(r0.j, r0.pf, q0);
+    coefficients(r0.j, r0.pf, q0, cnt);
   }
 
-  for (int kk = 0; kk < np; ++kk) {
+  // One particle: `use` holds particle kk+1's raw slots (loaded two iterations ago), `fill`
+  // receives particle kk+3's.
+  auto step = [&](int kk, RawSlots<K>& use, RawSlots<K>& fill) {
     const int li = t.lbase + pk;
-    // particle kk+3: raw loads (three iterations of latency cover)
-    int jn3[K];
-    double pfn3[K];
-    load_raw(lo3, cnt3, t.lbase + pk3, jn3, pfn3);
+    load_raw(lo3, cnt3, hdr3, t.lbase + pk3, fill);
     const int pk4 = pclamp(kk + 4);
     int lo4, cnt4;
     row(pk4, lo4, cnt4);
+    hdr3 = header(pk4);
 
     // the chain: gathers
     double vi[D], vq[K][D];
@@ -368,7 +442,7 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
 #endif
     chain_sum<D>(P, lane);
     double qfn[K];
-    mass_factors(jn, pfn, qfn);  // particle kk+1 (loaded an iteration ago)
+    mass_factors(use.j, use.pf, qfn);  // particle kk+1
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const double rate = P[d] * y;
@@ -386,14 +460,7 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
 
     diag = diag1;
     y = y1;
-    coefficients(jn, pfn, qfn, cnt1);
-#pragma unroll
-    for (int u = 0; u < K; ++u) {
-      jn[u] = jn2[u];
-      pfn[u] = pfn2[u];
-      jn2[u] = jn3[u];
-      pfn2[u] = pfn3[u];
-    }
+    coefficients(use.j, use.pf, qfn, cnt1);
     pk = pk1;
     pk1 = pk2;
     pk2 = pk3;
@@ -402,7 +469,29 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     cnt2 = cnt3;
     lo3 = lo4;
     cnt3 = cnt4;
+  };
+
+#if TLSPH_STREAM_ROTATE
+  for (int kk = 0; kk < np; ++kk) {
+    step(kk, ra, rc);
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      ra.j[u] = rb.j[u];
+      ra.pf[u] = rb.pf[u];
+      rb.j[u] = rc.j[u];
+      rb.pf[u] = rc.pf[u];
+    }
   }
+#else
+  for (int kk = 0;;) {
+    step(kk, ra, rc);
+    if (++kk >= np) break;
+    step(kk, rb, ra);
+    if (++kk >= np) break;
+    step(kk, rc, rb);
+    if (++kk >= np) break;
+  }
+#endif
 }
 
 }  // namespace tlsph_cuda

@@ -167,6 +167,8 @@ class DevSystem {
   void build_ordered_rows();
   DBuf<uint16_t> nloc;
   DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)
+  DBuf<double> pfsp;          // bank-spread rows: pf in the order of nlocf's regrouped rows
+  DBuf<unsigned long long> ghdr;  // ... and each row's group starts (k_spread_rows)
   bool uniform_mass = false;  // every particle has the same mass
   double minv_uniform = 0.0;  // RN(1/m) then
   double v0_uniform = 0.0;    // every V0 equal (> 0): that value; 0 otherwise (refresh_v0_uniform)
@@ -196,6 +198,7 @@ class DevSystem {
                 const double* dwdr0_h, const double* pf_h);
   void compute_sweep_stats();
   void refresh_minvf();  // also refreshes qf once the CSR exists
+  void build_spread_rows();  // nlocf, pfsp, ghdr: bank-spread rows of the FAST chain (uniform masses)
 
   // transfers (state.cu)
   void set_field(int field, const double* host);

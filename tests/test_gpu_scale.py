@@ -24,6 +24,7 @@ from oracle import oracle as O
 from paper_2103_08932_b200 import dev
 from paper_2103_08932_b200 import scenarios as S
 from paper_2103_08932_b200 import slabs
+from tests.fixtures import assert_slab_field
 
 pytestmark = pytest.mark.gpu
 
@@ -130,10 +131,13 @@ def test_cfg4_full_size_csr_and_first_20_steps():
     compare_loop(d, o, rd, ro, cfg, steps)
 
 
-def test_cfg5_weak_share_two_slabs_bitwise_undivided():
+@pytest.mark.parametrize("mode", ["ordered", "fast"])
+def test_cfg5_weak_share_two_slabs_bitwise_undivided(mode):
     """cfg5's weak-scaling share of one GPU (250^3 lattice, dp 0.004, 5-layer clamp): two x-slabs
     of it with the fused peer-store exchange and the device-side phase barrier give, after two
-    sweeps, exactly the velocities of the undivided body (bit for bit, owned and halo columns)."""
+    sweeps, the velocities of the undivided body, owned and halo columns: bit for bit in ORDERED
+    mode, within 1e-12 in FAST mode (a slab's bank-spread rows may sum in another order,
+    tests/fixtures.py assert_slab_field)."""
     dp, layers = 0.004, 250
     lo, hi = [0.0, 0.0, 0.0], [layers * dp, 1.0, 1.0]
     h = 1.3 * dp
@@ -144,7 +148,7 @@ def test_cfg5_weak_share_two_slabs_bitwise_undivided():
     v[cons == 1] = 0.0
     eta_t, dt = S.eta_for(h) / 0.2, 2e-5
     whole = dev.DeviceSystem(r0, dp ** 3, S.RHO0, h, cons)
-    whole.set_reduction("fast")
+    whole.set_reduction(mode)
     whole.set("v", v)
     whole.damping_sweep("particle_split", eta_t, dt, count=2)
     ref = whole.get("v")
@@ -155,14 +159,14 @@ def test_cfg5_weak_share_two_slabs_bitwise_undivided():
         assert np.array_equal(r0s, r0[part.ids])
         d = dev.DeviceSystem(r0s, dp ** 3, S.RHO0, h, cons[part.ids], grid=grid[:2])
         d.set_task_range(part.x0, part.x1)
-        d.set_reduction("fast")
+        d.set_reduction(mode)
         d.set("v", v[part.ids])
         systems.append(d)
         parts.append(part)
     slabs.link_peers(systems)
     slabs.sweep_linked(systems, "particle_split", eta_t, dt, count=2)
     for part, d in zip(parts, systems):
-        assert np.array_equal(d.get("v"), ref[part.ids])
+        assert_slab_field(d.get("v"), ref[part.ids], mode)
 
 
 def test_large_body_linear_kirchhoff_bitwise():

@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.fixtures import lattice_r0, random_velocities
+from tests.fixtures import assert_slab_field, lattice_r0, random_velocities
 from paper_2103_08932_b200 import slabs
 
 import oracle.oracle as orc
@@ -246,7 +246,7 @@ def test_device_slabs_equal_undivided_device(dim, world, mode):
     for s, d in zip(parts, systems):
         vv = d.get("v")
         own = (cols[s.ids] >= s.x0) & (cols[s.ids] < s.x1)
-        assert np.array_equal(vv[own], ref[s.ids[own]])
+        assert_slab_field(vv[own], ref[s.ids[own]], mode)
 
 
 @pytest.mark.gpu
@@ -274,9 +274,9 @@ def test_fused_peer_slabs_equal_undivided_device(dim, world, mode):
     for s, d in zip(parts, systems):
         vv = d.get("v")
         own = (cols[s.ids] >= s.x0) & (cols[s.ids] < s.x1)
-        assert np.array_equal(vv[own], ref[s.ids[own]])
+        assert_slab_field(vv[own], ref[s.ids[own]], mode)
         # halo columns hold the neighbours' current values too
-        assert np.array_equal(vv, ref[s.ids])
+        assert_slab_field(vv, ref[s.ids], mode)
 
 
 @pytest.mark.gpu
@@ -303,7 +303,7 @@ def test_linked_slabs_equal_undivided_device(dim, world, mode, scheme):
     assert el > 0.0
     ref = whole.get("v")
     for s, d in zip(parts, systems):
-        assert np.array_equal(d.get("v"), ref[s.ids])
+        assert_slab_field(d.get("v"), ref[s.ids], mode if scheme == "particle_split" else "ordered")
 
 
 @pytest.mark.gpu
@@ -505,13 +505,17 @@ def test_slab_loop_equals_undivided_device_loop(dim, world, mode, fused):
         sweeper = lambda scheme, et, dt: slabs.sweep_linked(systems, scheme, et, dt)  # noqa: E731
     out = slabs.run_loop(slabs.LocalGroup(engines, [(s.x0, s.x1) for s in parts]),
                          slabs.LoopSpec(mat, H, eta, alpha, steps, seed=seed), dim, sweeper=sweeper)
-    assert out["damped"] == ref["damped"] > 0 and out["t"] == ref["t"] and out["last_dt"] == ref["last_dt"]
+    assert out["damped"] == ref["damped"] > 0
+    if mode == "ordered":
+        assert out["t"] == ref["t"] and out["last_dt"] == ref["last_dt"]
+    else:  # FAST: the step size follows max |v|, |a| of fields equal to 1e-12 (assert_slab_field)
+        assert math.isclose(out["t"], ref["t"], rel_tol=1e-12) and math.isclose(out["last_dt"], ref["last_dt"], rel_tol=1e-12)
     cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
     for name in ("v", "r", "F", "dFdt", "rho", "a"):
         want = whole.get(name)
         for s, e in zip(parts, engines):
             own = (cols[s.ids] >= s.x0) & (cols[s.ids] < s.x1)
-            assert np.array_equal(e.d.get(name)[own], want[s.ids[own]]), name
+            assert_slab_field(e.d.get(name)[own], want[s.ids[own]], mode, name)
 
 
 # ---------------------------------------------------------------- cross-process phase handshake
@@ -600,7 +604,8 @@ def test_ipc_slabs_equal_undivided_device(tmp_path, dim, world, mode, scheme):
     ref = whole.get("v")
     for r in range(world):
         ids = np.load(os.path.join(tmp_path, f"ids{r}.npy"))
-        assert np.array_equal(np.load(os.path.join(tmp_path, f"v{r}.npy")), ref[ids])
+        assert_slab_field(np.load(os.path.join(tmp_path, f"v{r}.npy")), ref[ids],
+                          mode if scheme == "particle_split" else "ordered")
 
 
 def _ipc_loop_rank(rank, world, port, dim, mode, result_dir):
@@ -665,11 +670,12 @@ def test_ipc_slab_loop_equals_undivided_device_loop(tmp_path, dim, world, mode):
     cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
     for r in range(world):
         z = np.load(os.path.join(tmp_path, f"r{r}.npz"))
-        assert float(z["t"]) == ref["t"] and int(z["damped"]) == ref["damped"] > 0
+        assert int(z["damped"]) == ref["damped"] > 0
+        assert float(z["t"]) == ref["t"] if mode == "ordered" else math.isclose(float(z["t"]), ref["t"], rel_tol=1e-12)
         ids = z["ids"]
         own = (cols[ids] >= int(z["x0"])) & (cols[ids] < int(z["x1"]))
         for name in ("v", "r", "F", "dFdt", "rho", "a"):
-            assert np.array_equal(z[name][own], whole.get(name)[ids[own]]), (r, name)
+            assert_slab_field(z[name][own], whole.get(name)[ids[own]], mode, (r, name))
 
 
 @pytest.mark.parametrize("lo,hi,world", [([0, 0, 0], [0.4, 0.1, 0.08], 3), ([0, -0.2, -0.2], [0.8, 0.2, 0.2], 4),
@@ -915,8 +921,9 @@ def test_c_group_loop_equals_undivided_device_loop(tmp_path, dim, world, mode):
     cols = slabs.cell_columns(r0, grid[0], grid[2], grid[1][0])
     for r in range(world):
         z = np.load(os.path.join(tmp_path, f"r{r}.npz"))
-        assert float(z["t"]) == ref["t"] and int(z["damped"]) == ref["damped"] > 0
+        assert int(z["damped"]) == ref["damped"] > 0
+        assert float(z["t"]) == ref["t"] if mode == "ordered" else math.isclose(float(z["t"]), ref["t"], rel_tol=1e-12)
         ids = z["ids"]
         own = (cols[ids] >= int(z["x0"])) & (cols[ids] < int(z["x1"]))
         for name in ("v", "r", "F", "dFdt", "rho", "a"):
-            assert np.array_equal(z[name][own], whole.get(name)[ids[own]]), (r, name)
+            assert_slab_field(z[name][own], whole.get(name)[ids[own]], mode, (r, name))
