@@ -1120,6 +1120,17 @@ void launch_fast_impl(const DevSystem& s, const DFields& f, Phase ph) {
       if (cap > smem && static_cast<size_t>(ps) * (smem + kReserve) <= kSmemSM) smem = std::min<size_t>(cap, 200 * 1024);
     }
   }
+  {
+    // measurement knob: at most TLSPH_SWEEP_MAXCELLS cell tasks resident per SM (tile padded)
+    static const int max_cells = [] {
+      const char* e = std::getenv("TLSPH_SWEEP_MAXCELLS");
+      return e && *e ? std::atoi(e) : 0;
+    }();
+    if (max_cells > 0) {
+      const size_t cap = ((228 * 1024) / static_cast<size_t>(max_cells) - 1024) & ~static_cast<size_t>(127);
+      if (cap > smem) smem = std::min<size_t>(cap, 200 * 1024);
+    }
+  }
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     CK(cudaFuncSetAttribute(k_sweep_fast<D, K, STREAM, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
