@@ -293,8 +293,15 @@ struct CellSpan {
 // divisions, pairwise).
 // HDR: the bank-spread rows' per-particle headers take the place of the fold denominators (unused
 // by the FAST chain).
+// TROWS (velocities only: QF, no MASS): each stencil row's velocities by one bulk copy per
+// component (lane q < 3^(D-1) issues row q's) on the same mbarrier, instead of per-lane 16-byte
+// cp.async over the flattened row table -- no per-pair address arithmetic (~1,000 instructions
+// per cell) and no LSU wavefronts for the shared-memory writes.
+#ifndef TLSPH_SWEEP_TROWS
+#define TLSPH_SWEEP_TROWS 1
+#endif
 template <int D, bool FOLD, bool MASS, bool PDL = false, bool QF = false, bool SLOTS = true, bool UNI = false,
-          bool HDR = false>
+          bool HDR = false, bool TROWS = false>
 __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t, const CellSpan& cs,
                                               long long sstart, long long send, int lane,
                                               const uint16_t* nl_src = nullptr, const double* pf_src = nullptr) {
@@ -323,8 +330,9 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   uint32_t total = mybytes;
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+  static_assert(!TROWS || (QF && !MASS), "bulk row copies stage velocities only");
   if (lane == 0) {
-    mbar_init(t.bar, 1);
+    mbar_init(t.bar, TROWS ? 2 : 1);  // TROWS: the static data and the rows arrive separately
     fence_proxy_async_smem();  // the initialised barrier is visible to the TMA unit
     mbar_arrive_expect_tx(t.bar, total);
   }
@@ -355,6 +363,26 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
       tma_prefetch_l2_stream((nl_src ? nl_src : f.nloc) + cs.n0(), static_cast<uint32_t>((cs.n1() - cs.n0()) * 2));
   }
   stamp(blockIdx.x, 3);
+  constexpr int center = D == 2 ? 1 : 4;
+  if (TROWS) {
+    const uint32_t row_bytes = lane < kSegs ? static_cast<uint32_t>(plen) * 8u : 0u;
+    uint32_t rows_total = row_bytes;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) rows_total += __shfl_xor_sync(kFull, rows_total, o);  // lanes 0-15 hold the rows
+    const int lbase_t =
+        __shfl_sync(kFull, sbase, center) + static_cast<int>(cs.p0 - __shfl_sync(kFull, sstart, center));
+    if (lane == 0) reinterpret_cast<int*>(t.bar + 1)[0] = lbase_t;
+    if (PDL) grid_dependency_wait();  // the velocities are written by the preceding phase
+    if (lane == 0) mbar_arrive_expect_tx(t.bar, rows_total * D);
+    __syncwarp();
+    if (row_bytes) {
+      const long long g = sstart - par;
+      const int tb = sbase - par;
+#pragma unroll
+      for (int d = 0; d < D; ++d) tma_load_1d(t.sv[d] + tb, f.v[d] + g, row_bytes, t.bar);
+    }
+    return;
+  }
   const RowPairs rp = row_pairs(sstart, lane < kSegs ? slen : 0, sbase, lane);
   auto copy_pair = [&](long long g, int tt) {
 #pragma unroll
@@ -400,7 +428,6 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
       if (p < rp.total) copy_pair(g, tt);
     }
   }
-  constexpr int center = D == 2 ? 1 : 4;
   const int lbase =
       __shfl_sync(kFull, sbase, center) + static_cast<int>(cs.p0 - __shfl_sync(kFull, sstart, center));
   if (lane == 0) reinterpret_cast<int*>(t.bar + 1)[0] = lbase;  // the centre row holds the cell's particles
@@ -690,8 +717,10 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   stamp(blockIdx.x, 2);
   constexpr bool SPREAD = UNI && TLSPH_SWEEP_SPREAD;  // bank-spread slot rows (state.cu k_spread_rows)
   const double* const pf_rows = SPREAD ? f.pfsp : f.pf;
-  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI, SPREAD>(f, t, cs, sstart, send, lane,
-                                                                            UNI ? f.nlocf : f.nloc, pf_rows);
+  // bulk row copies for the streamed (large-body) form only: with a handful of cells per SM the
+  // serialised bulk issue costs the latency-bound chain more than it saves (cfg2 0.635 -> 0.684 ms)
+  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI, SPREAD, STREAM && UNI && TLSPH_SWEEP_TROWS>(
+      f, t, cs, sstart, send, lane, UNI ? f.nlocf : f.nloc, pf_rows);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
