@@ -454,17 +454,38 @@ __device__ __forceinline__ M<D> second_pk(const M<D>& F, double J, const DMateri
 template <int D>
 __host__ __device__ constexpr int pbv_stride() { return D == 3 ? 10 : 6; }
 
-// Layout of DFields::pbv: component c of particle p. Chunk-major: the 16-byte chunk
-// (components 2k, 2k+1) of every particle is contiguous, so the momentum pass's gather of a
-// chunk for the 32 neighbours a warp holds touches few 128-byte lines (neighbour indices come
-// in runs); an 80-byte record per particle made every chunk load touch every record's line.
+// Layout of DFields::pbv: component c of particle p. Chunk-major: a chunk of every particle is
+// contiguous, so the momentum pass's gather of a chunk for the 32 neighbours a warp holds touches
+// few 128-byte lines (neighbour indices come in runs); an 80-byte record per particle made every
+// chunk load touch every record's line. 3D (TLSPH_PBV_WIDE): two 32-byte chunks (components 0-3,
+// 4-7) and one 16-byte chunk (8, 9), gathered by two 256-bit loads and one 128-bit load instead of
+// five 128-bit loads (fewer L1 tag lookups, the pass's bound). 2D: three 16-byte chunks.
+#ifndef TLSPH_PBV_WIDE
+#define TLSPH_PBV_WIDE 1
+#endif
 template <int D>
 __host__ __device__ __forceinline__ long long pbv_at(long long n, long long p, int c) {
 #ifdef TLSPH_PBV_AOS
   return p * pbv_stride<D>() + c;
 #else
+  if (D == 3 && TLSPH_PBV_WIDE) return c < 8 ? 4 * ((c >> 2) * n + p) + (c & 3) : 8 * n + 2 * p + (c - 8);
   return 2 * ((c >> 1) * n + p) + (c & 1);
 #endif
+}
+
+// The packed 3D record of particle j (TLSPH_PBV_WIDE layout) into rec[0..9].
+__device__ __forceinline__ void pbv_gather3(const double* __restrict__ pbv, long long n, long long j, double* rec) {
+  const double* q0 = pbv + 4 * j;
+  const double* q1 = pbv + 4 * (n + j);
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(rec[0]), "=d"(rec[1]), "=d"(rec[2]), "=d"(rec[3])
+               : "l"(q0));
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(rec[4]), "=d"(rec[5]), "=d"(rec[6]), "=d"(rec[7])
+               : "l"(q1));
+  const double2 x = __ldg(reinterpret_cast<const double2*>(pbv + 8 * n + 2 * j));
+  rec[8] = x.x;
+  rec[9] = x.y;
 }
 
 template <int D>

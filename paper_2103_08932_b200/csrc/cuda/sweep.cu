@@ -1685,11 +1685,11 @@ void enqueue_sweep_d(DevSystem& s, int scheme, double eta, double dt, bool from_
 // ------------------------------------------------------------------ x-slab halo columns
 // Particles of cell column x in (z, y, cell order): the same sequence on every
 // rank that holds the column (cells keep ascending reference ids).
-// Component c of particle p of a column field lives at ptr[c][p * stride].
+// Component c of particle p of a column field lives at ptr[c][p * stride[c]].
 struct ColumnField {
   double* ptr[10];
   int ncomp;
-  long long stride;
+  long long stride[10];
 };
 
 __global__ void k_column_copy(const long long* __restrict__ cell_start, const long long* __restrict__ col_off,
@@ -1702,7 +1702,7 @@ __global__ void k_column_copy(const long long* __restrict__ cell_start, const lo
   const long long o = col_off[q];
   for (long long e = threadIdx.x; e < p1 - p0; e += blockDim.x)
     for (int c = 0; c < cf.ncomp; ++c) {
-      double* a = cf.ptr[c] + (p0 + e) * cf.stride;
+      double* a = cf.ptr[c] + (p0 + e) * cf.stride[c];
       if (pack) buf[c * count + o + e] = *a;
       else *a = buf[c * count + o + e];
     }
@@ -2041,14 +2041,18 @@ ColumnField column_field(const DevSystem& s, int field) {
   ColumnField cf{};
   if (field == TLSPH_DEV_COLUMN_VELOCITY) {
     cf.ncomp = s.D;
-    cf.stride = 1;
-    for (int d = 0; d < s.D; ++d) cf.ptr[d] = s.v[d].p;
+    for (int d = 0; d < s.D; ++d) {
+      cf.ptr[d] = s.v[d].p;
+      cf.stride[d] = 1;
+    }
   } else if (field == TLSPH_DEV_COLUMN_STRESS) {
     cf.ncomp = s.D * s.D + 1;  // P B0 row-major, V0 (the packed momentum-gather record)
-    // component c of particle p at pbv_at(n, p, c) = ptr[c] + p * stride
+    // component c of particle p at pbv_at(n, p, c) = ptr[c] + p * stride[c]
     const auto at = [&](long long p, int c) { return s.D == 2 ? pbv_at<2>(s.n, p, c) : pbv_at<3>(s.n, p, c); };
-    cf.stride = at(1, 0) - at(0, 0);
-    for (int c = 0; c < cf.ncomp; ++c) cf.ptr[c] = s.pbv.p + at(0, c);
+    for (int c = 0; c < cf.ncomp; ++c) {
+      cf.ptr[c] = s.pbv.p + at(0, c);
+      cf.stride[c] = at(1, c) - at(0, c);
+    }
   } else {
     throw DevError(TLSPH_ERR_INVALID_ARGUMENT, "unknown column field " + std::to_string(field));
   }
@@ -2084,7 +2088,7 @@ __global__ void k_column_push(const long long* __restrict__ cell_start, int x, i
     const int pi = peer_idx[p];
     if (pi == -1) continue;
     const long long idx = pi >= 0 ? pi : -2 - pi;
-    for (int c = 0; c < src.ncomp; ++c) dst.ptr[c][idx * dst.stride] = src.ptr[c][p * src.stride];
+    for (int c = 0; c < src.ncomp; ++c) dst.ptr[c][idx * dst.stride[c]] = src.ptr[c][p * src.stride[c]];
   }
 }
 
@@ -2094,13 +2098,17 @@ ColumnField peer_column_field(const DevSystem& s, int side, int field) {
   const IpcPeer& ip = s.ipc_peer[side];
   if (field == TLSPH_DEV_COLUMN_VELOCITY) {
     cf.ncomp = s.D;
-    cf.stride = 1;
-    for (int d = 0; d < s.D; ++d) cf.ptr[d] = s.peer_v[side][d];
+    for (int d = 0; d < s.D; ++d) {
+      cf.ptr[d] = s.peer_v[side][d];
+      cf.stride[d] = 1;
+    }
   } else {
     cf.ncomp = s.D * s.D + 1;
     const auto at = [&](long long p, int c) { return s.D == 2 ? pbv_at<2>(ip.n, p, c) : pbv_at<3>(ip.n, p, c); };
-    cf.stride = at(1, 0) - at(0, 0);
-    for (int c = 0; c < cf.ncomp; ++c) cf.ptr[c] = ip.pbv + at(0, c);
+    for (int c = 0; c < cf.ncomp; ++c) {
+      cf.ptr[c] = ip.pbv + at(0, c);
+      cf.stride[c] = at(1, c) - at(0, c);
+    }
   }
   return cf;
 }

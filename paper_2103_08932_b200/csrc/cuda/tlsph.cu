@@ -418,11 +418,15 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
 #ifdef TLSPH_PROBE_NOGATHER  // measurement probe only: the pass without its neighbour-record gather
           const double2 x = make_double2(pbi[2 * k] + j[u], pbi[2 * k + 1]);
 #else
+          if (D == 3 && TLSPH_PBV_WIDE) break;  // gathered below
           const double2 x = __ldg(reinterpret_cast<const double2*>(f.pbv + pbv_at<D>(f.n, j[u], 2 * k)));
 #endif
           pbj[u][2 * k] = x.x;
           pbj[u][2 * k + 1] = x.y;
         }
+#ifndef TLSPH_PROBE_NOGATHER
+        if constexpr (D == 3 && TLSPH_PBV_WIDE) pbv_gather3(f.pbv, f.n, j[u], pbj[u]);
+#endif
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
