@@ -1,10 +1,15 @@
 #!/bin/bash
-# Round-2c GPU pass: parity suite, staged/streamed choice for cfg3 with bank-spread rows, ncu --set
-# full of one streamed cfg4 sweep phase (bank-spread rows) next to the slot-order variant library.
+# Round-2c record pass (one GPU): the bench line, its ncu launch list, ncu --set full of passes B and
+# C and of one streamed sweep phase on cfg4 (the headline workload), and the cfg5-weak sweep phase.
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 o=gpurun_out/r2c; mkdir -p $o
-python -m pytest tests -m gpu -q > $o/gputest.log 2>&1; echo "rc=$?" >> $o/gputest.log; tail -15 $o/gputest.log | cut -c1-180
-for st in 0 1; do TLSPH_SWEEP_STREAM=$st python tools/sweep_sizes.py cfg2 cfg3 --sweeps 20; done 2>&1 | tee $o/cfg3_stream_ab.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_fast -s 30 -c 1 -o $o/cfg4_sweep_spread \
+python bench.py > $o/bench.json 2> $o/bench.err; echo "bench rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $o/launches.csv \
+   python bench.py --steps 2 --warmup 1 --no-cpu --no-legs --no-e2e > $o/launch_run.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_momentum_ordered|k_deformation_rate_ordered" -s 2 -c 2 -o $o/cfg4_tl \
+   python tools/cfg_steps.py cfg4 --steps 2 --sweeps 0 > $o/cfg4_tl_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_fast -s 30 -c 1 -o $o/cfg4_sweep \
    python tools/cfg_steps.py cfg4 --steps 0 --sweeps 1 > $o/cfg4_sweep_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:k_sweep_fast -s 30 -c 1 -o $o/cfg5w_sweep \
+   python tools/cfg_steps.py cfg5_weak --steps 0 --sweeps 1 > $o/cfg5w_sweep_ncu.log 2>&1
 ls -la $o
