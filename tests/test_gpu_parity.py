@@ -295,6 +295,49 @@ def test_sweep_irregular_bodies(case, mode, scheme):
     assert np.all(d.get("v")[cons == 1] == 0.0)
 
 
+@pytest.mark.parametrize("tiling", ["staged", "streamed"])
+def test_fast_sweep_follows_clamp_and_mass_changes(tiling):
+    """The FAST chain reads its own regrouped copy of the slot rows (bank-spread rows, state.cu
+    k_spread_rows: stencil index + clamp bit, pair factor) when every mass is equal, and the
+    per-slot / per-stencil mass factors otherwise; the copy must follow clamp flags and masses set
+    after construction (damping.cpp:84-86, :151 read them at every sweep)."""
+    rng = np.random.RandomState(4)
+    base = lattice_r0([14, 12, 10], 0.01)
+    r0 = base + rng.uniform(-0.003, 0.003, base.shape)
+    n = len(r0)
+    o, d = pair(r0, 1e-6, 1000.0, 0.013)
+    d.set_reduction("fast")
+    d.set_sweep_tiling(tiling)
+    v = random_velocities(n, 3, 1.0, 33)
+
+    def sweep_and_compare(cons):
+        vv = v.copy()
+        vv[cons == 1] = 0.0
+        for s in (o, d):
+            s.set("v", vv)
+        for _ in range(2):
+            o.damping_sweep("particle_split", 300.0, 1e-4)
+            d.damping_sweep("particle_split", 300.0, 1e-4)
+        assert rel_l2(d.get("v"), o.get("v")) <= TOL
+        assert np.all(d.get("v")[cons == 1] == 0.0)
+
+    none = np.zeros(n, np.uint8)
+    sweep_and_compare(none)                                  # uniform masses, nothing clamped
+    cons = (r0[:, 0] < 0.03).astype(np.uint8)
+    for s in (o, d):
+        s.set("constrained", cons.astype(np.float64))
+    sweep_and_compare(cons)                                  # clamp bits rebuilt
+    m = 1e-3 * (1.0 + 0.5 * rng.uniform(size=n))
+    for s in (o, d):
+        s.set("m", m)
+    sweep_and_compare(cons)                                  # per-particle masses: slot-order rows
+    cons2 = (r0[:, 1] > 0.08).astype(np.uint8)
+    for s in (o, d):
+        s.set("m", np.full(n, 1e-3))
+        s.set("constrained", cons2.astype(np.float64))
+    sweep_and_compare(cons2)                                 # uniform again, other clamp set
+
+
 def test_sweep_zero_eta_noop_and_explicit_rejected():
     r0 = lattice_r0([5, 5], 0.01)
     d = dev.DeviceSystem(r0, 1e-4, 1000.0, 0.013)
