@@ -1096,7 +1096,7 @@ void launch_pairwise_any(const DevSystem& s, const DFields& f, const Phase& ph) 
 // Staged or streamed slot block (tlsph_dev_set_sweep_tiling); AUTO: streamed
 // when the colour's cells exceed two waves of staged tiles
 // (TLSPH_SWEEP_STREAM=0/1 overrides AUTO, for A/B runs).
-inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_bytes) {
+inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_bytes, int waves = 2) {
   if (s.sweep_tiling != TLSPH_SWEEP_TILING_AUTO) return s.sweep_tiling == TLSPH_SWEEP_TILING_STREAMED;
   static const int force = [] {
     const char* e = std::getenv("TLSPH_SWEEP_STREAM");
@@ -1109,7 +1109,7 @@ inline bool stream_slots(const DevSystem& s, const Phase& ph, size_t staged_byte
   // measured crossover: staged still wins at ~1.6 waves (cfg3: 1.133 vs 1.188 ms per sweep) and
   // loses from ~11 waves on (cfg4 12.5 vs 10.4, cfg5-weak 24.2 vs 18.0)
   const long long per_sm = std::max<long long>(1, static_cast<long long>((228 * 1024) / (staged_bytes + 1024)));
-  return std::max(ph.ncol, ph.ncol_colour) > 2 * per_sm * sms;
+  return std::max(ph.ncol, ph.ncol_colour) > waves * per_sm * sms;
 }
 
 inline bool uniform_disabled() {  // TLSPH_SWEEP_UNIFORM=0: the stencil-1/m form even for uniform masses (A/B)
@@ -1233,7 +1233,11 @@ void launch_flow(const DevSystem& s, const DFields& f, const Phase& ph, const Fl
 // component d's terms in slot order (the D folds run side by side), and the rate (corrected
 // division), v_i and the scatter follow for all components at once. One pass over the slot
 // metadata per particle instead of one per component warp (k_sweep_phase).
-template <int D, int K>
+// STREAM (large bodies, as k_sweep_fast<STREAM>): the slot block (pair factors, stencil indices)
+// is not staged but read from global memory one particle ahead (the `meta` prefetch below), after
+// a bulk L2 prefetch of the cell's block; the tile shrinks to the stencil's velocities and masses,
+// so about twice as many cells share an SM. Same arithmetic, same order: bit-identical.
+template <int D, int K, bool STREAM = false>
 __global__ void __launch_bounds__(kWarp)
 k_sweep_ordered(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   if (ph.dt_from_scalars && sc->halt) return;
@@ -1250,14 +1254,14 @@ k_sweep_ordered(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   long long sstart, send;
   locate_row<D>(f, c, lane, sstart, send);
   if (cs.p0 == cs.p1) return;
-  issue_staging<D, true, true, true>(f, t, cs, sstart, send, lane);
+  issue_staging<D, true, true, true, false, !STREAM>(f, t, cs, sstart, send, lane);
   wait_staging(t);
   __syncwarp();
   const int lbase = reinterpret_cast<const int*>(t.bar + 1)[0];
   const long long s0 = cs.s0;
   const long long* offc = t.soff + (cs.p0 - cs.o0());
-  const double* pfc = t.spf + (s0 - cs.f0());
-  const uint16_t* nlc = t.snl + (s0 - cs.n0());
+  const double* pfc = STREAM ? f.pf + s0 : t.spf + (s0 - cs.f0());
+  const uint16_t* nlc = STREAM ? f.nloc + s0 : t.snl + (s0 - cs.n0());
   const double* fdg = t.sdiag + (cs.p0 - cs.q0());
   const double* fdn = t.sden + (cs.p0 - cs.q0());
   const double* fyy = t.sy + (cs.p0 - cs.q0());
@@ -1386,6 +1390,23 @@ inline bool ordered_warps() {  // TLSPH_SWEEP_ORDERED_WARPS=1: one warp per comp
 
 template <int D, int K>
 void launch_ordered(const DevSystem& s, const DFields& f, Phase ph) {
+  // large bodies: the slot block streamed from global memory (the staged / streamed choice of
+  // the FAST kernel: tlsph_dev_set_sweep_tiling, AUTO beyond two waves of staged tiles)
+  // (ORDERED crossover: cfg3, 3.3 waves of staged tiles, 2.87 ms staged vs 3.37 streamed; cfg4,
+  // 39 waves, 38.2 vs 28.0)
+  if (stream_slots(s, ph, tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast), 8)) {
+    ph.SC = 0;  // no slot block in the tile
+    const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
+    static size_t configured_s = 0;
+    if (smem > 48 * 1024 && smem > configured_s) {
+      CK(cudaFuncSetAttribute(k_sweep_ordered<D, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem)));
+      configured_s = smem;
+    }
+    launch_pdl_phase(k_sweep_ordered<D, K, true>, static_cast<unsigned>(ph.ncol), kWarp, smem, s.stream, f, ph,
+                     s.scal.p);
+    return;
+  }
   const size_t smem = tile_bytes<D>(ph.S, ph.SC, ph.MC, ph.MR, ph.fast);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
