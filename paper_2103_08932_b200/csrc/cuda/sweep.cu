@@ -293,7 +293,7 @@ struct CellSpan {
 // divisions, pairwise).
 // HDR: the bank-spread rows' per-particle headers take the place of the fold denominators (unused
 // by the FAST chain).
-// TROWS (velocities only: QF, no MASS): each stencil row's velocities by one bulk copy per
+// TROWS (no MASS): each stencil row's velocities (and, without QF, its 1/m) by one bulk copy per
 // component (lane q < 3^(D-1) issues row q's) on the same mbarrier, instead of per-lane 16-byte
 // cp.async over the flattened row table -- no per-pair address arithmetic (~1,000 instructions
 // per cell) and no LSU wavefronts for the shared-memory writes.
@@ -330,7 +330,7 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
   uint32_t total = mybytes;
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
-  static_assert(!TROWS || (QF && !MASS), "bulk row copies stage velocities only");
+  static_assert(!TROWS || !MASS, "bulk row copies stage the velocities and, without QF, the stencil's 1/m");
   if (lane == 0) {
     mbar_init(t.bar, TROWS ? 2 : 1);  // TROWS: the static data and the rows arrive separately
     fence_proxy_async_smem();  // the initialised barrier is visible to the TMA unit
@@ -373,13 +373,14 @@ __device__ __forceinline__ void issue_staging(const DFields& f, const Tile<D>& t
         __shfl_sync(kFull, sbase, center) + static_cast<int>(cs.p0 - __shfl_sync(kFull, sstart, center));
     if (lane == 0) reinterpret_cast<int*>(t.bar + 1)[0] = lbase_t;
     if (PDL) grid_dependency_wait();  // the velocities are written by the preceding phase
-    if (lane == 0) mbar_arrive_expect_tx(t.bar, rows_total * D);
+    if (lane == 0) mbar_arrive_expect_tx(t.bar, rows_total * (QF ? D : D + 1));
     __syncwarp();
     if (row_bytes) {
       const long long g = sstart - par;
       const int tb = sbase - par;
 #pragma unroll
       for (int d = 0; d < D; ++d) tma_load_1d(t.sv[d] + tb, f.v[d] + g, row_bytes, t.bar);
+      if (!QF) tma_load_1d(t.smf + tb, f.minvf + g, row_bytes, t.bar);
     }
     return;
   }
@@ -719,7 +720,7 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   const double* const pf_rows = SPREAD ? f.pfsp : f.pf;
   // bulk row copies for the streamed (large-body) form only: with a handful of cells per SM the
   // serialised bulk issue costs the latency-bound chain more than it saves (cfg2 0.635 -> 0.684 ms)
-  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI, SPREAD, STREAM && UNI && TLSPH_SWEEP_TROWS>(
+  issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI, SPREAD, STREAM && TLSPH_SWEEP_TROWS>(
       f, t, cs, sstart, send, lane, UNI ? f.nlocf : f.nloc, pf_rows);
   stamp(blockIdx.x, 4);
   wait_staging(t);
