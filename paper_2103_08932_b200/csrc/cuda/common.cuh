@@ -173,6 +173,11 @@ struct DFields {
 __device__ __forceinline__ bool is_owned(const DFields& f, long long i) { return !f.own || f.own[i]; }
 
 constexpr int kWarp = 32;
+// 3D slot-order neighbour passes: (dW/dr0, e0) of a slot as one 32-byte record of the interleaved
+// copy (DFields::odw holds 4 doubles per slot, oe0 unused); 0: four separate arrays (A/B)
+#ifndef TLSPH_TL_SLOTREC
+#define TLSPH_TL_SLOTREC 1
+#endif
 // FAST particle-split chain on bank-spread slot rows (state.cu k_spread_rows, sweep_chain.cuh);
 // 0: rows in slot order (A/B)
 #ifndef TLSPH_SWEEP_SPREAD

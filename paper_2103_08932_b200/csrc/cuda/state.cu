@@ -552,6 +552,11 @@ __global__ void k_interleave_rows(DFields f, const long long* __restrict__ gbase
   for (long long k = 0; k < cnt; ++k) {
     const long long src = lo + k, dst = base + 32 * k;
     onbr[dst] = f.nbr[src];
+    if (D == 3 && TLSPH_TL_SLOTREC) {  // one 32-byte record per slot (tlsph.cu SlotView::load)
+      *reinterpret_cast<double4*>(odw + 4 * dst) =
+          make_double4(f.dwdr0[src], f.e0[0][src], f.e0[1][src], f.e0[2][src]);
+      continue;
+    }
     odw[dst] = f.dwdr0[src];
     oe0x[dst] = f.e0[0][src];
     oe0y[dst] = f.e0[1][src];
@@ -1114,8 +1119,12 @@ void DevSystem::build_ordered_rows() {
   ogbase.alloc(gb.size());
   CK(cudaMemcpyAsync(ogbase.p, gb.data(), gb.size() * sizeof(long long), cudaMemcpyHostToDevice, stream));
   onbr.alloc(total);
-  odw.alloc(total);
-  for (int d = 0; d < D; ++d) oe0[d].alloc(total);
+  if (D == 3 && TLSPH_TL_SLOTREC) {
+    odw.alloc(4 * total);  // (dW/dr0, e0) records
+  } else {
+    odw.alloc(total);
+    for (int d = 0; d < D; ++d) oe0[d].alloc(total);
+  }
   const DFields f = fields();
   if (D == 2)
     k_interleave_rows<2><<<grid_for(n, 256), 256, 0, stream>>>(f, ogbase.p, onbr.p, odw.p, oe0[0].p, oe0[1].p, nullptr);

@@ -140,6 +140,19 @@ struct SlotView {
   __device__ __forceinline__ double e(int d, long long su) const {
     return TLSPH_TL_STREAM_HINT ? __ldcs(e0[d] + su) : e0[d][su];
   }
+  // (dW/dr0, e0) of slot su. 3D slot-order passes (TLSPH_TL_SLOTREC): one 32-byte record per slot
+  // in the interleaved copy (build_ordered_rows), one 256-bit load instead of four 64-bit loads.
+  __device__ __forceinline__ void load(long long su, double& dwv, double (&ev)[D]) const {
+    if constexpr (OI && D == 3 && TLSPH_TL_SLOTREC) {
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(dwv), "=d"(ev[0]), "=d"(ev[1]), "=d"(ev[2])
+                   : "l"(dw + 4 * su));
+    } else {
+      dwv = w(su);
+#pragma unroll
+      for (int d = 0; d < D; ++d) ev[d] = e(d, su);
+    }
+  }
 };
 
 // PDL (FAST passes B and C): launched with programmatic stream serialization, the kernel lets
@@ -178,9 +191,7 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
         const bool ok = s + u * G < hi;
         const long long su = sv.at(f, ob_i, lo_i, ok ? s + u * G : s);
         j[u] = sv.nb(su);
-        dw[u] = sv.w(su);
-#pragma unroll
-        for (int d = 0; d < D; ++d) e[u][d] = sv.e(d, su);
+        sv.load(su, dw[u], e[u]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -404,9 +415,7 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
       for (int u = 0; u < U; ++u) {
         const long long su = sv.at(f, ob_i, lo_i, s + u * G < hi ? s + u * G : s);
         j[u] = sv.nb(su);
-        dw[u] = sv.w(su);
-#pragma unroll
-        for (int d = 0; d < D; ++d) e[u][d] = sv.e(d, su);
+        sv.load(su, dw[u], e[u]);
       }
       // P B0 and V0 of each j in W/2 16-byte loads from one packed record; all U records are
       // requested before the first is used (slots past the row end re-read a valid record)
