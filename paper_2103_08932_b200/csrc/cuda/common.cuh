@@ -97,6 +97,7 @@ struct DFields {
   double* B0[9];
   // per particle, packed for the momentum gather: P(F) B0 row-major (D x D), V0, padding to 16 B
   double* pbv;
+  double* v4;  // 3D bodies with the interleaved slot copy: (v, V0) records for pass C (k_pack_v4)
   double* V0;
   double* m;
   double* minvf;  // RN(1/m), negated for clamped particles (flag travels with the TMA-staged mass)
@@ -177,6 +178,11 @@ constexpr int kWarp = 32;
 // copy (DFields::odw holds 4 doubles per slot, oe0 unused); 0: four separate arrays (A/B)
 #ifndef TLSPH_TL_SLOTREC
 #define TLSPH_TL_SLOTREC 1
+#endif
+// 3D slot-order pass C gathers (v_j, V0_j) as one 32-byte record packed right before the pass
+// (tlsph.cu k_pack_v4); 0: three or four 64-bit gathers from the component arrays (A/B)
+#ifndef TLSPH_TL_V4
+#define TLSPH_TL_V4 1
 #endif
 // FAST particle-split chain on bank-spread slot rows (state.cu k_spread_rows, sweep_chain.cuh);
 // 0: rows in slot order (A/B)

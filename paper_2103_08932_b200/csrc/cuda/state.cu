@@ -746,6 +746,7 @@ DFields DevSystem::fields() const {
   }
   f.V0 = V0.p;
   f.pbv = pbv.p;
+  f.v4 = v4.p;
   f.m = m.p;
   f.minvf = minvf.p;
   f.cell_slot = cell_slot.p;
@@ -1119,6 +1120,7 @@ void DevSystem::build_ordered_rows() {
   ogbase.alloc(gb.size());
   CK(cudaMemcpyAsync(ogbase.p, gb.data(), gb.size() * sizeof(long long), cudaMemcpyHostToDevice, stream));
   onbr.alloc(total);
+  if (D == 3 && TLSPH_TL_V4) v4.alloc(4 * static_cast<size_t>(n));
   if (D == 3 && TLSPH_TL_SLOTREC) {
     odw.alloc(4 * total);  // (dW/dr0, e0) records
   } else {

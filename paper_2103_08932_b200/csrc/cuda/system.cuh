@@ -122,6 +122,7 @@ class DevSystem {
   DBuf<double> r0[3], r[3], v[3], a[3], body[3];
   DBuf<double> F[9], dFdt[9], B0[9];
   DBuf<double> pbv;   // packed P B0 + V0 per particle (common.cuh)
+  DBuf<double> v4;    // (v, V0) records of the 3D slot-order pass C (tlsph.cu k_pack_v4)
   DBuf<double> V0, m, minvf, rho0, rho;
   DBuf<long long> cell_slot;
   // per-sweep particle-split constants and the (eta, dt) they were formed for

@@ -195,9 +195,17 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        v0[u] = UV0 ? f.v0_uniform : f.V0[j[u]];
+        if constexpr (OI && D == 3 && TLSPH_TL_V4) {
+          // (v_j, V0_j) as one 32-byte record (k_pack_v4, launched before this pass): one 256-bit
+          // gather instead of three or four 64-bit ones
+          asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                       : "=d"(vj[u][0]), "=d"(vj[u][1]), "=d"(vj[u][2]), "=d"(v0[u])
+                       : "l"(f.v4 + 4 * static_cast<long long>(j[u])));
+        } else {
+          v0[u] = UV0 ? f.v0_uniform : f.V0[j[u]];
 #pragma unroll
-        for (int d = 0; d < D; ++d) vj[u][d] = f.v[d][j[u]];
+          for (int d = 0; d < D; ++d) vj[u][d] = f.v[d][j[u]];
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -247,6 +255,14 @@ __device__ __forceinline__ void deformation_rate_body(const DFields& f, DScalars
       for (int d = 0; d < D; ++d) f.r[d][i] = f.r[d][i] + half * f.v[d][i];
     }
   }
+}
+
+// (v, V0) of every particle as one 32-byte record for the 3D slot-order pass C's gathers; run
+// right before that pass (v is final then: pass B's kick, and in a slab the halo refresh).
+__global__ void k_pack_v4(DFields f) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= f.n) return;
+  *reinterpret_cast<double4*>(f.v4 + 4 * i) = make_double4(f.v[0][i], f.v[1][i], f.v[2][i], f.V0[i]);
 }
 
 template <int D, int G, bool POST, bool UV0 = false>
@@ -555,6 +571,7 @@ void DevSystem::deformation_rate() {
     else k_deformation_rate<2, 4, false><<<grid_for(n * 4, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
   } else {
     if (ord) {
+      if (f.onbr && TLSPH_TL_V4) k_pack_v4<<<grid_for(n, 256), 256, 0, stream>>>(f);
       if (f.onbr) k_deformation_rate_ordered<3, false, true><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
       else k_deformation_rate_ordered<3, false><<<grid_for(n, 128), 128, 0, stream>>>(f, scal.p, 0.0, 0);
     }
@@ -646,6 +663,7 @@ void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop
     }
     else if (pass == 1) launch_pdl(k_momentum<3, kGB3, true>, n * kGB3, st, f, s.scal.p, dt, loop);
     else if (ord) {
+      if (f.onbr && TLSPH_TL_V4) k_pack_v4<<<grid_for(n, 256), 256, 0, st>>>(f);
       if (f.onbr) k_deformation_rate_ordered<3, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
       else k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
     }
