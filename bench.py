@@ -549,7 +549,11 @@ def sharded_cfg5(args, ws, rank):
             "damped_steps": res["damped"],
             "sweep": {"metric": METRIC_DPU, "value": 2 * s_free * nsw / t_sw, "unit": "DPU/s",
                       "ms_per_sweep": t_sw / nsw * 1e3},
-            "gpu_launches": None, "clocks": clk.summary(),
+            "gpu_launches": res["kernel_launches"],  # rank 0's kernels over the timed K steps (lower bound)
+            "e2e": {"value": None, "unit": "PS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "the reference's operator API is a one-process, one-body interface (no slab form): "
+                            "its end-to-end figure is the N = 1 line's e2e"},
+            "clocks": clk.summary(),
             "timing": "CUDA events on each slab's stream between a barrier and the last step, max over ranks"}
 
 

@@ -347,6 +347,11 @@ tlsph_status tlsph_dev_group_run(tlsph_dev_group* g, const tlsph_dev_loop_params
     res->steps = p->max_steps;
     res->t = t;
     res->last_dt = dt;
+    // this rank's kernels, a lower bound: per step the reduction and passes A-C (3D: + the (v, V0)
+    // pack), per damped step the fold constants and the 2 x 3^D colour phases; halo pushes not counted
+    const uint64_t per_elastic = p->elastic ? (g->dim == 3 ? 4u : 3u) : 0u;
+    const uint64_t phases = g->dim == 3 ? 54u : 18u;
+    res->kernel_launches = p->max_steps * (1u + per_elastic) + res->damped_steps * (1u + phases);
   });
 }
 

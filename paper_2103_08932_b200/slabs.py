@@ -686,7 +686,7 @@ class CGroup:
         r = dev.LoopResult()
         self._check(dev.lib().tlsph_dev_group_run(self._h, C.byref(p), C.byref(r)))
         return {"steps": r.steps, "damped": r.damped_steps, "t": r.t, "last_dt": r.last_dt,
-                "device_s": r.total_seconds}
+                "device_s": r.total_seconds, "kernel_launches": int(r.kernel_launches)}
 
     def close(self):
         from . import dev
