@@ -44,7 +44,28 @@
 #define TLSPH_SWEEP_SPREAD 1
 #endif
 
+// A/B knob (measured, rejected: profiles/r2e_sweep_idle_lanes.md). Idle lanes (no slot in this
+// iteration, pair factor 0) gather particle i's own entry; with the knob on they gather the stencil
+// entry of lane 0 of their half-warp instead, so that the half-warp's 64-bit shared-memory request
+// carries no second address in i's bank pair. The shuffle per slot iteration that forms the index
+// costs more than the saved wavefronts: cfg2 0.636 -> 0.673 ms, cfg4 8.95 -> 9.88, cfg5-weak 15.9 -> 17.6.
+#ifndef TLSPH_SWEEP_IDLE_BCAST
+#define TLSPH_SWEEP_IDLE_BCAST 0
+#endif
+
 namespace tlsph_cuda {
+
+// Stencil index an idle lane gathers (its result is multiplied by b = 0 and never scattered).
+__device__ __forceinline__ int idle_lane_index(int j, bool idle, int lane) {
+#if TLSPH_SWEEP_IDLE_BCAST
+  const int j0 = __shfl_sync(0xffffffffu, j, lane & 16);
+  return idle ? j0 : j;
+#else
+  (void)idle;
+  (void)lane;
+  return j;
+#endif
+}
 
 // Slot of this lane in iteration u of a bank-spread row: half-warp h = lane / 16 reads group
 // g = 2u + h, positions [start_g, start_g+1) of the row. Header byte g = start_g (byte 0 = 0;
@@ -190,7 +211,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       int s;
       bool v;
       slot(hdr0, cnt, u, s, v);
-      const int jr = v ? t.nl[lo + s] : t.lbase + pk;  // invalid lanes read i itself with b = 0
+      const int jr = idle_lane_index(v ? t.nl[lo + s] : t.lbase + pk, !v, lane);  // invalid lanes: b = 0
       const int j = UNI ? (jr & 0x7fff) : jr;
       const double q = UNI ? ((v && !(jr & 0x8000)) ? t.pf[lo + s] * t.minv : 0.0) : (v ? t.qf[lo + s] : 0.0);
       const bool up = q != 0.0;                      // clamped j: never written (damping.cpp:84-86)
@@ -214,7 +235,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       int s;
       bool v;
       slot(hdr1, cnt1, u, s, v);
-      jn[u] = v ? t.nl[lo1 + s] : li1;
+      jn[u] = idle_lane_index(v ? t.nl[lo1 + s] : li1, !v, lane);
       pfn[u] = v ? t.pf[lo1 + s] : 0.0;
       if (!UNI) qfn[u] = v ? t.qf[lo1 + s] : 0.0;
     }
@@ -400,6 +421,8 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     double q0[K];
     row(pk, lo, cnt);
     load_raw(lo, cnt, header(pk), t.lbase + pk, r0);
+#pragma unroll
+    for (int u = 0; u < K; ++u) r0.j[u] = idle_lane_index(r0.j[u], r0.pf[u] == 0.0, lane);
     diag = t.diag[pk];
     y = t.y[pk];
     mass_factors(r0.j, r0.pf, q0);
@@ -410,6 +433,9 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
   // receives particle kk+3's.
   auto step = [&](int kk, RawSlots<K>& use, RawSlots<K>& fill) {
     const int li = t.lbase + pk;
+    // particle kk+1's idle lanes (pair factor 0: no slot, or a slot that contributes nothing)
+#pragma unroll
+    for (int u = 0; u < K; ++u) use.j[u] = idle_lane_index(use.j[u], use.pf[u] == 0.0, lane);
     load_raw(lo3, cnt3, hdr3, t.lbase + pk3, fill);
     const int pk4 = pclamp(kk + 4);
     int lo4, cnt4;
