@@ -141,8 +141,11 @@ __device__ __forceinline__ void warp_sum_vec(double (&x)[D], int lane) {
 // receives the group sum), then a three-level xor butterfly adds the eight group sums. Dependent
 // latency ~185 cycles against ~233 for the shuffle tree (tools/dmma_probe.cu); the summation order
 // differs (FAST class).
+// TLSPH_SWEEP_MMA_SUM: 0 = shuffle tree, 1 = one MMA + three butterfly levels, 2 (default) = two
+// MMAs and no shuffle (warp_sum_vec_mma2; same-box A/B against 1, ms per sweep: cfg2 0.636 -> 0.597,
+// cfg3 1.088 -> 1.070, cfg4 8.95 -> 8.65, cfg5-weak 15.89 -> 15.42; profiles/r2e_sweep_mma2.md).
 #ifndef TLSPH_SWEEP_MMA_SUM
-#define TLSPH_SWEEP_MMA_SUM 1
+#define TLSPH_SWEEP_MMA_SUM 2
 #endif
 template <int D>
 __device__ __forceinline__ void warp_sum_vec_mma(double (&x)[D]) {
@@ -163,9 +166,34 @@ __device__ __forceinline__ void warp_sum_vec_mma(double (&x)[D]) {
   for (int d = 0; d < D; ++d) x[d] = r[d];
 }
 
+// The whole sum by two MMAs and no shuffle (TLSPH_SWEEP_MMA_SUM=2). First MMA with A = ones and the
+// lanes' values as B (lane 4n+k supplies B[k][n]): D[m][n] = G_n, the sum of lane group n, and lane
+// 4r+k receives G_2k and G_2k+1; it adds them. Second MMA with those pair sums as A (lane 4r+k
+// supplies A[r][k]) and B = ones: D[r][n] = sum_k (G_2k + G_2k+1), the total, in every lane.
+template <int D>
+__device__ __forceinline__ void warp_sum_vec_mma2(double (&x)[D]) {
+  double p[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double c0, c1;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+                 : "=d"(c0), "=d"(c1)
+                 : "d"(1.0), "d"(x[d]), "d"(0.0), "d"(0.0));
+    p[d] = c0 + c1;
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double unused;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+                 : "=d"(x[d]), "=d"(unused)
+                 : "d"(p[d]), "d"(1.0), "d"(0.0), "d"(0.0));
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void chain_sum(double (&x)[D], int lane) {
-  if (TLSPH_SWEEP_MMA_SUM) warp_sum_vec_mma<D>(x);
+  if (TLSPH_SWEEP_MMA_SUM == 2) warp_sum_vec_mma2<D>(x);
+  else if (TLSPH_SWEEP_MMA_SUM) warp_sum_vec_mma<D>(x);
   else warp_sum_vec<D>(x, lane);
 }
 
