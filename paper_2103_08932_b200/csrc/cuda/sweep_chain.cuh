@@ -22,6 +22,12 @@
 // diagonal) or one without neighbours (damping.cpp:54, :151) runs the same
 // code with its writes disabled, so the loop has no data-dependent branch.
 #pragma once
+// TLSPH_CHAIN_NORATE (default 1): 1/denominator folded into the slot coefficients when they are
+// formed (c y and diag y), so the scatter is one FMA on the reduced residual, without the rate
+// product on the chain (another rounding of the FAST class; 0 = the former rate form).
+#ifndef TLSPH_CHAIN_NORATE
+#define TLSPH_CHAIN_NORATE 1
+#endif
 // Y of the FAST update (see below): v_j + bm (v_j - v_i) (default), or the former
 // (1 + bm) v_j - bm v_i (TLSPH_Y_FORM=2: not exact for uniform fields; A/B only)
 // streamed chain: Y formed at the scatter (1) or before the reduction (0)
@@ -247,9 +253,11 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       bq[u] = v ? t.kb * t.pf[lo + s] : 0.0;
       bmq[u] = t.kb * q;
       cq[u] = -bmq[u] * (diag + bq[u]);
+      if (TLSPH_CHAIN_NORATE) cq[u] *= y;
       upm |= up ? (1u << u) : 0u;
     }
     if (skip) upm = 0;
+    if (TLSPH_CHAIN_NORATE) diag *= y;
   }
 
   for (int kk = 0; kk < np; ++kk) {
@@ -298,7 +306,7 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
     if (SHUF) chain_sum<D>(P, lane);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const double rate = P[d] * y;
+      const double rate = TLSPH_CHAIN_NORATE ? P[d] : P[d] * y;
       if (SCATTER) {
 #pragma unroll
         for (int u = 0; u < K; ++u)
@@ -328,9 +336,11 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
       bq[u] = t.kb * pfn[u];
       bmq[u] = t.kb * qfn[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
+      if (TLSPH_CHAIN_NORATE) cq[u] *= y;
       upm |= up ? (1u << u) : 0u;
     }
     if (skip) upm = 0;
+    if (TLSPH_CHAIN_NORATE) diag *= y;
     pk = pk1;
     pk1 = pk2;
     lo1 = lo2;
@@ -353,11 +363,21 @@ __device__ __forceinline__ void fast_chain(const ChainTile<D>& t, int lane) {
 // cfg4 / cfg5-weak ms per sweep, default 9.64 / 17.98):
 // TLSPH_STREAM_ROTATE=0: the particle loop unrolled three times with the three raw buffers renamed
 //   statically instead of moved down the pipeline every iteration (fewer instructions, but
-//   10.11 / 19.05: three copies of the ~270-instruction body);
+//   10.11 / 19.05 then; the default since round 2e, see below);
 // TLSPH_STREAM_U32=1: slot addresses as 32-bit indices into the body's arrays, one widening
 //   multiply-add per load instead of 64-bit pointer sums (10.15 / 18.80).
+// TLSPH_STREAM_ROTATE (default 0): 1 = the streamed chain's raw-load buffers are moved down the
+// pipeline every iteration (18 register moves per particle); 0 = the particle loop is unrolled
+// three times with the buffers renamed statically. With the shuffle-free warp sum and the folded
+// rate the unrolled form wins (same-box A/B, profiles/r2e_sweep_chain_forms.md: cfg4 8.65 -> 7.90 ms
+// per sweep, cfg5-weak 15.42 -> 14.60); with the round-2c chain it lost (10.11 vs 9.64).
 #ifndef TLSPH_STREAM_ROTATE
-#define TLSPH_STREAM_ROTATE 1
+#define TLSPH_STREAM_ROTATE 0
+#endif
+// TLSPH_STREAM_DEPTH: raw slot loads issued this many particles ahead of the particle they belong to
+// (3: two whole iterations in flight, three register buffers; 2: one iteration, two buffers).
+#ifndef TLSPH_STREAM_DEPTH
+#define TLSPH_STREAM_DEPTH 3
 #endif
 #ifndef TLSPH_STREAM_U32
 #define TLSPH_STREAM_U32 0
@@ -426,24 +446,16 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
       bq[u] = t.kb * pf[u];
       bmq[u] = t.kb * q[u];
       cq[u] = -bmq[u] * (diag + bq[u]);
+      if (TLSPH_CHAIN_NORATE) cq[u] *= y;
       upm |= q[u] != 0.0 ? (1u << u) : 0u;
     }
     if (skip) upm = 0;
+    if (TLSPH_CHAIN_NORATE) diag *= y;
   };
 
-  // particle 0: coefficients; particles 1, 2: raw loads in flight; particle 3: row extents
-  int pk = pidx(0);
-  int pk1 = pclamp(1), pk2 = pclamp(2), pk3 = pclamp(3);
-  int lo1, cnt1, lo2, cnt2, lo3, cnt3;
-  RawSlots<K> ra, rb, rc;
-  row(pk1, lo1, cnt1);
-  row(pk2, lo2, cnt2);
-  row(pk3, lo3, cnt3);
   auto header = [&](int p) { return SPREAD ? t.hdr[p] : 0ull; };
-  unsigned long long hdr3 = header(pk3);
-  load_raw(lo1, cnt1, header(pk1), t.lbase + pk1, ra);
-  load_raw(lo2, cnt2, header(pk2), t.lbase + pk2, rb);
-  {
+  int pk = pidx(0);
+  auto first = [&] {  // particle 0: coefficients (after the next particles' loads are in flight)
     int lo, cnt;
     RawSlots<K> r0;
     double q0[K];
@@ -455,21 +467,16 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     y = t.y[pk];
     mass_factors(r0.j, r0.pf, q0);
     coefficients(r0.j, r0.pf, q0, cnt);
-  }
+  };
+  int pk1 = pclamp(1);
 
-  // One particle: `use` holds particle kk+1's raw slots (loaded two iterations ago), `fill`
-  // receives particle kk+3's.
-  auto step = [&](int kk, RawSlots<K>& use, RawSlots<K>& fill) {
+  // One particle of the chain (pk); `use` holds the raw slots of the next one (pk1, cnt_next slots),
+  // whose coefficients are formed after the scatter.
+  auto update = [&](RawSlots<K>& use, int cnt_next) {
     const int li = t.lbase + pk;
-    // particle kk+1's idle lanes (pair factor 0: no slot, or a slot that contributes nothing)
+    // the next particle's idle lanes (pair factor 0: no slot, or a slot that contributes nothing)
 #pragma unroll
     for (int u = 0; u < K; ++u) use.j[u] = idle_lane_index(use.j[u], use.pf[u] == 0.0, lane);
-    load_raw(lo3, cnt3, hdr3, t.lbase + pk3, fill);
-    const int pk4 = pclamp(kk + 4);
-    int lo4, cnt4;
-    row(pk4, lo4, cnt4);
-    hdr3 = header(pk4);
-
     // the chain: gathers
     double vi[D], vq[K][D];
 #pragma unroll
@@ -496,10 +503,10 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
 #endif
     chain_sum<D>(P, lane);
     double qfn[K];
-    mass_factors(use.j, use.pf, qfn);  // particle kk+1
+    mass_factors(use.j, use.pf, qfn);  // the next particle
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const double rate = P[d] * y;
+      const double rate = TLSPH_CHAIN_NORATE ? P[d] : P[d] * y;
 #pragma unroll
       for (int u = 0; u < K; ++u)
 #if TLSPH_Y_LATE
@@ -514,7 +521,71 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
 
     diag = diag1;
     y = y1;
-    coefficients(use.j, use.pf, qfn, cnt1);
+    coefficients(use.j, use.pf, qfn, cnt_next);
+  };
+
+#if TLSPH_STREAM_DEPTH == 2
+  // Raw loads one particle ahead of their use: particle 1 in flight; particle 2: row extents.
+  int pk2 = pclamp(2);
+  int lo1, cnt1, lo2, cnt2;
+  RawSlots<K> ra, rb;
+  row(pk1, lo1, cnt1);
+  row(pk2, lo2, cnt2);
+  unsigned long long hdr2 = header(pk2);
+  load_raw(lo1, cnt1, header(pk1), t.lbase + pk1, ra);
+  first();
+  // `use` holds particle kk+1's raw slots (loaded one iteration ago), `fill` receives particle kk+2's
+  auto step = [&](int kk, RawSlots<K>& use, RawSlots<K>& fill) {
+    load_raw(lo2, cnt2, hdr2, t.lbase + pk2, fill);
+    const int pk3 = pclamp(kk + 3);
+    int lo3, cnt3;
+    row(pk3, lo3, cnt3);
+    hdr2 = header(pk3);
+    update(use, cnt1);
+    pk = pk1;
+    pk1 = pk2;
+    pk2 = pk3;
+    cnt1 = cnt2;
+    lo2 = lo3;
+    cnt2 = cnt3;
+  };
+#if TLSPH_STREAM_ROTATE
+  for (int kk = 0; kk < np; ++kk) {
+    step(kk, ra, rb);
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      ra.j[u] = rb.j[u];
+      ra.pf[u] = rb.pf[u];
+    }
+  }
+#else
+  for (int kk = 0;;) {
+    step(kk, ra, rb);
+    if (++kk >= np) break;
+    step(kk, rb, ra);
+    if (++kk >= np) break;
+  }
+#endif
+#else
+  // Raw loads two particles ahead of their use: particles 1, 2 in flight; particle 3: row extents.
+  int pk2 = pclamp(2), pk3 = pclamp(3);
+  int lo1, cnt1, lo2, cnt2, lo3, cnt3;
+  RawSlots<K> ra, rb, rc;
+  row(pk1, lo1, cnt1);
+  row(pk2, lo2, cnt2);
+  row(pk3, lo3, cnt3);
+  unsigned long long hdr3 = header(pk3);
+  load_raw(lo1, cnt1, header(pk1), t.lbase + pk1, ra);
+  load_raw(lo2, cnt2, header(pk2), t.lbase + pk2, rb);
+  first();
+  // `use` holds particle kk+1's raw slots (loaded two iterations ago), `fill` receives particle kk+3's
+  auto step = [&](int kk, RawSlots<K>& use, RawSlots<K>& fill) {
+    load_raw(lo3, cnt3, hdr3, t.lbase + pk3, fill);
+    const int pk4 = pclamp(kk + 4);
+    int lo4, cnt4;
+    row(pk4, lo4, cnt4);
+    hdr3 = header(pk4);
+    update(use, cnt1);
     pk = pk1;
     pk1 = pk2;
     pk2 = pk3;
@@ -524,7 +595,6 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     lo3 = lo4;
     cnt3 = cnt4;
   };
-
 #if TLSPH_STREAM_ROTATE
   for (int kk = 0; kk < np; ++kk) {
     step(kk, ra, rc);
@@ -545,6 +615,7 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     step(kk, rc, rb);
     if (++kk >= np) break;
   }
+#endif
 #endif
 }
 
