@@ -488,12 +488,15 @@ __host__ __device__ __forceinline__ long long pbv_at(long long n, long long p, i
 __device__ __forceinline__ void pbv_gather3(const double* __restrict__ pbv, long long n, long long j, double* rec) {
   const double* q0 = pbv + 4 * j;
   const double* q1 = pbv + 4 * (n + j);
-  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(rec[0]), "=d"(rec[1]), "=d"(rec[2]), "=d"(rec[3])
-               : "l"(q0));
-  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(rec[4]), "=d"(rec[5]), "=d"(rec[6]), "=d"(rec[7])
-               : "l"(q1));
+  // TLSPH_TL_GATHER_HINT=1 (A/B): the gathered records kept in L1 with evict_last priority
+#if defined(TLSPH_TL_GATHER_HINT) && TLSPH_TL_GATHER_HINT == 1
+#define TLSPH_PBV_LD "ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+#else
+#define TLSPH_PBV_LD "ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+#endif
+  asm volatile(TLSPH_PBV_LD : "=d"(rec[0]), "=d"(rec[1]), "=d"(rec[2]), "=d"(rec[3]) : "l"(q0));
+  asm volatile(TLSPH_PBV_LD : "=d"(rec[4]), "=d"(rec[5]), "=d"(rec[6]), "=d"(rec[7]) : "l"(q1));
+#undef TLSPH_PBV_LD
   const double2 x = __ldg(reinterpret_cast<const double2*>(pbv + 8 * n + 2 * j));
   rec[8] = x.x;
   rec[9] = x.y;

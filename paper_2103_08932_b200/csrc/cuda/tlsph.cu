@@ -112,6 +112,9 @@ template <int D, int G, bool OI = false>
 #ifndef TLSPH_TL_STREAM_HINT
 #define TLSPH_TL_STREAM_HINT 0
 #endif
+#ifndef TLSPH_TL_SLOTREC_HINT
+#define TLSPH_TL_SLOTREC_HINT 0
+#endif
 struct SlotView {
   const int* nbr;
   const double* dw;
@@ -144,7 +147,16 @@ struct SlotView {
   // in the interleaved copy (build_ordered_rows), one 256-bit load instead of four 64-bit loads.
   __device__ __forceinline__ void load(long long su, double& dwv, double (&ev)[D]) const {
     if constexpr (OI && D == 3 && TLSPH_TL_SLOTREC) {
+      // TLSPH_TL_SLOTREC_HINT (A/B): 1 = L1::no_allocate, 2 = + L2::evict_first, 3 = L1::evict_first
+#if TLSPH_TL_SLOTREC_HINT == 1
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+#elif TLSPH_TL_SLOTREC_HINT == 2
+      asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+#elif TLSPH_TL_SLOTREC_HINT == 3
+      asm volatile("ld.global.nc.L1::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+#else
       asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+#endif
                    : "=d"(dwv), "=d"(ev[0]), "=d"(ev[1]), "=d"(ev[2])
                    : "l"(dw + 4 * su));
     } else {
