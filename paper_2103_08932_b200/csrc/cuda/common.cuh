@@ -110,6 +110,13 @@ struct DFields {
   // regrouped for conflict-free half-warp gathers; ghdr[i] = the row's group starts (k_spread_rows)
   const double* pfsp;
   const unsigned long long* ghdr;
+  // dense rows (large bodies, build_spread_rows): the bank-spread rows again, each padded to
+  // dense_r = 32 K slots (group g at 16 g; padding: pair factor 0, the group's first stencil index),
+  // so lane l of iteration u reads slot 32 u + l of row i at i * dense_r with no header decode and
+  // no predicate; null when not built
+  const uint16_t* nld;
+  const double* pfd;
+  int dense_r;
   double minv_uniform;
   double v0_uniform;  // every V0 equal: that value (the FAST dF/dt pass skips the V0_j gather); 0 otherwise
   // x-slab peers (slabs.py): per particle of a column shared with a neighbouring slab, the

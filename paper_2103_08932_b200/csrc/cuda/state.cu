@@ -520,6 +520,34 @@ __global__ void k_spread_rows(const long long* __restrict__ offs, const uint16_t
   }
 }
 
+// Dense copy of the bank-spread rows for the streamed FAST chain: row i at i * R (R = 16 * groups),
+// group g at 16 g. Padding slots carry pair factor 0 (they add nothing and are never written) and
+// the stencil index of their group's first slot (a broadcast in the half-warp's gather: no extra
+// bank-pair wavefront); an empty group borrows the row's first slot, an empty row index 0.
+__global__ void k_dense_rows(const long long* __restrict__ offs, const uint16_t* __restrict__ nlocf,
+                             const double* __restrict__ pfsp, const unsigned long long* __restrict__ ghdr,
+                             int groups, uint16_t* __restrict__ nld, double* __restrict__ pfd, long long n) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long lo = offs[i];
+  const int cnt = static_cast<int>(offs[i + 1] - lo);
+  const unsigned long long hdr = ghdr[i];
+  const int R = 16 * groups;
+  const long long base = i * R;
+  const uint16_t row_first = cnt > 0 ? static_cast<uint16_t>(nlocf[lo] & 0x7fffu) : static_cast<uint16_t>(0);
+  for (int g = 0; g < groups; ++g) {
+    const int st = g == 0 ? 0 : static_cast<int>((hdr >> (8 * g)) & 0xffu);
+    const int en = g + 1 < 8 ? static_cast<int>((hdr >> (8 * (g + 1))) & 0xffu) : cnt;
+    const int end = g + 1 < groups ? en : cnt;  // the last group ends the row
+    const uint16_t fill = end > st ? static_cast<uint16_t>(nlocf[lo + st] & 0x7fffu) : row_first;
+    for (int k = 0; k < 16; ++k) {
+      const bool v = st + k < end;
+      nld[base + 16 * g + k] = v ? nlocf[lo + st + k] : fill;
+      pfd[base + 16 * g + k] = v ? pfsp[lo + st + k] : 0.0;
+    }
+  }
+}
+
 // Rows re-ordered by ascending neighbour index (distinct within a row): one warp per row, each
 // slot's destination is its rank in the row.
 template <int D>
@@ -784,6 +812,9 @@ DFields DevSystem::fields() const {
   f.nlocf = uniform_mass ? nlocf.p : nullptr;
   f.pfsp = pfsp.p;
   f.ghdr = ghdr.p;
+  f.nld = uniform_mass && dense_r > 0 ? nld.p : nullptr;
+  f.pfd = pfd.p;
+  f.dense_r = dense_r;
   f.minv_uniform = minv_uniform;
   f.v0_uniform = v0_uniform;
   f.cell_start = cell_start.p;
@@ -1027,6 +1058,28 @@ void DevSystem::build_spread_rows() {
   k_spread_rows<<<grid_for(n, 128), 128, 0, stream>>>(offs.p, nloc.p, nbr.p, flag.p, pf.p, 2 * K, nlocf.p, pfsp.p,
                                                       ghdr.p, n);
   CK_LAUNCH("k_spread_rows");
+  // Dense rows for the streamed chain, opt-in (TLSPH_SWEEP_DENSE=1; measured slower than the
+  // header-decoded rows: cfg4 8.28 vs 7.72 ms per sweep, cfg5-weak 14.60 vs 14.30,
+  // profiles/r2e_sweep_chain_forms.md), when the device has the room (10 B per padded slot).
+  static const int dense_mode = [] {
+    const char* e = std::getenv("TLSPH_SWEEP_DENSE");
+    return e && *e ? std::atoi(e) : 0;
+  }();
+  dense_r = 0;
+  const bool want = dense_mode != 0;
+  if (want) {
+    const size_t R = static_cast<size_t>(32 * K), need = static_cast<size_t>(n) * R * 10;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t have = (nld.p ? static_cast<size_t>(n) * R * 10 : 0) + free_b;  // a rebuild reuses its buffers
+    if (have > need + (size_t(8) << 30)) {
+      nld.alloc(static_cast<size_t>(n) * R);
+      pfd.alloc(static_cast<size_t>(n) * R);
+      k_dense_rows<<<grid_for(n, 128), 128, 0, stream>>>(offs.p, nlocf.p, pfsp.p, ghdr.p, 2 * K, nld.p, pfd.p, n);
+      CK_LAUNCH("k_dense_rows");
+      dense_r = static_cast<int>(R);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ per-step re-sort (BASELINE cfg4)

@@ -718,10 +718,14 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   stamp(blockIdx.x, 2);
   constexpr bool SPREAD = UNI && TLSPH_SWEEP_SPREAD;  // bank-spread slot rows (state.cu k_spread_rows)
   const double* const pf_rows = SPREAD ? f.pfsp : f.pf;
+  // dense rows (large bodies): the streamed chain reads row p at p * dense_r; the staging call below
+  // then prefetches that block (its slot range is only used for the L2 prefetch when nothing is staged)
+  const bool dense = STREAM && SPREAD && f.nld != nullptr;
+  const CellSpan cst = dense ? CellSpan{cs.p0, cs.p1, cs.p0 * f.dense_r, cs.p1 * f.dense_r} : cs;
   // bulk row copies for the streamed (large-body) form only: with a handful of cells per SM the
   // serialised bulk issue costs the latency-bound chain more than it saves (cfg2 0.635 -> 0.684 ms)
   issue_staging<D, true, false, PDL, !STREAM || UNI, !STREAM, UNI, SPREAD, STREAM && TLSPH_SWEEP_TROWS>(
-      f, t, cs, sstart, send, lane, UNI ? f.nlocf : f.nloc, pf_rows);
+      f, t, cst, sstart, send, lane, dense ? f.nld : UNI ? f.nlocf : f.nloc, dense ? f.pfd : pf_rows);
   stamp(blockIdx.x, 4);
   wait_staging(t);
   __syncwarp();
@@ -738,6 +742,10 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
     ct.qf = nullptr;  // formed from 1/m (fast_chain_stream)
     ct.nl = (UNI ? f.nlocf : f.nloc) + cs.s0;
     ct.minv = f.minv_uniform;
+    if (dense) {
+      ct.pf = f.pfd + cs.p0 * f.dense_r;
+      ct.nl = f.nld + cs.p0 * f.dense_r;
+    }
   } else {
     ct.pf = t.spf + (cs.s0 - cs.f0());
     ct.qf = UNI ? nullptr : t.sqf + (cs.s0 - cs.f0());
@@ -753,7 +761,8 @@ __device__ __forceinline__ void fast_task(const DFields& f, const Phase& ph, lon
   ct.np = static_cast<int>(cs.p1 - cs.p0);
   ct.forward = ph.forward;
   ct.kb = kb;
-  if (STREAM) fast_chain_stream<D, K, UNI, SPREAD>(ct, lane);
+  if (STREAM && SPREAD && dense) fast_chain_stream<D, K, UNI, SPREAD, STREAM && SPREAD>(ct, lane);
+  else if (STREAM) fast_chain_stream<D, K, UNI, SPREAD>(ct, lane);
   else fast_chain<D, K, true, true, UNI, SPREAD>(ct, lane);
   __syncwarp();
   stamp(blockIdx.x, 6);

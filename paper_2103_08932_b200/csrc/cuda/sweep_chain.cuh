@@ -388,17 +388,33 @@ struct RawSlots {
   double pf[K];  // pair factor
 };
 
-template <int D, int K, bool UNI, bool SPREAD = false>
+// DENSE (with UNI, SPREAD): t.nl / t.pf point at the cell's dense rows (state.cu k_dense_rows), R =
+// 32 K slots per particle; lane l of iteration u owns slot 32 u + l of every row, the padding has
+// pair factor 0. No row extents, group headers or load predicates.
+template <int D, int K, bool UNI, bool SPREAD = false, bool DENSE = false>
 __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lane) {
   const int np = t.np;
   auto pidx = [&](int kk) { return t.forward ? kk : np - 1 - kk; };
   auto pclamp = [&](int kk) { return pidx(kk < np ? kk : np - 1); };
   auto row = [&](int p, int& lo, int& cnt) {
+    if (DENSE) {
+      lo = p * (32 * K);
+      cnt = 32 * K;
+      return;
+    }
     lo = static_cast<int>(t.offs[p] - t.s0);
     cnt = static_cast<int>(t.offs[p + 1] - t.s0) - lo;
   };
   // raw loads; UNI: j keeps bit 15 (clamped j) until mass_factors / coefficients strip it
   auto load_raw = [&](int lo, int cnt, unsigned long long hdr, int li, RawSlots<K>& r) {
+    if (DENSE) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        r.j[u] = static_cast<int>(t.nl[lo + lane + 32 * u]);
+        r.pf[u] = t.pf[lo + lane + 32 * u];
+      }
+      return;
+    }
 #pragma unroll
     for (int u = 0; u < K; ++u) {
       int s;
@@ -453,7 +469,7 @@ __device__ __forceinline__ void fast_chain_stream(const ChainTile<D>& t, int lan
     if (TLSPH_CHAIN_NORATE) diag *= y;
   };
 
-  auto header = [&](int p) { return SPREAD ? t.hdr[p] : 0ull; };
+  auto header = [&](int p) { return SPREAD && !DENSE ? t.hdr[p] : 0ull; };
   int pk = pidx(0);
   auto first = [&] {  // particle 0: coefficients (after the next particles' loads are in flight)
     int lo, cnt;

@@ -170,6 +170,9 @@ class DevSystem {
   DBuf<uint16_t> nlocf;       // uniform masses: nloc | 0x8000 for clamped j (refresh_minvf)
   DBuf<double> pfsp;          // bank-spread rows: pf in the order of nlocf's regrouped rows
   DBuf<unsigned long long> ghdr;  // ... and each row's group starts (k_spread_rows)
+  DBuf<uint16_t> nld;         // dense rows (k_dense_rows): n x dense_r stencil indices ...
+  DBuf<double> pfd;           // ... and pair factors; large bodies only
+  int dense_r = 0;            // 32 K, 0: not built
   bool uniform_mass = false;  // every particle has the same mass
   double minv_uniform = 0.0;  // RN(1/m) then
   double v0_uniform = 0.0;    // every V0 equal (> 0): that value; 0 otherwise (refresh_v0_uniform)
