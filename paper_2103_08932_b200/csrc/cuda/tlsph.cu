@@ -372,8 +372,11 @@ __global__ void k_stress(DFields f, DScalars* sc, DMaterial mat, double dt, int 
 // momentum_rhs's last steps for particle i from its neighbour sum acc (integrator.cpp:111-115):
 // a = acc / m + ExternalAccel::eval (forces.hpp:34-38: body[i], + the contact plane at the current
 // position); with KICK the loop's fused kick v += dt a and the constraints.
-template <int D, bool KICK>
-__device__ __forceinline__ void momentum_finish(const DFields& f, long long i, const double (&acc)[D], double dt) {
+// PACK (3D, with KICK): also writes the particle's (v, V0) record for pass C's gathers (k_pack_v4's
+// work, when pass C follows on the same stream with nothing touching v in between).
+template <int D, bool KICK, bool PACK = false>
+__device__ __forceinline__ void momentum_finish(const DFields& f, long long i, const double (&acc)[D], double dt,
+                                                double v0i = 0.0) {
   const double mi = f.m[i];
   // ExternalAccel::eval (forces.hpp:34-38): body[i] (+ contact plane at the current position)
   double ext[D];
@@ -394,20 +397,27 @@ __device__ __forceinline__ void momentum_finish(const DFields& f, long long i, c
     f.a[d][i] = a[d];
   }
   if (KICK) {
+    double vn[D];
     if (f.flag[i]) {
 #pragma unroll
       for (int d = 0; d < D; ++d) {
+        vn[d] = 0.0;
         f.v[d][i] = 0.0;
         f.r[d][i] = f.r0[d][i];
       }
     } else {
 #pragma unroll
-      for (int d = 0; d < D; ++d) f.v[d][i] = f.v[d][i] + dt * a[d];
+      for (int d = 0; d < D; ++d) {
+        vn[d] = f.v[d][i] + dt * a[d];
+        f.v[d][i] = vn[d];
+      }
     }
+    if constexpr (PACK && D == 3)
+      *reinterpret_cast<double4*>(f.v4 + 4 * i) = make_double4(vn[0], vn[1], vn[2], v0i);
   }
 }
 
-template <int D, int G, int U, bool KICK, bool OI = false>
+template <int D, int G, int U, bool KICK, bool OI = false, bool PACK = false>
 __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, double dt_arg, int loop) {
   if (TLSPH_TL_PDL && G > 1) {
     grid_launch_dependents();  // pass C may launch and wait
@@ -484,16 +494,17 @@ __device__ __forceinline__ void momentum_body(const DFields& f, DScalars* sc, do
     for (int d = 0; d < D; ++d) acc[d] = group_sum_fast<G>(acc[d]);
   }
   if (!active || l != 0) return;
-  momentum_finish<D, KICK>(f, i, acc, dt);
+  if constexpr (PACK) momentum_finish<D, KICK, true>(f, i, acc, dt, f.V0[i]);
+  else momentum_finish<D, KICK>(f, i, acc, dt);
 }
 
 template <int D, int G, bool KICK>
 __global__ void TL_BOUNDS_B k_momentum(DFields f, DScalars* sc, double dt_arg, int loop) {
   momentum_body<D, G, TLSPH_TL_UB, KICK>(f, sc, dt_arg, loop);
 }
-template <int D, bool KICK, bool OI = false>
+template <int D, bool KICK, bool OI = false, bool PACK = false>
 __global__ void TL_BOUNDS_O k_momentum_ordered(DFields f, DScalars* sc, double dt_arg, int loop) {
-  momentum_body<D, 1, OI ? TLSPH_TL_OU : 1, KICK, OI>(f, sc, dt_arg, loop);
+  momentum_body<D, 1, OI ? TLSPH_TL_OU : 1, KICK, OI, PACK>(f, sc, dt_arg, loop);
 }
 
 template <int D>
@@ -643,8 +654,15 @@ void launch_pdl(void (*kernel)(KArgs...), long long threads, cudaStream_t st, Ar
   CK(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop, int pass) {
+// fused: the three passes are enqueued back to back on an undivided body (enqueue_verlet): pass B
+// writes pass C's (v, V0) records itself (TLSPH_TL_PACK_IN_B) and k_pack_v4 is not launched; the
+// per-pass entry of the x-slab driver refreshes halo velocities between B and C and packs after that.
+#ifndef TLSPH_TL_PACK_IN_B
+#define TLSPH_TL_PACK_IN_B 1
+#endif
+void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop, int pass, bool fused = false) {
   DFields f = s.fields();
+  const bool pack_in_b = fused && TLSPH_TL_PACK_IN_B && TLSPH_TL_V4 && f.onbr && !f.own && s.D == 3;
   const long long n = s.n;
   // large bodies (group-interleaved slot copy present): both modes run the slot-order one-thread
   // kernels (build_ordered_rows, state.cu); TLSPH_TL_EIGHT_LANES=1 keeps FAST on eight lanes (A/B)
@@ -670,12 +688,13 @@ void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop
   } else {
     if (pass == 0) k_stress<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, mat, dt, loop);
     else if (pass == 1 && ord) {
-      if (f.onbr) k_momentum_ordered<3, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      if (pack_in_b) k_momentum_ordered<3, true, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
+      else if (f.onbr) k_momentum_ordered<3, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
       else k_momentum_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
     }
     else if (pass == 1) launch_pdl(k_momentum<3, kGB3, true>, n * kGB3, st, f, s.scal.p, dt, loop);
     else if (ord) {
-      if (f.onbr && TLSPH_TL_V4) k_pack_v4<<<grid_for(n, 256), 256, 0, st>>>(f);
+      if (f.onbr && TLSPH_TL_V4 && !pack_in_b) k_pack_v4<<<grid_for(n, 256), 256, 0, st>>>(f);
       if (f.onbr) k_deformation_rate_ordered<3, true, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
       else k_deformation_rate_ordered<3, true><<<grid_for(n, 128), 128, 0, st>>>(f, s.scal.p, dt, loop);
     }
@@ -687,7 +706,7 @@ void enqueue_verlet_pass(DevSystem& s, const DMaterial& mat, double dt, int loop
 
 // Enqueues the three verlet passes on the handle's stream (no sync).
 void enqueue_verlet(DevSystem& s, const DMaterial& mat, double dt, int loop) {
-  for (int pass = 0; pass < 3; ++pass) enqueue_verlet_pass(s, mat, dt, loop, pass);
+  for (int pass = 0; pass < 3; ++pass) enqueue_verlet_pass(s, mat, dt, loop, pass, true);
   CK_LAUNCH("verlet passes");
 }
 
