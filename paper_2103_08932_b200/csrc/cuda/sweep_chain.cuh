@@ -7,7 +7,10 @@
 // D velocity components. Reassociated update (FAST tolerance class): with
 // w = v_j - v_i, Y = v_j + bm w and C = -bm (diag + b),
 //   v_j' = v_j - bm (v_i + diag rate - (v_j - b rate)) = Y + C rate,
-// so one FMA per slot follows the residual reduction on the chain. Y is formed from w (not as
+// so one FMA per slot follows the residual reduction on the chain (rate = residual * y with
+// y = RN(1 / denominator); TLSPH_CHAIN_NORATE folds y into C and diag when they are formed, so the
+// FMA acts on the reduced residual itself). The D residuals are summed over the warp by two fp64
+// MMAs per component and no shuffle (warp_sum_vec_mma2). Y is formed from w (not as
 // (1 + bm) v_j - bm v_i): a uniform velocity field (w = 0, rate = 0) is left exactly unchanged, as
 // in the reference's order -- the sweep amplifies any non-uniformity when eta~ dt is large (the
 // falling-ball case), so FAST must not create one.
