@@ -791,8 +791,18 @@ __device__ __forceinline__ void cell_coords(const DFields& f, long long lin, int
 // more cells share an SM -- the form for colours with more cells than one
 // wave of staged tiles holds (large bodies).
 // UNI (with STREAM, uniform masses): no stencil 1/m staged (fast_chain_stream).
+// TLSPH_SWEEP_FAST_MINB (A/B): minimum resident one-warp CTAs per SM (a register bound of
+// 65536 / (32 MINB)); 0: the compiler's choice
+#ifndef TLSPH_SWEEP_FAST_MINB
+#define TLSPH_SWEEP_FAST_MINB 0
+#endif
+#if TLSPH_SWEEP_FAST_MINB > 0
+#define SWEEP_FAST_BOUNDS __launch_bounds__(kWarp, TLSPH_SWEEP_FAST_MINB)
+#else
+#define SWEEP_FAST_BOUNDS __launch_bounds__(kWarp)
+#endif
 template <int D, int K, bool STREAM, bool UNI>
-__global__ void __launch_bounds__(kWarp)
+__global__ void SWEEP_FAST_BOUNDS
 k_sweep_fast(DFields f, Phase ph, const DScalars* __restrict__ sc) {
   if (ph.dt_from_scalars && sc->halt) return;
   extern __shared__ __align__(16) unsigned char smem[];
