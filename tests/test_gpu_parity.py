@@ -538,6 +538,23 @@ def test_sweep_tiling_staged_equals_streamed(case, mode):
     assert np.array_equal(out["staged"], out["streamed"])
 
 
+def test_dense_rows_of_the_streamed_chain_in_a_subprocess():
+    """The opt-in dense rows of the streamed FAST chain (TLSPH_SWEEP_DENSE=1: every bank-spread row
+    padded to 32 K slots, state.cu k_dense_rows) give the staged form's results bit for bit. The knob is
+    read once per process, so the staged-vs-streamed cases above run again in a child with it set."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, TLSPH_SWEEP_DENSE="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_parity.py"), "-m", "gpu",
+                        "-q", "-x", "-k", "staged_equals_streamed and fast"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 def blocking_bodies():
     rng = np.random.RandomState(11)
     base3 = lattice_r0([100, 8, 7], 0.01)
