@@ -653,6 +653,12 @@ def main():
                     out["e2e"] = {"value": e["value"], "unit": "PS/s", "h2d_bytes_per_step": e["h2d_bytes_per_step"],
                                   "d2h_bytes_per_step": e["d2h_bytes_per_step"], "path": e["api"],
                                   "host_memory": e.get("host_memory"),
+                                  "ms_per_step": e["seconds"] / max(args.steps, 1) * 1e3,
+                                  "caller_host_ms_per_step": (e.get("caller_host_seconds", 0.0) /
+                                                              max(args.steps, 1) * 1e3),
+                                  "caller_host_note": "the reference runner's own serial host code inside the "
+                                                      "timed loop (check_finite, runner.cpp:233-247; "
+                                                      "apply_constraints), not part of the operator API",
                                   "window": f"steps {args.warmup}..{args.warmup + args.steps - 1}",
                                   "damped_steps": e["damped_steps"]}
                 except Exception as exc:
